@@ -1,0 +1,162 @@
+/*
+ * dxpbd.h -- C ABI of the B200-native DiffXPBD hot path
+ * (arXiv 2301.01396, "DiffXPBD: Differentiable Position-Based Simulation of
+ * Compliant Constraint Dynamics"; line numbers below refer to PAPER.md).
+ *
+ * One handle = one scene (a mesh or a batch of disjoint meshes) resident on one
+ * CUDA device.  All compute runs in hand-written sm_100a kernels on the stream
+ * passed to each call (NULL = legacy default stream).  No torch types, no CPU
+ * fallback: a call that cannot run on the device returns an error code.
+ *
+ * Layouts: vectors of vertices are row-major [V][3] float32 (x, y, z).  Per-frame
+ * arrays are [frames][V][3].  Index buffers are int32.  Unless a call says
+ * otherwise, pointers are HOST or DEVICE according to its `mem` argument
+ * (DXPBD_MEM_HOST / DXPBD_MEM_DEVICE); device pointers must be on the scene's
+ * device and 4-byte aligned.  The library copies every input it keeps; the
+ * caller owns all pointers it passes.
+ *
+ * Errors: every call returns DXPBD_OK (0) or a positive error code;
+ * dxpbd_last_error() returns a thread-local message for the last failure.  On a
+ * CUDA error the scene is left in an unspecified state and must be destroyed.
+ */
+#ifndef DXPBD_H
+#define DXPBD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DXPBD_OK 0
+#define DXPBD_ERR_ARG 1      /* invalid argument (null pointer, size, index range) */
+#define DXPBD_ERR_CUDA 2     /* CUDA runtime error (message has the CUDA string)    */
+#define DXPBD_ERR_STATE 3    /* call out of order (e.g. backward before forward)    */
+#define DXPBD_ERR_OOM 4      /* device allocation failed                            */
+#define DXPBD_ERR_SOLVE 5    /* PCG did not reach the tolerance within max_iter     */
+#define DXPBD_ERR_LIMIT 6    /* more than 256 colors, or a capacity exceeded        */
+
+#define DXPBD_MEM_HOST 0
+#define DXPBD_MEM_DEVICE 1
+
+/* gradient families (dxpbd_grads kind, dxpbd_scene_desc.grad_flags bit = 1 << kind) */
+#define DXPBD_GRAD_COMPLIANCE 0   /* d phi / d alpha_j, [E] user constraint order            */
+#define DXPBD_GRAD_X0 1           /* d phi / d x_0,     [V][3]                                */
+#define DXPBD_GRAD_V0 2           /* d phi / d v_0,     [V][3]                                */
+#define DXPBD_GRAD_FORCES 3       /* d phi / d f_frame, [frames][V][3]                        */
+#define DXPBD_GRAD_SHAPE 4        /* d phi / d beta,    [num_shape] capsule shape coefficients*/
+#define DXPBD_GRAD_SPHERE 5       /* d phi / d (c_x, c_y, c_z, r), [S][4]                     */
+#define DXPBD_GRAD_MATERIAL 6     /* d phi / d (a, b) per tet, [T][2]  (mu = a^2, lambda = b^2)*/
+#define DXPBD_NUM_GRADS 7
+
+/* parameter families for dxpbd_set_params */
+#define DXPBD_PARAM_COMPLIANCE 0  /* alpha per distance constraint [E]                       */
+#define DXPBD_PARAM_SHAPE 1       /* capsule shape coefficients beta [num_shape]             */
+#define DXPBD_PARAM_MATERIAL 2    /* (a, b) per tet [T][2]                                   */
+#define DXPBD_PARAM_SPHERES 3     /* spheres [S][4]                                          */
+
+typedef struct dxpbd_scene dxpbd_scene;
+
+/* Scene description for dxpbd_create.  ALL pointers are HOST pointers (copied). */
+typedef struct dxpbd_scene_desc {
+    int32_t num_vertices;            /* V >= 1                                              */
+    const float *x_rest;             /* [V][3] rest positions: rest lengths, Dm^-1, volumes */
+    const float *inv_mass;           /* [V] 1/kg; 0 = pinned (PAPER.md l.161 infinite mass)  */
+
+    /* distance constraints C = |x_a - x_b| - L, L from x_rest (cloth stretch/shear/bend)  */
+    int32_t num_dist;                /* E >= 0                                              */
+    const int32_t *dist_idx;         /* [E][2] vertex ids, distinct, < V                     */
+    const float *dist_compliance;    /* [E] alpha >= 0 (PAPER.md Eq. xpbdUenergy l.76)      */
+
+    /* stable Neo-Hookean tets (Sec.5.2 l.229; R6)                        */
+    int32_t num_tets;                /* T >= 0                                              */
+    const int32_t *tet_idx;          /* [T][4] vertex ids, positive rest orientation        */
+    const float *tet_a;              /* [T] a, mu = a^2                                     */
+    const float *tet_b;              /* [T] b, lambda = b^2                                 */
+
+    /* analytic colliders (Sec.4.5 l.209, Sec.5.3; R7)                    */
+    int32_t num_spheres;             /* S >= 0                                              */
+    const float *spheres;            /* [S][4] center xyz, radius                           */
+    int32_t num_capsules;            /* K >= 0                                              */
+    const float *cap_center;         /* [K][3]                                              */
+    const float *cap_axis;           /* [K][3] unit axis                                    */
+    const float *cap_r0;             /* [K] radius at beta = 0                              */
+    const float *cap_L0;             /* [K] segment length at beta = 0                      */
+    int32_t num_shape;               /* NS >= 0                                             */
+    const float *cap_rbasis;         /* [K][NS] d r_k / d beta                              */
+    const float *cap_lbasis;         /* [K][NS] d L_k / d beta                              */
+    const float *shape_beta;         /* [NS] initial shape coefficients                     */
+
+    float gravity[3];                /* m/s^2, applied to free vertices (R2)               */
+    float frame_dt;                  /* s per frame                                         */
+    int32_t substeps;                /* substeps per frame, dt = frame_dt / substeps        */
+    int32_t iterations;              /* Gauss-Seidel iterations per substep (K >= 1)        */
+    float thickness;                 /* collision thickness h (m)                           */
+    float collision_compliance;      /* alpha of contact constraints                        */
+
+    int32_t max_frames;              /* checkpoint capacity (frames) for forward/backward   */
+    uint32_t grad_flags;             /* OR of (1 << DXPBD_GRAD_*) to accumulate             */
+    int32_t pd_projection;           /* 1 = project derivative blocks (Sec.4.3.2), 0 = off  */
+    float cg_tol;                    /* relative residual of the filtered PCG (e.g. 1e-6)   */
+    int32_t cg_max_iter;             /* PCG iteration cap per substep                       */
+    int32_t device;                  /* CUDA device ordinal                                 */
+} dxpbd_scene_desc;
+
+/* Build the device-resident scene: uploads topology and parameters, computes rest
+ * quantities, greedy-colors the constraints (R1) and sorts them by color.
+ * Cost: O(E + T) host work once.  On success *out receives the handle. */
+int dxpbd_create(const dxpbd_scene_desc *desc, dxpbd_scene **out);
+
+/* Free all device and host memory of the scene.  NULL is a no-op. */
+int dxpbd_destroy(dxpbd_scene *scene);
+
+/* Forward simulation (Sec.3.1, Eqs. xpbd l.81, position update l.85,
+ * xpbdUpdateRule l.88-96): num_frames * substeps XPBD substeps from x0, v0 with
+ * per-frame external forces (NULL = none), checkpointing x_n of every substep for
+ * the backward pass (R9).  x0, v0: [V][3]; forces: [num_frames][V][3] (N). */
+int dxpbd_forward(dxpbd_scene *scene, const float *x0, const float *v0, const float *forces,
+                  int32_t num_frames, int32_t mem, void *stream);
+
+/* Positions at the end of `frame` (0 = x0) of the last forward: out [V][3]. */
+int dxpbd_positions(dxpbd_scene *scene, int32_t frame, float *out, int32_t mem, void *stream);
+
+/* Adjoint pass (Sec.4.1-4.4, Eqs. rawAdjoint/adjointXPBD/gradientRule;
+ * DESIGN.md R3-R11) over the last forward trajectory for the keyframe goal
+ * phi = 1/2 sum_k sum_v W_v |x(frame k) - target_k|^2.
+ * key_frames: HOST [num_keys] in 0..num_frames; targets: [num_keys][V][3];
+ * weights: [V] or NULL (= 1).  Writes phi to *loss_out (HOST, may be NULL).  Gradients
+ * of the families in grad_flags are recomputed from zero (read with dxpbd_grads). */
+int dxpbd_backward(dxpbd_scene *scene, int32_t num_keys, const int32_t *key_frames,
+                   const float *targets, const float *weights, int32_t mem, float *loss_out,
+                   void *stream);
+
+/* Copy one gradient family (DXPBD_GRAD_*) of the last backward into out (out_len
+ * floats, must equal the family's size). */
+int dxpbd_grads(dxpbd_scene *scene, int32_t kind, float *out, int64_t out_len, int32_t mem,
+                void *stream);
+
+/* Replace a parameter family (DXPBD_PARAM_*) between optimization iterations. */
+int dxpbd_set_params(dxpbd_scene *scene, int32_t kind, const float *data, int64_t len,
+                     int32_t mem, void *stream);
+
+/* Colors of the constraints of a family (0 = distance [E], 1 = tets [T]) in user
+ * order into HOST out; returns the number of colors in *num_colors. */
+int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out_len,
+                   int32_t *num_colors);
+
+/* Statistics of the last calls: HOST out[0..n): see DXPBD_STAT_* in dxpbd.cu docs
+ * (0: total PCG iterations of the last backward, 1: max PCG iterations of one solve,
+ *  2: number of kernel launches of the last forward, 3: of the last backward,
+ *  4: substeps solved, 5: worst final relative residual). */
+int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
+
+/* Thread-local message of the last error ("" if none). */
+const char *dxpbd_last_error(void);
+
+/* ABI version (major * 100 + minor). */
+int dxpbd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DXPBD_H */

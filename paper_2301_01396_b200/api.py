@@ -1,0 +1,319 @@
+"""Thin Python binding of the DiffXPBD C-ABI (include/dxpbd.h): argument marshalling only.
+
+Every function has the name of the C entry point it calls.  Inputs may be numpy arrays
+(host memory), CPU torch tensors (host) or CUDA torch tensors (device memory, passed
+without copies on the current torch stream).  There is no fallback: if the CUDA
+library is missing or the device is unavailable, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+try:
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdxpbd.so")
+
+MEM_HOST, MEM_DEVICE = 0, 1
+GRAD_COMPLIANCE, GRAD_X0, GRAD_V0, GRAD_FORCES, GRAD_SHAPE, GRAD_SPHERE, GRAD_MATERIAL = range(7)
+PARAM_COMPLIANCE, PARAM_SHAPE, PARAM_MATERIAL, PARAM_SPHERES = range(4)
+GRAD_NAMES = {"compliance": GRAD_COMPLIANCE, "x0": GRAD_X0, "v0": GRAD_V0, "forces": GRAD_FORCES,
+              "shape": GRAD_SHAPE, "sphere": GRAD_SPHERE, "material": GRAD_MATERIAL}
+
+_fp = ctypes.POINTER(ctypes.c_float)
+_ip = ctypes.POINTER(ctypes.c_int32)
+
+
+class SceneDesc(ctypes.Structure):
+    _fields_ = [
+        ("num_vertices", ctypes.c_int32), ("x_rest", ctypes.c_void_p), ("inv_mass", ctypes.c_void_p),
+        ("num_dist", ctypes.c_int32), ("dist_idx", ctypes.c_void_p), ("dist_compliance", ctypes.c_void_p),
+        ("num_tets", ctypes.c_int32), ("tet_idx", ctypes.c_void_p), ("tet_a", ctypes.c_void_p),
+        ("tet_b", ctypes.c_void_p),
+        ("num_spheres", ctypes.c_int32), ("spheres", ctypes.c_void_p),
+        ("num_capsules", ctypes.c_int32), ("cap_center", ctypes.c_void_p), ("cap_axis", ctypes.c_void_p),
+        ("cap_r0", ctypes.c_void_p), ("cap_L0", ctypes.c_void_p),
+        ("num_shape", ctypes.c_int32), ("cap_rbasis", ctypes.c_void_p), ("cap_lbasis", ctypes.c_void_p),
+        ("shape_beta", ctypes.c_void_p),
+        ("gravity", ctypes.c_float * 3), ("frame_dt", ctypes.c_float), ("substeps", ctypes.c_int32),
+        ("iterations", ctypes.c_int32), ("thickness", ctypes.c_float), ("collision_compliance", ctypes.c_float),
+        ("max_frames", ctypes.c_int32), ("grad_flags", ctypes.c_uint32), ("pd_projection", ctypes.c_int32),
+        ("cg_tol", ctypes.c_float), ("cg_max_iter", ctypes.c_int32), ("device", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdxpbd.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"DiffXPBD CUDA library missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        sig = {
+            "dxpbd_create": ([ctypes.POINTER(SceneDesc), ctypes.POINTER(vp)], ctypes.c_int),
+            "dxpbd_destroy": ([vp], ctypes.c_int),
+            "dxpbd_forward": ([vp, vp, vp, vp, i32, i32, vp], ctypes.c_int),
+            "dxpbd_positions": ([vp, i32, vp, i32, vp], ctypes.c_int),
+            "dxpbd_backward": ([vp, i32, vp, vp, vp, i32, vp, vp], ctypes.c_int),
+            "dxpbd_grads": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
+            "dxpbd_set_params": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
+            "dxpbd_coloring": ([vp, i32, vp, i64, vp], ctypes.c_int),
+            "dxpbd_stats": ([vp, vp, i32], ctypes.c_int),
+            "dxpbd_last_error": ([], ctypes.c_char_p),
+            "dxpbd_version": ([], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["dxpbd_create", "dxpbd_destroy", "dxpbd_forward", "dxpbd_positions", "dxpbd_backward",
+            "dxpbd_grads", "dxpbd_set_params", "dxpbd_coloring", "dxpbd_stats", "dxpbd_last_error",
+            "dxpbd_version"]
+
+
+class DxpbdError(RuntimeError):
+    pass
+
+
+def _check(code: int, what: str):
+    if code != 0:
+        msg = lib().dxpbd_last_error().decode()
+        raise DxpbdError(f"{what} failed (code {code}): {msg}")
+
+
+# ------------------------------------------------------------------ marshalling helpers
+class _Arg:
+    """Holds a contiguous float32/int32 buffer alive and exposes (ptr, mem)."""
+
+    def __init__(self, a, dtype):
+        self.keep = None
+        if a is None:
+            self.ptr, self.mem = None, MEM_HOST
+            return
+        if torch is not None and isinstance(a, torch.Tensor):
+            t = a.detach().to(dtype=torch.float32 if dtype == np.float32 else torch.int32).contiguous()
+            self.keep = t
+            self.ptr = t.data_ptr()
+            self.mem = MEM_DEVICE if t.is_cuda else MEM_HOST
+        else:
+            arr = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+            self.keep = arr
+            self.ptr = arr.ctypes.data
+            self.mem = MEM_HOST
+
+
+def _host(a, dtype=np.float32):
+    if a is None:
+        return None
+    if torch is not None and isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    return np.ascontiguousarray(np.asarray(a), dtype=dtype)
+
+
+def _stream(*args):
+    if torch is not None and any(isinstance(a, torch.Tensor) and a.is_cuda for a in args):
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(0)
+
+
+class DxScene:
+    """Owning handle of a dxpbd_scene."""
+
+    def __init__(self, handle, V, E, T, S, K, NS, max_frames, substeps):
+        self.handle = handle
+        self.V, self.E, self.T, self.S, self.K, self.NS = V, E, T, S, K, NS
+        self.max_frames, self.substeps = max_frames, substeps
+        self.frames = 0
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().dxpbd_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ C entry points
+def dxpbd_create(x_rest, inv_mass, dist_idx=None, dist_compliance=None, tet_idx=None, tet_a=None, tet_b=None,
+                 spheres=None, cap_center=None, cap_axis=None, cap_r0=None, cap_L0=None, cap_rbasis=None,
+                 cap_lbasis=None, shape_beta=None, gravity=(0.0, -9.81, 0.0), frame_dt=1 / 60, substeps=1,
+                 iterations=1, thickness=0.0, collision_compliance=0.0, max_frames=1, grad_flags=0,
+                 pd_projection=1, cg_tol=1e-6, cg_max_iter=500, device=0) -> DxScene:
+    keep = []
+
+    def h(a, dt=np.float32):
+        arr = _host(a, dt)
+        keep.append(arr)
+        return None if arr is None else arr.ctypes.data
+
+    x_rest = _host(x_rest)
+    V = int(x_rest.reshape(-1, 3).shape[0])
+    E = 0 if dist_idx is None else int(np.asarray(dist_idx).reshape(-1, 2).shape[0])
+    T = 0 if tet_idx is None else int(np.asarray(tet_idx).reshape(-1, 4).shape[0])
+    S = 0 if spheres is None else int(np.asarray(spheres).reshape(-1, 4).shape[0])
+    K = 0 if cap_center is None else int(np.asarray(cap_center).reshape(-1, 3).shape[0])
+    NS = 0 if shape_beta is None else int(np.asarray(shape_beta).size)
+    d = SceneDesc()
+    d.num_vertices = V
+    d.x_rest = h(x_rest)
+    d.inv_mass = h(inv_mass)
+    d.num_dist = E
+    d.dist_idx = h(dist_idx, np.int32) if E else None
+    d.dist_compliance = h(dist_compliance) if E else None
+    d.num_tets = T
+    d.tet_idx = h(tet_idx, np.int32) if T else None
+    d.tet_a = h(tet_a) if T else None
+    d.tet_b = h(tet_b) if T else None
+    d.num_spheres = S
+    d.spheres = h(spheres) if S else None
+    d.num_capsules = K
+    if K:
+        d.cap_center, d.cap_axis = h(cap_center), h(cap_axis)
+        d.cap_r0, d.cap_L0 = h(cap_r0), h(cap_L0)
+    d.num_shape = NS if K else 0
+    if K and NS:
+        d.cap_rbasis, d.cap_lbasis, d.shape_beta = h(cap_rbasis), h(cap_lbasis), h(shape_beta)
+    d.gravity = (ctypes.c_float * 3)(*[float(g) for g in gravity])
+    d.frame_dt = float(frame_dt)
+    d.substeps = int(substeps)
+    d.iterations = int(iterations)
+    d.thickness = float(thickness)
+    d.collision_compliance = float(collision_compliance)
+    d.max_frames = int(max_frames)
+    d.grad_flags = int(grad_flags)
+    d.pd_projection = int(pd_projection)
+    d.cg_tol = float(cg_tol)
+    d.cg_max_iter = int(cg_max_iter)
+    d.device = int(device)
+    out = ctypes.c_void_p()
+    _check(lib().dxpbd_create(ctypes.byref(d), ctypes.byref(out)), "dxpbd_create")
+    return DxScene(out.value, V, E, T, S, K, NS if K else 0, int(max_frames), int(substeps))
+
+
+def dxpbd_destroy(scene: DxScene):
+    if scene.handle:
+        _check(lib().dxpbd_destroy(scene.handle), "dxpbd_destroy")
+        scene.handle = None
+
+
+def _mem_of(*args):
+    mems = {a.mem for a in args if a.ptr is not None}
+    if len(mems) > 1:
+        raise ValueError("mixing host and device buffers in one call")
+    return mems.pop() if mems else MEM_HOST
+
+
+def dxpbd_forward(scene: DxScene, x0, v0, forces=None, num_frames: int = 1):
+    ax, av, af = _Arg(x0, np.float32), _Arg(v0, np.float32), _Arg(forces, np.float32)
+    mem = _mem_of(ax, av, af)
+    _check(lib().dxpbd_forward(scene.handle, ax.ptr, av.ptr, af.ptr, int(num_frames), mem,
+                               _stream(x0, v0, forces)), "dxpbd_forward")
+    scene.frames = int(num_frames)
+
+
+def dxpbd_positions(scene: DxScene, frame: int, out=None):
+    if out is None:
+        out = np.zeros((scene.V, 3), np.float32)
+    a = _Arg(out, np.float32)
+    _check(lib().dxpbd_positions(scene.handle, int(frame), a.ptr, a.mem, _stream(out)), "dxpbd_positions")
+    return out
+
+
+def dxpbd_backward(scene: DxScene, key_frames, targets, weights=None) -> float:
+    kf = np.ascontiguousarray(np.asarray(key_frames, np.int32).reshape(-1))
+    at, aw = _Arg(targets, np.float32), _Arg(weights, np.float32)
+    mem = _mem_of(at, aw)
+    loss = ctypes.c_float(0.0)
+    _check(lib().dxpbd_backward(scene.handle, len(kf), kf.ctypes.data, at.ptr, aw.ptr, mem,
+                                ctypes.byref(loss), _stream(targets, weights)), "dxpbd_backward")
+    return float(loss.value)
+
+
+def _grad_size(scene: DxScene, kind: int):
+    return {GRAD_COMPLIANCE: (scene.E,), GRAD_X0: (scene.V, 3), GRAD_V0: (scene.V, 3),
+            GRAD_FORCES: (max(scene.frames, 1), scene.V, 3), GRAD_SHAPE: (scene.NS,),
+            GRAD_SPHERE: (scene.S, 4), GRAD_MATERIAL: (scene.T, 2)}[kind]
+
+
+def dxpbd_grads(scene: DxScene, kind, out=None):
+    kind = GRAD_NAMES.get(kind, kind)
+    shape = _grad_size(scene, kind)
+    if out is None:
+        out = np.zeros(shape, np.float32)
+    a = _Arg(out, np.float32)
+    n = int(np.prod(shape))
+    _check(lib().dxpbd_grads(scene.handle, int(kind), a.ptr, n, a.mem, _stream(out)), "dxpbd_grads")
+    return out
+
+
+def dxpbd_set_params(scene: DxScene, kind: int, data):
+    a = _Arg(data, np.float32)
+    n = int(np.asarray(a.keep.shape).prod()) if a.keep is not None else 0
+    _check(lib().dxpbd_set_params(scene.handle, int(kind), a.ptr, n, a.mem, _stream(data)), "dxpbd_set_params")
+
+
+def dxpbd_coloring(scene: DxScene, family: int = 0) -> np.ndarray:
+    n = scene.E if family == 0 else scene.T
+    out = np.zeros(n, np.int32)
+    nc = ctypes.c_int32(0)
+    _check(lib().dxpbd_coloring(scene.handle, int(family), out.ctypes.data, n, ctypes.byref(nc)),
+           "dxpbd_coloring")
+    return out
+
+
+def dxpbd_stats(scene: DxScene) -> dict:
+    out = np.zeros(8, np.float64)
+    _check(lib().dxpbd_stats(scene.handle, out.ctypes.data, 8), "dxpbd_stats")
+    return dict(cg_iters_total=out[0], cg_iters_max=out[1], fwd_launches=out[2], bwd_launches=out[3],
+                solves=out[4], worst_relres=out[5], loss=out[6])
+
+
+def dxpbd_last_error() -> str:
+    return lib().dxpbd_last_error().decode()
+
+
+def dxpbd_version() -> int:
+    return int(lib().dxpbd_version())
+
+
+# ------------------------------------------------------------------ convenience
+def scene_kwargs(scene) -> dict:
+    """Map a synth.Scene (duck-typed) onto dxpbd_create keyword arguments."""
+    s = scene
+    kw = dict(x_rest=s.x_rest, inv_mass=s.inv_mass, gravity=tuple(s.gravity), frame_dt=s.frame_dt,
+              substeps=s.substeps, iterations=s.iterations, thickness=s.thickness,
+              collision_compliance=s.collision_compliance)
+    if len(s.dist_idx):
+        kw.update(dist_idx=s.dist_idx, dist_compliance=s.dist_compliance)
+    if len(s.tet_idx):
+        kw.update(tet_idx=s.tet_idx, tet_a=s.tet_a, tet_b=s.tet_b)
+    if len(s.spheres):
+        kw.update(spheres=s.spheres)
+    if len(s.cap_center):
+        kw.update(cap_center=s.cap_center, cap_axis=s.cap_axis, cap_r0=s.cap_r0, cap_L0=s.cap_L0)
+        if len(s.shape_beta):
+            kw.update(cap_rbasis=s.cap_rbasis, cap_lbasis=s.cap_lbasis, shape_beta=s.shape_beta)
+    return kw
+
+
+def flags(*names) -> int:
+    f = 0
+    for n in names:
+        f |= 1 << GRAD_NAMES[n]
+    return f

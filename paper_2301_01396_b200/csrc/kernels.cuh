@@ -1,0 +1,640 @@
+// sm_100a kernels of the DiffXPBD hot path: forward substep, differentiable replay,
+// matrix-free filtered PCG, adjoint recursion and gradient accumulation.
+// Section / equation / line references are to PAPER.md (arXiv 2301.01396) and to the
+// readings R1..R13 of DESIGN.md.
+#pragma once
+#include "common.cuh"
+
+namespace dx {
+
+constexpr int kBlock = 256;
+constexpr float kEpsLen = 1e-9f;
+
+// Collider record (R7).  type 0 = sphere (c, r), 1 = capsule (c, axis, r, L).
+struct Collider {
+    float4 c;   // center (w unused)
+    float4 a;   // unit axis (capsule)
+    float r;    // radius
+    float L;    // segment length (capsule)
+    int type;
+    int pad;
+};
+
+// ============================================================================ predict
+// x~ = x_n + dt v_n + dt^2 (g + w f)  for free vertices, x~ = x_n for pinned ones
+// (Eq. xpbdUpdateRule l.91, R2).  v_n = (x_n - x_{n-1}) / dt exactly as the forward
+// defines it (R9), or v0 at n = 0.  Writes x~ (w = inverse mass) into out.
+__global__ void k_predict(int V, const double4 *__restrict__ xn, const double4 *__restrict__ xprev,
+                          const float4 *__restrict__ v0, const float *__restrict__ f, double dt,
+                          double inv_dt, float3 g, double4 *__restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= V) return;
+    double4 x = xn[i];
+    double3 v;
+    if (xprev) {
+        double4 p = xprev[i];
+        v = make_double3(__dmul_rn(__dsub_rn(x.x, p.x), inv_dt), __dmul_rn(__dsub_rn(x.y, p.y), inv_dt),
+                         __dmul_rn(__dsub_rn(x.z, p.z), inv_dt));
+    } else {
+        float4 q = v0[i];
+        v = make_double3(q.x, q.y, q.z);
+    }
+    double4 o = x;
+    if (x.w > 0.0) {
+        double3 acc = make_double3(g.x, g.y, g.z);
+        if (f) acc = make_double3(__fma_rn(x.w, (double)f[3 * i], acc.x), __fma_rn(x.w, (double)f[3 * i + 1], acc.y),
+                                  __fma_rn(x.w, (double)f[3 * i + 2], acc.z));
+        double dt2 = __dmul_rn(dt, dt);
+        o.x = __fma_rn(dt2, acc.x, __fma_rn(dt, v.x, x.x));
+        o.y = __fma_rn(dt2, acc.y, __fma_rn(dt, v.y, x.y));
+        o.z = __fma_rn(dt2, acc.z, __fma_rn(dt, v.z, x.z));
+    }
+    out[i] = o;
+}
+
+// ============================================================================ distance
+// Shared projection core (Eq. xpbd l.81 scalar form, Eq. l.85): identical instruction
+// sequence in the forward and in the replay (R9).  Returns false when skipped (R13).
+struct DistCore {
+    double3 d;    // x_a - x_b (fp64)
+    double len;   // |d|
+    float3 n;     // d / len
+    float C;      // len - rest (evaluated in fp64)
+    float J;      // w_a + w_b + at
+    float dl;     // delta lambda
+};
+
+DX_INLINE bool dist_core(const double4 &pa, const double4 &pb, float rest, float at, float lam0, DistCore &o) {
+    float wsum = radd((float)pa.w, (float)pb.w);
+    if (!(wsum > 0.f)) return false;
+    o.d = dsub3(d3(pa), d3(pb));
+    o.len = __dsqrt_rn(ddot3(o.d, o.d));
+    if (!(o.len > (double)kEpsLen)) return false;
+    double il = __drcp_rn(o.len);
+    o.n = make_float3((float)(o.d.x * il), (float)(o.d.y * il), (float)(o.d.z * il));
+    o.C = (float)__dsub_rn(o.len, (double)rest);
+    o.J = radd(wsum, at);
+    o.dl = rdiv(rsub(-o.C, rmul(at, lam0)), o.J);
+    return true;
+}
+
+// x_a += w_a n dl, x_b -= w_b n dl  (n in fp64 from d / len)
+DX_INLINE void dist_apply(double4 &pa, double4 &pb, const DistCore &o) {
+    double s = __ddiv_rn((double)o.dl, o.len);
+    double sa = __dmul_rn(pa.w, s), sb = -__dmul_rn(pb.w, s);
+    pa.x = __fma_rn(sa, o.d.x, pa.x); pa.y = __fma_rn(sa, o.d.y, pa.y); pa.z = __fma_rn(sa, o.d.z, pa.z);
+    pb.x = __fma_rn(sb, o.d.x, pb.x); pb.y = __fma_rn(sb, o.d.y, pb.y); pb.z = __fma_rn(sb, o.d.z, pb.z);
+}
+
+// One color of the Gauss-Seidel sweep over distance constraints (R1): constraints
+// [begin, begin+count) of the color-sorted arrays are vertex-disjoint.
+template <bool READ_LAM, bool WRITE_LAM>
+__global__ void __launch_bounds__(kBlock) k_dist_project(int begin, int count, const int2 *__restrict__ idx,
+                                                         const float *__restrict__ rest,
+                                                         const float *__restrict__ alpha, float inv_dt2,
+                                                         float *__restrict__ lam, double4 *__restrict__ x) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    int j = begin + t;
+    int2 e = idx[j];
+    double4 pa = x[e.x], pb = x[e.y];
+    float at = rmul(alpha[j], inv_dt2);
+    float lam0 = READ_LAM ? lam[j] : 0.f;
+    DistCore o;
+    if (!dist_core(pa, pb, rest[j], at, lam0, o)) return;
+    if (WRITE_LAM) lam[j] = radd(lam0, o.dl);
+    dist_apply(pa, pb, o);
+    x[e.x] = pa;
+    x[e.y] = pb;
+}
+
+// Differentiable replay of one color (Sec.4.3 l.166-194, Sec.4.4; R3).  For a distance
+// constraint grad C = [n, -n], H = [[K,-K],[-K,K]], K = (I - n n^T)/len, dJ/dx = 0, so every
+// stencil quantity has the form [s, -s] and D_j = [[B,-B],[-B,B]] with
+//   sigma_s = (-n - at sigma) / J          (a-part of d dlam / dx)
+//   B += dl K + n sigma_s^T                (kept symmetrised, R5)
+//   sigma += sigma_s
+// compliance control u = alpha_j (dat/du = dJ/du = 1/dt^2, dC/du = 0):
+//   t = (-(lam0 + dl)/dt^2 - at T) / J ;   e += t n ;   T += t
+// After the last iteration: Q_j = psd(-B) (R5) and e_j are stored for the PCG / gradients.
+struct DistScratch {   // per-constraint running state for iterations > 1 (SoA)
+    float *lam, *sig, *B, *T, *e;   // lam[E], sig[3E], B[6E], T[E], e[3E]
+};
+
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, int E, const int2 *__restrict__ idx,
+                                                        const float *__restrict__ rest,
+                                                        const float *__restrict__ alpha, float inv_dt2,
+                                                        DistScratch sc, int pd, float *__restrict__ Qout,
+                                                        float *__restrict__ eout, double4 *__restrict__ x) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    int j = begin + t;
+    int2 ev = idx[j];
+    double4 pa = x[ev.x], pb = x[ev.y];
+    float at = rmul(alpha[j], inv_dt2);
+    float lam0 = 0.f, T = 0.f;
+    float3 sig = make_float3(0.f, 0.f, 0.f), ec = make_float3(0.f, 0.f, 0.f);
+    Sym3 B = sym3_zero();
+    if (!FIRST) {
+        lam0 = sc.lam[j];
+        T = sc.T[j];
+        sig = make_float3(sc.sig[j], sc.sig[E + j], sc.sig[2 * E + j]);
+        ec = make_float3(sc.e[j], sc.e[E + j], sc.e[2 * E + j]);
+        B = Sym3{sc.B[j], sc.B[E + j], sc.B[2 * E + j], sc.B[3 * E + j], sc.B[4 * E + j], sc.B[5 * E + j]};
+    }
+    DistCore o;
+    bool ok = dist_core(pa, pb, rest[j], at, lam0, o);
+    if (ok) {
+        float il = (float)(1.0 / o.len);
+        float3 n = o.n;
+        float iJ = 1.f / o.J;
+        float3 ss = -iJ * (n + at * sig);
+        sym3_add_perp(B, o.dl * il, n);
+        sym3_add_symouter(B, n, ss);
+        sig = sig + ss;
+        float tt = (-(lam0 + o.dl) * inv_dt2 - at * T) * iJ;
+        ec = ec + tt * n;
+        T += tt;
+        lam0 = radd(lam0, o.dl);
+        dist_apply(pa, pb, o);
+        x[ev.x] = pa;
+        x[ev.y] = pb;
+    }
+    if (LAST) {
+        Sym3 mB = Sym3{-B.xx, -B.xy, -B.xz, -B.yy, -B.yz, -B.zz};
+        Sym3 Q = pd ? sym3_psd(mB) : mB;
+        Qout[j] = Q.xx; Qout[E + j] = Q.xy; Qout[2 * E + j] = Q.xz;
+        Qout[3 * E + j] = Q.yy; Qout[4 * E + j] = Q.yz; Qout[5 * E + j] = Q.zz;
+        if (eout) { eout[j] = ec.x; eout[E + j] = ec.y; eout[2 * E + j] = ec.z; }
+    } else {
+        sc.lam[j] = lam0;
+        sc.T[j] = T;
+        sc.sig[j] = sig.x; sc.sig[E + j] = sig.y; sc.sig[2 * E + j] = sig.z;
+        sc.e[j] = ec.x; sc.e[E + j] = ec.y; sc.e[2 * E + j] = ec.z;
+        sc.B[j] = B.xx; sc.B[E + j] = B.xy; sc.B[2 * E + j] = B.xz;
+        sc.B[3 * E + j] = B.yy; sc.B[4 * E + j] = B.yz; sc.B[5 * E + j] = B.zz;
+    }
+}
+
+// ============================================================================ collisions
+// C = |x - w(x)| - r - h against sphere center / closest capsule-segment point, applied only
+// while C < 0 (R7).  Per free vertex, colliders in index order.
+struct ContactCore {
+    double3 d;   // x - witness (fp64)
+    double len;
+    float3 n;
+    float C;
+    float J;
+    float dl;
+    float s;     // (x - c).axis (capsule)
+    int interior;
+};
+
+DX_INLINE bool contact_core(const double4 &p, const Collider &cd, float h, float at, float lam0, ContactCore &o) {
+    double3 x = d3(p);
+    double3 c = make_double3(cd.c.x, cd.c.y, cd.c.z);
+    double3 wpt = c;
+    o.interior = 0;
+    o.s = 0.f;
+    if (cd.type == 1) {
+        double3 ax = make_double3(cd.a.x, cd.a.y, cd.a.z);
+        double s = ddot3(dsub3(x, c), ax);
+        double half = 0.5 * (double)cd.L;
+        o.s = (float)s;
+        o.interior = (s > -half) && (s < half);
+        double tcl = fmin(fmax(s, -half), half);
+        wpt = make_double3(__fma_rn(tcl, ax.x, c.x), __fma_rn(tcl, ax.y, c.y), __fma_rn(tcl, ax.z, c.z));
+    }
+    o.d = dsub3(x, wpt);
+    o.len = __dsqrt_rn(ddot3(o.d, o.d));
+    if (!(o.len > (double)kEpsLen)) return false;
+    double Cd = __dsub_rn(__dsub_rn(o.len, (double)cd.r), (double)h);
+    if (!(Cd < 0.0)) return false;
+    double il = __drcp_rn(o.len);
+    o.n = make_float3((float)(o.d.x * il), (float)(o.d.y * il), (float)(o.d.z * il));
+    o.C = (float)Cd;
+    o.J = radd((float)p.w, at);
+    o.dl = rdiv(rsub(-o.C, rmul(at, lam0)), o.J);
+    return true;
+}
+
+DX_INLINE void contact_apply(double4 &p, const ContactCore &o) {
+    double sa = __dmul_rn(p.w, __ddiv_rn((double)o.dl, o.len));
+    p.x = __fma_rn(sa, o.d.x, p.x); p.y = __fma_rn(sa, o.d.y, p.y); p.z = __fma_rn(sa, o.d.z, p.z);
+}
+
+template <bool READ_LAM, bool WRITE_LAM>
+__global__ void __launch_bounds__(kBlock) k_contact_project(int V, int NC, const Collider *__restrict__ cols,
+                                                            float h, float at, float *__restrict__ lam,
+                                                            double4 *__restrict__ x) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    double4 p = x[v];
+    if (!(p.w > 0.f)) return;
+    bool moved = false;
+    for (int c = 0; c < NC; ++c) {
+        Collider cd = cols[c];
+        float lam0 = READ_LAM ? lam[(size_t)c * V + v] : 0.f;
+        ContactCore o;
+        if (contact_core(p, cd, h, at, lam0, o)) {
+            if (WRITE_LAM) lam[(size_t)c * V + v] = radd(lam0, o.dl);
+            contact_apply(p, o);
+            moved = true;
+        }
+    }
+    if (moved) x[v] = p;
+}
+
+// Differentiable replay of the contacts.  Per (collider c, vertex v): grad C = n, H = (I - n n^T
+// - interior a a^T)/len, H M^-1 g = 0 (unit normal), so with sigma the running d dlam/dx:
+//   sigma_s = (-n - at sigma)/J ;  B += dl H + n sigma_s^T ;  sigma += sigma_s
+// Controls (dC/du, dn/du, dJ/du = 0, dat/du = 0; running T_u):
+//   t_u = (-dC/du - at T_u)/J ;  e_u += dl dn/du + t_u n ;  T_u += t_u
+//   sphere u = (c_x, c_y, c_z, r): dC/dc = -n, dC/dr = -1, dn/dc = -(I - n n^T)/len
+//   capsule u = (r, L): dC/dr = -1; for the clamped ends dcp/dL = +-a/2:
+//       dC/dL = -n.dcp/dL, dn/dL = -(I - n n^T) dcp/dL / len; interior: 0.
+// The per-pair scratch layout: [c][v] for lam, T(4), sigma(3), B(6), e(12 = 4 params x 3).
+// After the last iteration: Qc_v = Sum_c psd(-B_cv) (per-vertex 3x3, R5), e stored per pair.
+struct ContactScratch {
+    float *lam, *T, *sig, *B, *e;   // sizes NC*V*{1,4,3,6,12}
+};
+
+DX_INLINE void contact_deriv(const Collider &cd, const ContactCore &o, float at, float inv_len, float3 n,
+                             float3 &sig, Sym3 &B, float (&T)[4], float (&e)[12]) {
+    float iJ = 1.f / o.J;
+    float3 ss = -iJ * (n + at * sig);
+    // dl H
+    sym3_add_perp(B, o.dl * inv_len, n);
+    if (cd.type == 1 && o.interior) {
+        float3 ax = f3(cd.a);
+        float q = -o.dl * inv_len;
+        B.xx += q * ax.x * ax.x; B.yy += q * ax.y * ax.y; B.zz += q * ax.z * ax.z;
+        B.xy += q * ax.x * ax.y; B.xz += q * ax.x * ax.z; B.yz += q * ax.y * ax.z;
+    }
+    sym3_add_symouter(B, n, ss);
+    sig = sig + ss;
+    if (cd.type == 0) {
+        // u = c_k (k = 0..2): dC/dc_k = -n_k ; dn/dc_k = -(e_k - n n_k)/len
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float nk = k == 0 ? n.x : (k == 1 ? n.y : n.z);
+            float tt = (nk - at * T[k]) * iJ;
+            float3 ek = make_float3(k == 0 ? 1.f : 0.f, k == 1 ? 1.f : 0.f, k == 2 ? 1.f : 0.f);
+            float3 dn = -inv_len * (ek - nk * n);
+            float3 add = o.dl * dn + tt * n;
+            e[3 * k] += add.x; e[3 * k + 1] += add.y; e[3 * k + 2] += add.z;
+            T[k] += tt;
+        }
+        // u = r: dC/dr = -1, dn/dr = 0
+        float tt = (1.f - at * T[3]) * iJ;
+        e[9] += tt * n.x; e[10] += tt * n.y; e[11] += tt * n.z;
+        T[3] += tt;
+    } else {
+        float tt = (1.f - at * T[0]) * iJ;   // u = r
+        e[0] += tt * n.x; e[1] += tt * n.y; e[2] += tt * n.z;
+        T[0] += tt;
+        // u = L
+        float sgn = o.interior ? 0.f : (o.s >= 0.f ? 0.5f : -0.5f);
+        float3 ax = f3(cd.a);
+        float3 dcp = sgn * ax;
+        float dCdL = -dot3(n, dcp);
+        float3 dn = -inv_len * (dcp - dot3(n, dcp) * n);
+        float t2 = (-dCdL - at * T[1]) * iJ;
+        float3 add = o.dl * dn + t2 * n;
+        e[3] += add.x; e[4] += add.y; e[5] += add.z;
+        T[1] += t2;
+    }
+}
+
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kBlock) k_contact_replay(int V, int NC, const Collider *__restrict__ cols,
+                                                           float h, float at, ContactScratch sc, int pd,
+                                                           float *__restrict__ Qc, float *__restrict__ eout,
+                                                           double4 *__restrict__ x) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    double4 p = x[v];
+    if (!(p.w > 0.f)) {
+        if (LAST) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) Qc[(size_t)k * V + v] = 0.f;
+        }
+        return;
+    }
+    Sym3 Qsum = sym3_zero();
+    bool moved = false;
+    const size_t NV = (size_t)NC * V;
+    for (int c = 0; c < NC; ++c) {
+        const Collider cd = cols[c];
+        const size_t pr = (size_t)c * V + v;
+        float lam0 = 0.f;
+        float T[4] = {0.f, 0.f, 0.f, 0.f};
+        float e[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) e[k] = 0.f;
+        float3 sig = make_float3(0.f, 0.f, 0.f);
+        Sym3 B = sym3_zero();
+        if (!FIRST) {
+            lam0 = sc.lam[pr];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) T[k] = sc.T[k * NV + pr];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) e[k] = sc.e[k * NV + pr];
+            sig = make_float3(sc.sig[pr], sc.sig[NV + pr], sc.sig[2 * NV + pr]);
+            B = Sym3{sc.B[pr], sc.B[NV + pr], sc.B[2 * NV + pr], sc.B[3 * NV + pr], sc.B[4 * NV + pr],
+                     sc.B[5 * NV + pr]};
+        }
+        ContactCore o;
+        if (contact_core(p, cd, h, at, lam0, o)) {
+            float il = (float)(1.0 / o.len);
+            float3 n = o.n;
+            contact_deriv(cd, o, at, il, n, sig, B, T, e);
+            lam0 = radd(lam0, o.dl);
+            contact_apply(p, o);
+            moved = true;
+        }
+        if (LAST) {
+            Sym3 mB = Sym3{-B.xx, -B.xy, -B.xz, -B.yy, -B.yz, -B.zz};
+            Sym3 Q = pd ? sym3_psd(mB) : mB;
+            Qsum.xx += Q.xx; Qsum.xy += Q.xy; Qsum.xz += Q.xz;
+            Qsum.yy += Q.yy; Qsum.yz += Q.yz; Qsum.zz += Q.zz;
+            if (eout) {
+#pragma unroll
+                for (int k = 0; k < 12; ++k) eout[k * NV + pr] = e[k];
+            }
+        } else {
+            sc.lam[pr] = lam0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sc.T[k * NV + pr] = T[k];
+#pragma unroll
+            for (int k = 0; k < 12; ++k) sc.e[k * NV + pr] = e[k];
+            sc.sig[pr] = sig.x; sc.sig[NV + pr] = sig.y; sc.sig[2 * NV + pr] = sig.z;
+            sc.B[pr] = B.xx; sc.B[NV + pr] = B.xy; sc.B[2 * NV + pr] = B.xz;
+            sc.B[3 * NV + pr] = B.yy; sc.B[4 * NV + pr] = B.yz; sc.B[5 * NV + pr] = B.zz;
+        }
+    }
+    if (moved) x[v] = p;
+    if (LAST) {
+        Qc[v] = Qsum.xx; Qc[V + v] = Qsum.xy; Qc[2 * (size_t)V + v] = Qsum.xz;
+        Qc[3 * (size_t)V + v] = Qsum.yy; Qc[4 * (size_t)V + v] = Qsum.yz; Qc[5 * (size_t)V + v] = Qsum.zz;
+    }
+}
+
+// ============================================================================ PCG
+// Filtered PCG (Sec.4.2.1) on (M + Sum_j Q_j)_free y = r (Eq. adjointXPBD, R4), matrix-free,
+// preconditioner M (P^-1 = inverse mass; pinned rows filtered).  Scalars live in a per-iteration
+// slot array sc[it*4 + {0: p.Ap, 1: r.z, 2: r.r}] (double) so no reset is ever needed:
+// iteration `it` accumulates into slot it, reads slot it-1 (and slot "rz" of it-1).
+// done-test: an iteration returns immediately if the previous residual met the tolerance.
+struct CGState {
+    double *sc;      // [(max_iter+2)*4]
+    double *bnorm2;  // b.b (filtered)
+    float tol2;
+};
+
+DX_INLINE bool cg_done(const CGState &s, int it) {
+    // converged after iteration it-1 ?
+    if (it == 0) return false;
+    double rr = s.sc[(it - 1) * 4 + 2];
+    return rr <= (double)s.tol2 * s.bnorm2[0];
+}
+
+// init: r = b (filtered), y = 0, p = M^-1 r ; slot[-1] rz = r.M^-1 r stored in sc[...] of "it=-1"
+// we store it in slot 0 field 1 of a dedicated init slot: sc layout shifted by one (slot 0 = init).
+__global__ void k_cg_init(int V, const float4 *__restrict__ b, float4 *__restrict__ y, float4 *__restrict__ r,
+                          float4 *__restrict__ p, const float *__restrict__ wv, CGState s) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc[3] = {0.f, 0.f, 0.f};
+    if (v < V) {
+        float w = wv[v];
+        float4 bb = b[v];
+        if (!(w > 0.f)) bb = make_float4(0.f, 0.f, 0.f, 0.f);
+        y[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        r[v] = bb;
+        float4 pp = make_float4(w * bb.x, w * bb.y, w * bb.z, 0.f);
+        p[v] = pp;
+        acc[1] = bb.x * pp.x + bb.y * pp.y + bb.z * pp.z;   // r.z
+        acc[2] = bb.x * bb.x + bb.y * bb.y + bb.z * bb.z;   // r.r
+    }
+    block_reduce_add<3>(acc, s.sc);   // slot 0
+}
+
+// per-vertex part of q = A p: q = M p + Qc p (contacts), and the p.q partial of these terms.
+// For it > 0 first updates p = M^-1 r + beta p with beta = rz(it)/rz(it-1) (slots it, it-1).
+__global__ void k_cg_vertex(int V, int it, float4 *__restrict__ p, const float4 *__restrict__ r,
+                            float4 *__restrict__ q, const float *__restrict__ wv,
+                            const float *__restrict__ Qc, CGState s) {
+    // slot index: sc slot (it+1) accumulates this iteration's p.q; slot it holds the current rz
+    if (cg_done(s, it + 1)) return;
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc[1] = {0.f};
+    if (v < V) {
+        float w = wv[v];
+        float4 pv = p[v];
+        if (it > 0) {
+            double beta = s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1];
+            float bf = (float)beta;
+            float4 rv = r[v];
+            pv = make_float4(w * rv.x + bf * pv.x, w * rv.y + bf * pv.y, w * rv.z + bf * pv.z, 0.f);
+            p[v] = pv;
+        }
+        float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (w > 0.f) {
+            float m = 1.f / w;
+            float3 pp = f3(pv);
+            float3 qq = m * pp;
+            if (Qc) {
+                Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                              Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                qq = qq + sym3_mul(A, pp);
+            }
+            qv = make_float4(qq.x, qq.y, qq.z, 0.f);
+            acc[0] = dot3(pp, qq);
+        }
+        q[v] = qv;
+    }
+    block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
+}
+
+// distance-constraint part of q = A p: q_a += Q d, q_b -= Q d with d = p_a - p_b (pinned rows
+// filtered), and its p.q partial d^T Q d.
+__global__ void __launch_bounds__(kBlock) k_cg_dist(int E, int it, const int2 *__restrict__ idx,
+                                                    const float *__restrict__ Q, const float4 *__restrict__ p,
+                                                    float4 *__restrict__ q, const float *__restrict__ wv,
+                                                    CGState s) {
+    if (cg_done(s, it + 1)) return;
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc[1] = {0.f};
+    if (j < E) {
+        int2 e = idx[j];
+        float4 pa = p[e.x], pb = p[e.y];   // p is zero on pinned vertices
+        float3 d = f3(pa) - f3(pb);
+        Sym3 A = Sym3{Q[j], Q[E + j], Q[2 * (size_t)E + j], Q[3 * (size_t)E + j], Q[4 * (size_t)E + j],
+                      Q[5 * (size_t)E + j]};
+        float3 y = sym3_mul(A, d);
+        acc[0] = dot3(d, y);
+        if (wv[e.x] > 0.f) red_add_f4(q + e.x, make_float4(y.x, y.y, y.z, 0.f));
+        if (wv[e.y] > 0.f) red_add_f4(q + e.y, make_float4(-y.x, -y.y, -y.z, 0.f));
+    }
+    block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
+}
+
+// y += alpha p, r -= alpha q, alpha = rz(it) / pq(it+1); accumulates rz and rr into slot it+1.
+__global__ void k_cg_update(int V, int it, float4 *__restrict__ y, float4 *__restrict__ r,
+                            const float4 *__restrict__ p, const float4 *__restrict__ q,
+                            const float *__restrict__ wv, CGState s) {
+    if (cg_done(s, it + 1)) return;
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc[2] = {0.f, 0.f};
+    if (v < V) {
+        double pq = s.sc[(it + 1) * 4 + 0];
+        float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
+        float w = wv[v];
+        float4 yv = y[v], rv = r[v], pv = p[v], qv = q[v];
+        yv.x += alpha * pv.x; yv.y += alpha * pv.y; yv.z += alpha * pv.z;
+        rv.x -= alpha * qv.x; rv.y -= alpha * qv.y; rv.z -= alpha * qv.z;
+        y[v] = yv;
+        r[v] = rv;
+        acc[0] = w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
+        acc[1] = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
+    }
+    block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
+}
+
+// ============================================================================ adjoint
+// Increment form of Eq. adjointXPBD (R3/R4): with A_n = M + Sum_j Q_j(n),
+// y_n = M^-1 xhat_n and the paper's right-hand side 2 xhat_{n+1} - vhat_{n+1}/dt + dphi/dx (l.155)
+//   A_n y_n = M (2 y_{n+1} - y_{n+2}) + dphi/dx_{n+1}
+// is solved for u_n = y_n - y_{n+1}:
+//   A_n u_n = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1},   y_n = y_{n+1} + u_n,
+// algebraically identical, but the PCG tolerance is relative to the (small) increment instead of
+// being integrated twice by the second difference.  Pinned rows are filtered (R11).
+// b = M u_next + dphi_{n+1} - Qc y_next   (vertex part)
+__global__ void k_rhs_vertex(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
+                             const float4 *__restrict__ y, const float *__restrict__ Qc,
+                             const double4 *__restrict__ xkey, const float *__restrict__ target,
+                             const float *__restrict__ weights, float4 *__restrict__ b) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    float w = wv[v];
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (w > 0.f) {
+        float3 r = (1.f / w) * f3(u[v]);
+        if (Qc) {
+            Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v], Qc[4 * (size_t)V + v],
+                          Qc[5 * (size_t)V + v]};
+            r = r - sym3_mul(A, f3(y[v]));
+        }
+        if (target) {
+            double4 x = xkey[v];
+            float W = weights ? weights[v] : 1.f;
+            r = r + W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
+                                    (float)(x.z - target[3 * v + 2]));
+        }
+        o = make_float4(r.x, r.y, r.z, 0.f);
+    }
+    b[v] = o;
+}
+
+// b_a -= Q_j (y_a - y_b), b_b += Q_j (y_a - y_b)   (distance-constraint part of -Q y)
+__global__ void __launch_bounds__(kBlock) k_rhs_dist(int E, const int2 *__restrict__ idx, const float *__restrict__ Q,
+                                                     const float4 *__restrict__ y, float4 *__restrict__ b,
+                                                     const float *__restrict__ wv) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= E) return;
+    int2 e = idx[j];
+    float3 d = f3(y[e.x]) - f3(y[e.y]);
+    Sym3 A = Sym3{Q[j], Q[E + j], Q[2 * (size_t)E + j], Q[3 * (size_t)E + j], Q[4 * (size_t)E + j],
+                  Q[5 * (size_t)E + j]};
+    float3 q = sym3_mul(A, d);
+    if (wv[e.x] > 0.f) red_add_f4(b + e.x, make_float4(-q.x, -q.y, -q.z, 0.f));
+    if (wv[e.y] > 0.f) red_add_f4(b + e.y, make_float4(q.x, q.y, q.z, 0.f));
+}
+
+// after the solve: y_n = y_{n+1} + u_n ; dphi/df_frame += dt^2 y_n (R8)
+__global__ void k_adjoint_accum(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
+                                float4 *__restrict__ y, float *__restrict__ gforce, float dt) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    if (!(wv[v] > 0.f)) return;
+    float4 uv = u[v], yv = y[v];
+    yv.x += uv.x; yv.y += uv.y; yv.z += uv.z;
+    y[v] = yv;
+    if (gforce) {
+        float dt2 = dt * dt;
+        gforce[3 * v] += dt2 * yv.x;
+        gforce[3 * v + 1] += dt2 * yv.y;
+        gforce[3 * v + 2] += dt2 * yv.z;
+    }
+}
+
+// dphi/dx_0 = xbar_0 = M u_0 + dphi/dx_0(direct) ; dphi/dv_0 = vbar_0 = dt M y_0   (Eq. rawAdjoint)
+__global__ void k_adjoint_final(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
+                                const float4 *__restrict__ y, const double4 *__restrict__ x0,
+                                const float *__restrict__ target, const float *__restrict__ weights, float dt,
+                                float *__restrict__ gx0, float *__restrict__ gv0) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    float w = wv[v];
+    float3 gx = make_float3(0.f, 0.f, 0.f), gv = gx;
+    if (w > 0.f) {
+        float m = 1.f / w;
+        gx = m * f3(u[v]);
+        if (target) {
+            double4 x = x0[v];
+            float W = weights ? weights[v] : 1.f;
+            gx = gx + W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
+                                      (float)(x.z - target[3 * v + 2]));
+        }
+        gv = (dt * m) * f3(y[v]);
+    }
+    gx0[3 * v] = gx.x; gx0[3 * v + 1] = gx.y; gx0[3 * v + 2] = gx.z;
+    gv0[3 * v] = gv.x; gv0[3 * v + 1] = gv.y; gv0[3 * v + 2] = gv.z;
+}
+
+// phi += 1/2 Sum_v W_v |x_v - target_v|^2 (all vertices, R10)
+__global__ void k_loss(int V, const double4 *__restrict__ x, const float *__restrict__ target,
+                       const float *__restrict__ weights, double *acc) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    float a[1] = {0.f};
+    if (v < V) {
+        double4 p = x[v];
+        float W = weights ? weights[v] : 1.f;
+        float dx = (float)(p.x - target[3 * v]), dy = (float)(p.y - target[3 * v + 1]),
+              dz = (float)(p.z - target[3 * v + 2]);
+        a[0] = 0.5f * W * (dx * dx + dy * dy + dz * dz);
+    }
+    block_reduce_add<1>(a, acc);
+}
+
+// dphi/dalpha_j += e_j . (y_a - y_b)   (Eq. gradientRule; e_j is the a-part of M dDx/dalpha_j)
+__global__ void k_grad_compliance(int E, const int2 *__restrict__ idx, const float *__restrict__ e,
+                                  const float4 *__restrict__ y, float *__restrict__ g) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= E) return;
+    int2 id = idx[j];
+    float3 d = f3(y[id.x]) - f3(y[id.y]);
+    g[j] += e[j] * d.x + e[E + j] * d.y + e[2 * (size_t)E + j] * d.z;
+}
+
+// collider parameter gradients: acc[c*4 + u] += Sum_v e_{c,v,u} . y_v
+__global__ void k_grad_colliders(int V, int NC, const float *__restrict__ e, const float4 *__restrict__ y,
+                                 double *acc) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t NV = (size_t)NC * V;
+    for (int c = 0; c < NC; ++c) {
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        if (v < V) {
+            float3 yv = f3(y[v]);
+            size_t pr = (size_t)c * V + v;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                a[u] = e[(3 * u) * NV + pr] * yv.x + e[(3 * u + 1) * NV + pr] * yv.y + e[(3 * u + 2) * NV + pr] * yv.z;
+        }
+        block_reduce_add<4>(a, acc + 4 * c);
+        __syncthreads();
+    }
+}
+
+}  // namespace dx

@@ -1,0 +1,103 @@
+"""GPU parity: CUDA path (through the C-ABI) vs the fp64 oracle on the same seeded inputs.
+Bars (BASELINE.json north_star): positions within 1e-4 relative L2, every gradient vector within
+1e-3 relative L2, colorings and index buffers bit-exact."""
+import numpy as np
+import pytest
+
+from synth import tiny_cloth, medium_cloth, large_cloth, garment
+from tests.gpu_helpers import f32, gpu_run, oracle_run, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+POS_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+def _compare(g, o, grads, pos_tol=POS_TOL, grad_tol=GRAD_TOL):
+    errs = {}
+    for f, (xg, xo) in enumerate(zip(g["x"], o["x"])):
+        errs[f"pos{f}"] = rel_l2(xg, xo)
+    for k in grads:
+        errs[k] = rel_l2(g[k], o[k])
+    print({k: f"{v:.2e}" for k, v in errs.items() if not k.startswith("pos") or k == f"pos{len(g['x']) - 1}"})
+    for f in range(len(g["x"])):
+        assert errs[f"pos{f}"] < pos_tol, ("positions", f, errs[f"pos{f}"])
+    if "loss" in o:
+        # |dphi| <= |x - x*| |dx| + |dx|^2 / 2 with |dx| <= pos_tol |x| (phi = 1/2 |x - x*|^2, R10)
+        dxn = pos_tol * max(np.linalg.norm(x) for x in o["x"])
+        bound = np.sqrt(2 * abs(o["loss"])) * dxn + 0.5 * dxn * dxn
+        assert abs(g["loss"] - o["loss"]) <= bound, (g["loss"], o["loss"], bound)
+    for k in grads:
+        assert np.isfinite(g[k]).all(), k
+        assert errs[k] < grad_tol, (k, errs[k])
+
+
+def test_coloring_bit_exact():
+    from oracle import greedy_color
+    for s in (tiny_cloth(), medium_cloth(n=64, frames=1)):
+        g = gpu_run(f32(s), frames=1, backward=False)
+        from paper_2301_01396_b200 import api
+        col = api.dxpbd_coloring(g["scene"], 0)
+        np.testing.assert_array_equal(col, greedy_color(s.dist_idx, s.num_vertices))
+
+
+@pytest.mark.parametrize("iters", [1, 3])
+def test_tiny_cloth_forward_backward(iters):
+    """configs[0] (16x16, 30 frames x 10 substeps; 1 and 3 GS iterations)."""
+    frames = 30 if iters == 1 else 6
+    s = f32(tiny_cloth(iterations=iters, frames=frames))
+    grads = ("compliance", "v0")
+    g = gpu_run(s, grads)
+    o = oracle_run(s)
+    _compare(g, o, grads + ("x0",))
+
+
+def test_tiny_cloth_no_pd_projection():
+    s = f32(tiny_cloth(frames=4))
+    g = gpu_run(s, ("compliance",), pd=0)
+    o = oracle_run(s, pd=False)
+    _compare(g, o, ("compliance", "v0", "x0"))
+
+
+def test_medium_cloth_sphere_small():
+    """configs[1] shape at reduced size: cloth dropped on a sphere with contacts."""
+    s = f32(medium_cloth(n=24, frames=12))
+    grads = ("compliance", "x0", "sphere")
+    g = gpu_run(s, grads)
+    o = oracle_run(s)
+    _compare(g, o, ("compliance", "x0", "v0", "sphere"))
+
+
+def test_forces_keyframes_small():
+    """configs[4] shape at reduced size: per-frame forces, keyframes 1/2/3."""
+    s = f32(large_cloth(n=20, frames=3, side=1.0, key_frames=(1, 2, 3)))
+    grads = ("forces", "x0", "v0")
+    g = gpu_run(s, grads)
+    o = oracle_run(s)
+    _compare(g, o, grads)
+
+
+def test_garment_capsules_small():
+    """configs[3] shape at reduced size: tube over the 12-capsule body, shape gradients."""
+    s = f32(garment(n_around=20, n_along=14, frames=4))
+    grads = ("shape", "compliance")
+    g = gpu_run(s, grads)
+    o = oracle_run(s)
+    _compare(g, o, ("shape", "compliance", "v0"))
+
+
+def test_host_buffers_e2e_matches_device():
+    s = f32(tiny_cloth(frames=3))
+    a = gpu_run(s, ("compliance",), device_inputs=True)
+    b = gpu_run(s, ("compliance",), device_inputs=False)
+    for xa, xb in zip(a["x"], b["x"]):
+        np.testing.assert_array_equal(xa, xb)
+    assert rel_l2(a["compliance"], b["compliance"]) < 1e-5
+
+
+def test_medium_full_size_forward_one_frame():
+    """configs[1] at full size (256x256), 1 frame: all positions vs the oracle."""
+    s = f32(medium_cloth(frames=1))
+    g = gpu_run(s, backward=False, frames=1)
+    o = oracle_run(s, frames=1, backward=False)
+    assert rel_l2(g["x"][-1], o["x"][-1]) < POS_TOL
