@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""DiffXPBD hot-path benchmark (one JSON line on rank 0).
+
+A "step" = forward over all frames (XPBD substeps with checkpoints) + keyframe loss + adjoint
+pass over every substep (replay, PCG, gradient accumulation) for BASELINE.json configs[4]
+("large cloth at paper scale": 2944x2944 grid, ~26M DoF, 30 frames x 10 substeps, per-frame
+per-vertex forces, keyframes 10/20/30, gradients w.r.t. the force sequence).
+
+metric value = forward constraint solves of the step / (forward + adjoint) time, whole job.
+Timing: CUDA events on the library's stream, barrier + synchronize on both sides, max over ranks.
+Inputs are resident in HBM when the timed region starts (e2e repeats it with pinned host buffers).
+N > 1 (torchrun): every rank runs its own independent scene (weak scaling, no data-path collective).
+--impl reference: the fp64 oracle (oracle/) on a bounded crop of the same workload, host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "constraint solves/s & ms/step fwd+adjoint at ~26M DoF cloth; HBM GB/s vs peak"
+UNIT = "constraint solves/s"
+
+
+def args_():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=2944, help="grid side (2944 = configs[4])")
+    p.add_argument("--frames", type=int, default=30)
+    p.add_argument("--substeps", type=int, default=10)
+    p.add_argument("--iterations", type=int, default=1)
+    p.add_argument("--cg-tol", type=float, default=1e-6)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-profile", action="store_true")
+    p.add_argument("--ref-n", type=int, default=80, help="grid side of the oracle crop")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_sample(ref_n: int, frames: int = 1):
+    """Bounded sample of the same workload for the fp64 oracle: a ref_n x ref_n crop of the large
+    cloth (same constraint types, forces, spacing), `frames` frames x 10 substeps, fwd + adjoint."""
+    import numpy as np
+    from synth import large_cloth, as_float32_exact
+    from oracle import OracleModel
+    side = 10.0 * (ref_n - 1) / 2943.0
+    s = as_float32_exact(large_cloth(n=ref_n, frames=frames, side=side, key_frames=(frames,)))
+    m = OracleModel(s)
+    t0 = time.perf_counter()
+    xs = m.simulate(s.x0, s.v0, s.forces, frames)
+    t1 = time.perf_counter()
+    m.backward(xs, s.v0, s.forces)
+    t2 = time.perf_counter()
+    solves = len(s.dist_idx) * s.iterations * s.substeps * frames
+    return dict(solves=solves, t_fwd=t1 - t0, t_total=t2 - t0, E=len(s.dist_idx), V=s.num_vertices,
+                sample=f"{ref_n}x{ref_n} crop of configs[4], {frames} frame x {s.substeps} substeps, fwd+adjoint, "
+                       f"fp64 oracle (numpy + scipy spsolve)")
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(a.warmup):
+        oracle_sample(a.ref_n)
+    times, res = [], None
+    for _ in range(a.steps):
+        res = oracle_sample(a.ref_n)
+        times.append(res["t_total"])
+    tmax = max(times)
+    value = res["solves"] / (sum(times) / len(times))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "large_cloth (configs[4]) bounded crop", "crop": f"{a.ref_n}x{a.ref_n}",
+                   "frames": 1, "substeps": 10, "iterations": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": res["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "t_max_s": tmax,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+# algorithmic (compulsory) HBM bytes per launch of each kernel class
+def algo_bytes(cls, E, V, count, grads_comp=False):
+    if cls == "dist_project":      # per constraint: idx 8 + rest 4 + alpha 4 + 2 x (32 B read + 32 B write)
+        return 144.0 * E / count
+    if cls == "dist_replay":       # + Q 24 (+ e 12)
+        return (168.0 + (12.0 if grads_comp else 0.0)) * E / count
+    if cls == "cg_dist":           # per constraint idx 8 + Q 24; per vertex p 16 + q r/w 32 + w 4
+        return 32.0 * E + 52.0 * V
+    if cls == "cg_vertex":         # p r/w 32, r 16, q w 16, w 4
+        return 68.0 * V
+    if cls == "cg_update":         # y r/w 32, r r/w 32, p 16, q 16, w 4
+        return 100.0 * V
+    if cls == "predict":           # x_n 32, x_{n-1} 32, f 12, out 32
+        return 108.0 * V
+    if cls == "rhs":
+        return (32.0 * E + 52.0 * V) / 2
+    return None
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2301_01396_b200 import api
+    from synth import large_cloth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    side = 10.0 * (a.n - 1) / 2943.0
+    s = large_cloth(n=a.n, frames=a.frames, substeps=a.substeps, iterations=a.iterations, seed=4 + rank,
+                    side=side, with_forces=False, key_frames=tuple(k for k in (10, 20, 30) if k <= a.frames)
+                    or (a.frames,))
+    V, E = s.num_vertices, len(s.dist_idx)
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    forces_h = (torch.randn((a.frames, V, 3), generator=g, dtype=torch.float32) * 0.1).pin_memory()
+    x0_h = torch.as_tensor(s.x0, dtype=torch.float32).pin_memory()
+    v0_h = torch.as_tensor(s.v0, dtype=torch.float32).pin_memory()
+    tg_h = torch.as_tensor(s.targets, dtype=torch.float32).pin_memory()
+    kf = np.asarray(s.key_frames, np.int32)
+    t_create = time.perf_counter()
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=a.frames, grad_flags=api.flags("forces"),
+                          cg_tol=a.cg_tol, cg_max_iter=1000, device=local)
+    t_create = time.perf_counter() - t_create
+    del s
+    forces_d, x0_d, v0_d, tg_d = (t.to(dev, non_blocking=True) for t in (forces_h, x0_h, v0_h, tg_h))
+    gforce_d = torch.empty((a.frames, V, 3), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def step(t_fwd_ev=None):
+        api.dxpbd_forward(sc, x0_d, v0_d, forces_d, a.frames)
+        if t_fwd_ev is not None:
+            t_fwd_ev.record(stream)
+        loss = api.dxpbd_backward(sc, kf, tg_d)
+        api.dxpbd_grads(sc, "forces", gforce_d)
+        return loss
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    if not a.no_profile:
+        api.dxpbd_profile(sc, True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    launches, cg_iters = 0, 0
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for i in range(a.steps):
+        ev[i][0].record(stream)
+        loss = step(ev[i][1])
+        ev[i][2].record(stream)
+        st = api.dxpbd_stats(sc)
+        launches += int(st["fwd_launches"] + st["bwd_launches"]) + 1
+        cg_iters += int(st["cg_iters_total"])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_steps = [ev[i][0].elapsed_time(ev[i][2]) for i in range(a.steps)]
+    t_fwds = [ev[i][0].elapsed_time(ev[i][1]) for i in range(a.steps)]
+    ktimes = api.dxpbd_kernel_times(sc) if not a.no_profile else {}
+    api.dxpbd_profile(sc, False)
+    total_ms = sum(t_steps)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / a.steps
+    substeps_total = a.frames * a.substeps
+    solves_per_step = E * a.iterations * substeps_total
+    value = world * solves_per_step / (ms_per_step / 1e3)
+
+    # ---- e2e through the public API with pinned host buffers (copies inside the timed region)
+    e2e = None
+    if not a.no_e2e:
+        gforce_h = torch.empty((a.frames, V, 3), dtype=torch.float32).pin_memory()
+        n_e2e = max(1, min(2, a.steps))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            api.dxpbd_forward(sc, x0_h, v0_h, forces_h, a.frames)
+            api.dxpbd_backward(sc, kf, tg_h)
+            api.dxpbd_grads(sc, "forces", gforce_h)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e2e_ms = max(e0.elapsed_time(e1), 1e3 * wall) / n_e2e
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        h2d = 4 * (x0_h.numel() + v0_h.numel() + forces_h.numel() + tg_h.numel())
+        d2h = 4 * gforce_h.numel() + 4
+        e2e = {"value": world * solves_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+
+    # ---- roofline of the dominant kernel class
+    peaks = load_peaks()
+    peak = peaks["hbm_gbs"] if peaks else 6650.0
+    roof = None
+    if ktimes:
+        dom = max(ktimes, key=lambda k: ktimes[k][0])
+        ms, cnt = ktimes[dom]
+        b = algo_bytes(dom, E, V, max(cnt // max(1, a.steps), 1) if dom in ("dist_project", "dist_replay") else cnt)
+        if dom in ("dist_project", "dist_replay"):
+            # bytes per launch = per-constraint bytes x constraints of one color launch (average)
+            per_launch_units = E * a.iterations * substeps_total / max(cnt / a.steps, 1)
+            b = algo_bytes(dom, per_launch_units, V, 1)
+        avg_ms = ms / cnt
+        ach = (b / (avg_ms / 1e3)) / 1e9 if b else None
+        share = ms / sum(v[0] for v in ktimes.values())
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": None, "kernel": dom,
+                "avg_launch_ms": avg_ms, "launches": cnt, "share_of_kernel_time": share,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+
+    # ---- CPU baseline (oracle on a bounded crop, rank 0 at N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        r = oracle_sample(a.ref_n)
+        cpu = {"value": r["solves"] / r["t_total"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": r["sample"], "seconds": r["t_total"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "precision": "fp32 arithmetic, fp64 position state (DESIGN.md Precision)",
+            "data": "synthetic",
+            "config": {"workload": f"large_cloth {a.n}x{a.n} (BASELINE configs[4])" if a.n == 2944 else
+                       f"large_cloth {a.n}x{a.n} (reduced)", "vertices": V, "dof": 3 * V, "constraints": E,
+                       "frames": a.frames, "substeps": a.substeps, "iterations": a.iterations,
+                       "keyframes": kf.tolist(), "grads": "per-frame per-vertex forces",
+                       "cg_tol": a.cg_tol, "l2": "inputs larger than L2 (positions 277 MB fp64 state per GPU)",
+                       "parallelism": f"independent scene per GPU x{world}"},
+            "ms_per_substep_fwd": (sum(t_fwds) / a.steps) / substeps_total,
+            "ms_per_substep_fwd_adjoint": ms_per_step / substeps_total,
+            "cg_iters_per_substep": cg_iters / max(1, a.steps * substeps_total),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches, "create_s": t_create, "loss": loss,
+            "kernel_ms_per_step": {k: v[0] / a.steps for k, v in ktimes.items()},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = args_()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -150,6 +150,33 @@ int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out
  *  4: substeps solved, 5: worst final relative residual). */
 int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
 
+/* Kernel classes timed by the opt-in event profiler (dxpbd_profile / dxpbd_kernel_times). */
+#define DXPBD_K_PREDICT 0
+#define DXPBD_K_DIST_PROJECT 1
+#define DXPBD_K_CONTACT_PROJECT 2
+#define DXPBD_K_TET_PROJECT 3
+#define DXPBD_K_DIST_REPLAY 4
+#define DXPBD_K_CONTACT_REPLAY 5
+#define DXPBD_K_TET_REPLAY 6
+#define DXPBD_K_CG_VERTEX 7
+#define DXPBD_K_CG_DIST 8
+#define DXPBD_K_CG_TET 9
+#define DXPBD_K_CG_UPDATE 10
+#define DXPBD_K_CG_INIT 11
+#define DXPBD_K_RHS 12
+#define DXPBD_K_ADJOINT 13
+#define DXPBD_K_GRADS 14
+#define DXPBD_K_OTHER 15
+#define DXPBD_NUM_KCLASSES 16
+
+/* Enable (1) / disable (0) and reset the per-kernel-class CUDA-event profiler: when enabled,
+ * every kernel launch of the scene is bracketed by two events on the launching stream. */
+int dxpbd_profile(dxpbd_scene *scene, int32_t enable);
+
+/* Per-class totals since the last dxpbd_profile(scene, 1): HOST ms[n] (summed event time) and
+ * count[n] (launches).  Synchronizes the scene's recorded events. */
+int dxpbd_kernel_times(dxpbd_scene *scene, double *ms, double *count, int32_t n);
+
 /* Thread-local message of the last error ("" if none). */
 const char *dxpbd_last_error(void);
 

@@ -7,4 +7,5 @@ from . import api  # noqa: F401
 from .api import (  # noqa: F401
     dxpbd_create, dxpbd_destroy, dxpbd_forward, dxpbd_positions, dxpbd_backward, dxpbd_grads,
     dxpbd_set_params, dxpbd_coloring, dxpbd_stats, dxpbd_last_error, dxpbd_version,
+    dxpbd_profile, dxpbd_kernel_times,
 )

@@ -70,6 +70,8 @@ def lib():
             "dxpbd_set_params": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
             "dxpbd_coloring": ([vp, i32, vp, i64, vp], ctypes.c_int),
             "dxpbd_stats": ([vp, vp, i32], ctypes.c_int),
+            "dxpbd_profile": ([vp, i32], ctypes.c_int),
+            "dxpbd_kernel_times": ([vp, vp, vp, i32], ctypes.c_int),
             "dxpbd_last_error": ([], ctypes.c_char_p),
             "dxpbd_version": ([], ctypes.c_int),
         }
@@ -83,7 +85,11 @@ def lib():
 
 EXPORTED = ["dxpbd_create", "dxpbd_destroy", "dxpbd_forward", "dxpbd_positions", "dxpbd_backward",
             "dxpbd_grads", "dxpbd_set_params", "dxpbd_coloring", "dxpbd_stats", "dxpbd_last_error",
-            "dxpbd_version"]
+            "dxpbd_version", "dxpbd_profile", "dxpbd_kernel_times"]
+
+KCLASSES = ["predict", "dist_project", "contact_project", "tet_project", "dist_replay", "contact_replay",
+            "tet_replay", "cg_vertex", "cg_dist", "cg_tet", "cg_update", "cg_init", "rhs", "adjoint", "grads",
+            "other"]
 
 
 class DxpbdError(RuntimeError):
@@ -282,6 +288,18 @@ def dxpbd_stats(scene: DxScene) -> dict:
     _check(lib().dxpbd_stats(scene.handle, out.ctypes.data, 8), "dxpbd_stats")
     return dict(cg_iters_total=out[0], cg_iters_max=out[1], fwd_launches=out[2], bwd_launches=out[3],
                 solves=out[4], worst_relres=out[5], loss=out[6])
+
+
+def dxpbd_profile(scene: DxScene, enable: bool = True):
+    _check(lib().dxpbd_profile(scene.handle, int(bool(enable))), "dxpbd_profile")
+
+
+def dxpbd_kernel_times(scene: DxScene) -> dict:
+    n = len(KCLASSES)
+    ms = np.zeros(n, np.float64)
+    cnt = np.zeros(n, np.float64)
+    _check(lib().dxpbd_kernel_times(scene.handle, ms.ctypes.data, cnt.ctypes.data, n), "dxpbd_kernel_times")
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KCLASSES) if cnt[i] > 0}
 
 
 def dxpbd_last_error() -> str:

@@ -244,10 +244,37 @@ struct dxpbd_scene {
 
     // stats
     double stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // opt-in event profiler
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> prof_rec;   // (class, index of start event)
     double *h_scal = nullptr;   // pinned host scratch
 };
 
 namespace {
+
+inline void prof_begin(dxpbd_scene *s, int cls, cudaStream_t st) {
+    if (!s->prof) return;
+    if (s->ev_used + 2 > s->ev_pool.size()) {
+        size_t n0 = s->ev_pool.size(), n1 = std::max<size_t>(2 * n0, 1024);
+        s->ev_pool.resize(n1);
+        for (size_t i = n0; i < n1; ++i) DX_CHECK_CUDA(cudaEventCreate(&s->ev_pool[i]));
+    }
+    s->prof_rec.push_back({cls, s->ev_used});
+    DX_CHECK_CUDA(cudaEventRecord(s->ev_pool[s->ev_used], st));
+    s->ev_used += 2;
+}
+inline void prof_end(dxpbd_scene *s, cudaStream_t st) {
+    if (!s->prof) return;
+    DX_CHECK_CUDA(cudaEventRecord(s->ev_pool[s->prof_rec.back().second + 1], st));
+}
+#define LAUNCH(cls, ...)                 \
+    do {                                 \
+        prof_begin(s, (cls), st);        \
+        __VA_ARGS__;                     \
+        prof_end(s, st);                 \
+    } while (0)
 
 void upload(void *dst, const void *src, size_t bytes, int mem, cudaStream_t st) {
     if (!bytes) return;
@@ -277,8 +304,8 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int frame = n / s->substeps;
     double4 *xo = state(s, n + 1);
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
-    k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f, (double)s->dt,
-                                          1.0 / (double)s->dt, s->gravity, xo);
+    LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
+                                                                   (double)s->dt, 1.0 / (double)s->dt, s->gravity, xo));
     int launches = 1;
     const float inv_dt2 = s->inv_dt * s->inv_dt;
     const int K = s->iterations;
@@ -288,22 +315,22 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
             if (!rd && !wr)
-                k_dist_project<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo);
+                LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo));
             else if (!rd && wr)
-                k_dist_project<false, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo);
+                LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project<false, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo));
             else if (rd && wr)
-                k_dist_project<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo);
+                LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo));
             else
-                k_dist_project<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo);
+                LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo));
             ++launches;
         }
         launches += tet_forward_sweep(s->tets, k, K, inv_dt2, s->dt, xo, st);
         if (s->NC) {
             float at = s->coll_alpha * inv_dt2;
-            if (!rd && !wr) k_contact_project<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo);
-            else if (!rd && wr) k_contact_project<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo);
-            else if (rd && wr) k_contact_project<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo);
-            else k_contact_project<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo);
+            if (!rd && !wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
+            else if (!rd && wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
+            else if (rd && wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
+            else LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
             ++launches;
         }
     }
@@ -317,8 +344,8 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int frame = n / s->substeps;
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
     double4 *x = s->xr.p;
-    k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f, (double)s->dt,
-                                          1.0 / (double)s->dt, s->gravity, x);
+    LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
+                                                                   (double)s->dt, 1.0 / (double)s->dt, s->gravity, x));
     int launches = 1;
     const float inv_dt2 = s->inv_dt * s->inv_dt;
     const int K = s->iterations;
@@ -333,23 +360,23 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             if (!cnt) continue;
             float *eo = want_e ? s->ed.p : nullptr;
             if (first && last)
-                k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x);
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else if (first)
-                k_dist_replay<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x);
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else if (last)
-                k_dist_replay<false, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x);
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<false, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else
-                k_dist_replay<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x);
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             ++launches;
         }
         launches += tet_replay_sweep(s->tets, k, K, inv_dt2, s->dt, s->pd, x, st);
         if (s->NC) {
             float at = s->coll_alpha * inv_dt2;
             float *eo = want_ce ? s->ec.p : nullptr;
-            if (first && last) k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x);
-            else if (first) k_contact_replay<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x);
-            else if (last) k_contact_replay<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x);
-            else k_contact_replay<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x);
+            if (first && last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
+            else if (first) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
+            else if (last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
+            else LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
             ++launches;
         }
     }
@@ -364,7 +391,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     DX_CHECK_CUDA(cudaMemsetAsync(s->cg_sc.p, 0, sizeof(double) * (size_t)(maxit + 2) * 4, st));
     CGState cs{s->cg_sc.p, s->cg_sc.p + 2, s->cg_tol * s->cg_tol};
     const float *xw = s->inv_mass.p;
-    k_cg_init<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->ax.p, s->r.p, s->p.p, xw, cs);
+    LAUNCH(DXPBD_K_CG_INIT, k_cg_init<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->ax.p, s->r.p, s->p.p, xw, cs));
     int launches = 1;
     const float *Qc = s->NC ? s->Qc.p : nullptr;
     int it = 0;
@@ -374,14 +401,14 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         for (; it < end; ++it) {
-            k_cg_vertex<<<nblk(V), kBlock, 0, st>>>(V, it, s->p.p, s->r.p, s->q.p, xw, Qc, cs);
+            LAUNCH(DXPBD_K_CG_VERTEX, k_cg_vertex<<<nblk(V), kBlock, 0, st>>>(V, it, s->p.p, s->r.p, s->q.p, xw, Qc, cs));
             ++launches;
             if (E) {
-                k_cg_dist<<<nblk(E), kBlock, 0, st>>>(E, it, s->d_idx.p, s->Qd.p, s->p.p, s->q.p, xw, cs);
+                LAUNCH(DXPBD_K_CG_DIST, k_cg_dist<<<nblk(E), kBlock, 0, st>>>(E, it, s->d_idx.p, s->Qd.p, s->p.p, s->q.p, xw, cs));
                 ++launches;
             }
             launches += tet_cg_matvec(s->tets, it, s->p.p, s->q.p, xw, cs, st);
-            k_cg_update<<<nblk(V), kBlock, 0, st>>>(V, it, s->ax.p, s->r.p, s->p.p, s->q.p, xw, cs);
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update<<<nblk(V), kBlock, 0, st>>>(V, it, s->ax.p, s->r.p, s->p.p, s->q.p, xw, cs));
             ++launches;
         }
         // convergence check: rr of the last completed iteration
@@ -419,6 +446,7 @@ int dxpbd_destroy(dxpbd_scene *s) {
     if (!s) return DXPBD_OK;
     cudaSetDevice(s->device);
     if (s->h_scal) cudaFreeHost(s->h_scal);
+    for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
     delete s;
     return DXPBD_OK;
 }
@@ -658,7 +686,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     for (int k = 0; k < num_keys; ++k) key_of[key_frames[k] * sub] = k;   // duplicates: last wins
     // loss
     for (int k = 0; k < num_keys; ++k)
-        k_loss<<<nblk(V), kBlock, 0, st>>>(V, state(s, key_frames[k] * sub), s->targets.p + (size_t)k * V * 3, wts, s->acc.p);
+        LAUNCH(DXPBD_K_OTHER, k_loss<<<nblk(V), kBlock, 0, st>>>(V, state(s, key_frames[k] * sub), s->targets.p + (size_t)k * V * 3, wts, s->acc.p));
     // increment-form adjoint (kernels.cuh "adjoint"): y = u = 0 beyond the horizon
     auto tgt = [&](int n) -> const float * { return key_of[n] >= 0 ? s->targets.p + (size_t)key_of[n] * V * 3 : nullptr; };
     DX_CHECK_CUDA(cudaMemsetAsync(s->y.p, 0, sizeof(float4) * V, st));
@@ -674,11 +702,11 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         float *gf = g_forces ? s->g_force.p + (size_t)frame * V * 3 : nullptr;
         launches += replay_substep(s, n, st);
         // b = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1}
-        k_rhs_vertex<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, Qc, state(s, n + 1), tgt(n + 1), wts,
-                                                 s->rhs.p);
+        LAUNCH(DXPBD_K_RHS, k_rhs_vertex<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, Qc, state(s, n + 1), tgt(n + 1), wts,
+                                                 s->rhs.p));
         ++launches;
         if (E) {
-            k_rhs_dist<<<nblk(E), kBlock, 0, st>>>(E, s->d_idx.p, s->Qd.p, s->y.p, s->rhs.p, s->inv_mass.p);
+            LAUNCH(DXPBD_K_RHS, k_rhs_dist<<<nblk(E), kBlock, 0, st>>>(E, s->d_idx.p, s->Qd.p, s->y.p, s->rhs.p, s->inv_mass.p));
             ++launches;
         }
         launches += tet_rhs(s->tets, s->y.p, s->rhs.p, s->inv_mass.p, st);
@@ -689,22 +717,22 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         max_it = std::max(max_it, iters);
         worst = std::max(worst, rel);
         ++solves;
-        k_adjoint_accum<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, gf, s->dt);
+        LAUNCH(DXPBD_K_ADJOINT, k_adjoint_accum<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, gf, s->dt));
         ++launches;
         if (g_comp && E) {
-            k_grad_compliance<<<nblk(E), kBlock, 0, st>>>(E, s->d_idx.p, s->ed.p, s->y.p, s->g_comp.p);
+            LAUNCH(DXPBD_K_GRADS, k_grad_compliance<<<nblk(E), kBlock, 0, st>>>(E, s->d_idx.p, s->ed.p, s->y.p, s->g_comp.p));
             ++launches;
         }
         if (g_coll && s->NC) {
-            k_grad_colliders<<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->ec.p, s->y.p, s->acc.p + 1);
+            LAUNCH(DXPBD_K_GRADS, k_grad_colliders<<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->ec.p, s->y.p, s->acc.p + 1));
             ++launches;
         }
         launches += tet_grads(s->tets, s->y.p, st);
     }
     if (s->g_x0.n < (size_t)3 * V) s->g_x0.alloc((size_t)3 * V);
     if (s->g_v0.n < (size_t)3 * V) s->g_v0.alloc((size_t)3 * V);
-    k_adjoint_final<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, state(s, 0), tgt(0), wts, s->dt,
-                                                s->g_x0.p, s->g_v0.p);
+    LAUNCH(DXPBD_K_ADJOINT, k_adjoint_final<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, state(s, 0), tgt(0), wts, s->dt,
+                                                s->g_x0.p, s->g_v0.p));
     DX_CHECK_CUDA(cudaGetLastError());
     // loss to host
     double phi = 0.0;
@@ -824,6 +852,31 @@ int dxpbd_coloring(dxpbd_scene *s, int32_t family, int32_t *out, int64_t out_len
     DX_REQUIRE(out_len == (int64_t)c.size(), DXPBD_ERR_ARG, "out_len mismatch");
     std::memcpy(out, c.data(), sizeof(int32_t) * c.size());
     if (num_colors) *num_colors = family == 0 ? s->n_dist_colors : s->n_tet_colors;
+    DX_API_END
+}
+
+int dxpbd_profile(dxpbd_scene *s, int32_t enable) {
+    DX_API_BEGIN
+    DX_REQUIRE(s, DXPBD_ERR_ARG, "null scene");
+    DX_CHECK_CUDA(cudaSetDevice(s->device));
+    DX_CHECK_CUDA(cudaDeviceSynchronize());
+    s->prof = enable != 0;
+    s->prof_rec.clear();
+    s->ev_used = 0;
+    DX_API_END
+}
+
+int dxpbd_kernel_times(dxpbd_scene *s, double *ms, double *count, int32_t n) {
+    DX_API_BEGIN
+    DX_REQUIRE(s && ms && count, DXPBD_ERR_ARG, "null argument");
+    DX_CHECK_CUDA(cudaSetDevice(s->device));
+    for (int k = 0; k < n; ++k) ms[k] = count[k] = 0.0;
+    if (!s->prof_rec.empty()) DX_CHECK_CUDA(cudaEventSynchronize(s->ev_pool[s->prof_rec.back().second + 1]));
+    for (auto &r : s->prof_rec) {
+        float t = 0.f;
+        DX_CHECK_CUDA(cudaEventElapsedTime(&t, s->ev_pool[r.second], s->ev_pool[r.second + 1]));
+        if (r.first < n) { ms[r.first] += t; count[r.first] += 1; }
+    }
     DX_API_END
 }
 
