@@ -100,27 +100,79 @@ void color_sort(const std::vector<int32_t> &col, int nc, std::vector<int32_t> &p
     for (size_t j = 0; j < col.size(); ++j) perm[pos[col[j]]++] = (int32_t)j;
 }
 
-__global__ void k_pack4(int V, const float *__restrict__ x3, const float *__restrict__ w, float4 *__restrict__ out) {
+// Morton (Z-order) permutation of the rest positions: internal vertex i = user vertex perm[i]
+// (tiles of kTileV consecutive internal vertices are spatially compact).
+static inline uint64_t spread3(uint64_t x) {
+    x &= 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+void morton_order(const float *x, int V, std::vector<int32_t> &perm) {
+    float lo[3] = {x[0], x[1], x[2]}, hi[3] = {x[0], x[1], x[2]};
+    for (int i = 0; i < V; ++i)
+        for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], x[3 * i + k]); hi[k] = std::max(hi[k], x[3 * i + k]); }
+    float ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
+    double sc = ext > 0 ? 2097151.0 / ext : 0.0;
+    std::vector<std::pair<uint64_t, int32_t>> key(V);
+    for (int i = 0; i < V; ++i) {
+        uint64_t q[3];
+        for (int k = 0; k < 3; ++k) q[k] = (uint64_t)std::llround((x[3 * i + k] - lo[k]) * sc);
+        key[i] = {spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2), i};
+    }
+    std::sort(key.begin(), key.end());
+    perm.resize(V);
+    for (int i = 0; i < V; ++i) perm[i] = key[i].second;
+}
+
+// dst[i] = src[perm[i]] for [count][V][3] arrays (user -> internal vertex order)
+__global__ void k_gather3(int V, int count, const float *__restrict__ src, const int32_t *__restrict__ perm,
+                          float *__restrict__ dst) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)V * count) return;
+    size_t f = i / V, v = i % V;
+    const float *s = src + (f * V + perm[v]) * 3;
+    float *o = dst + i * 3;
+    o[0] = s[0]; o[1] = s[1]; o[2] = s[2];
+}
+// dst[perm[i]] = src[i] (internal -> user vertex order)
+__global__ void k_scatter3(int V, int count, const float *__restrict__ src, const int32_t *__restrict__ perm,
+                           float *__restrict__ dst) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)V * count) return;
+    size_t f = i / V, v = i % V;
+    const float *s = src + i * 3;
+    float *o = dst + (f * V + perm[v]) * 3;
+    o[0] = s[0]; o[1] = s[1]; o[2] = s[2];
+}
+__global__ void k_gather1(int V, const float *__restrict__ src, const int32_t *__restrict__ perm, float *__restrict__ dst) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < V) dst[i] = src[perm[i]];
+}
+// user-order [V][3] -> internal double4 / float4 (gathered through perm)
+__global__ void k_pack4d(int V, const float *__restrict__ x3, const int32_t *__restrict__ perm,
+                         const float *__restrict__ w, double4 *__restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= V) return;
-    out[i] = make_float4(x3[3 * i], x3[3 * i + 1], x3[3 * i + 2], w ? w[i] : 0.f);
+    int u = perm[i];
+    out[i] = make_double4(x3[3 * u], x3[3 * u + 1], x3[3 * u + 2], w ? (double)w[i] : 0.0);
 }
-__global__ void k_pack4d(int V, const float *__restrict__ x3, const float *__restrict__ w, double4 *__restrict__ out) {
+__global__ void k_pack4g(int V, const float *__restrict__ x3, const int32_t *__restrict__ perm, float4 *__restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= V) return;
-    out[i] = make_double4(x3[3 * i], x3[3 * i + 1], x3[3 * i + 2], w ? (double)w[i] : 0.0);
+    int u = perm[i];
+    out[i] = make_float4(x3[3 * u], x3[3 * u + 1], x3[3 * u + 2], 0.f);
 }
-__global__ void k_unpack3(int V, const double4 *__restrict__ x, float *__restrict__ out) {
+// internal double4 -> user-order [V][3] float
+__global__ void k_unpack3(int V, const double4 *__restrict__ x, const int32_t *__restrict__ perm, float *__restrict__ out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= V) return;
     double4 p = x[i];
-    out[3 * i] = (float)p.x; out[3 * i + 1] = (float)p.y; out[3 * i + 2] = (float)p.z;
-}
-__global__ void k_gather_i2(int n, const int32_t *__restrict__ src, const int32_t *__restrict__ perm, int2 *__restrict__ dst) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    int u = perm[j];
-    dst[j] = make_int2(src[2 * u], src[2 * u + 1]);
+    int u = perm[i];
+    out[3 * u] = (float)p.x; out[3 * u + 1] = (float)p.y; out[3 * u + 2] = (float)p.z;
 }
 __global__ void k_gather_f(int n, const float *__restrict__ src, const int32_t *__restrict__ perm, float *__restrict__ dst) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -184,12 +236,6 @@ __global__ void k_shape_grad(int nsph, int ncap, int ns, const double *__restric
     }
     if (s < 4 * nsph) gsph[s] = (float)acc[s];
 }
-__global__ void k_copy_xyz(int V, const float4 *__restrict__ a, float *__restrict__ out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= V) return;
-    float4 p = a[i];
-    out[3 * i] = p.x; out[3 * i + 1] = p.y; out[3 * i + 2] = p.z;
-}
 
 }  // namespace
 
@@ -212,7 +258,21 @@ struct dxpbd_scene {
     DBuf<int2> d_idx;
     DBuf<float> d_rest, d_alpha;
     DBuf<int32_t> d_perm;
-    DBuf<float> inv_mass;
+    DBuf<float> inv_mass;                 // internal vertex order
+    std::vector<int32_t> vperm_h;         // internal -> user vertex
+    DBuf<int32_t> vperm;
+    int ntiles = 0;
+    int64_t n_foreign = 0;
+    DBuf<int> d_seg;                      // [(n_dist_colors) * (ntiles+1)] (color, owner tile) offsets
+    DBuf<int> d_fseg, d_fidx;             // foreign (b-endpoint) constraint lists per (color, tile)
+    DBuf<int4> d_fent;                    // foreign entries {j, a, b, 0}
+    // CG-local tile structure (TMA-staged matvec, QF = 1)
+    bool use_tma = false;
+    int hcap = 0;
+    size_t tma_smem = 0;
+    DBuf<int> d_hoff, d_hlist, d_fpos;
+    DBuf<uint32_t> d_cpair, d_fpair;
+    DBuf<float4> d_fQ;
     // tets
     TetData tets;
     // colliders
@@ -232,7 +292,8 @@ struct dxpbd_scene {
 
     // backward
     DBuf<double4> xr;
-    DBuf<float4> ax, av, rhs, y, r, p, q;
+    DBuf<float4> ax, rhs, y, r, p, q, p1;
+    int qf = 0;   // Q format: 0 = sym6 SoA, 1 = iso+rank1 float4 (K = 1 with PD projection)
     DBuf<float> Qd, ed, Qc, ec;
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
     DBuf<float> cc_lam, cc_T, cc_sig, cc_B, cc_e;               // contact scratch (K>1)
@@ -359,7 +420,10 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
             float *eo = want_e ? s->ed.p : nullptr;
-            if (first && last)
+            if (first && last && s->qf == 1)
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true, 1><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x,
+                                                                                                   s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p));
+            else if (first && last)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else if (first)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
@@ -394,6 +458,10 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     LAUNCH(DXPBD_K_CG_INIT, k_cg_init<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->ax.p, s->r.p, s->p.p, xw, cs));
     int launches = 1;
     const float *Qc = s->NC ? s->Qc.p : nullptr;
+    CGBufs bufs{s->ax.p, s->r.p, s->p.p, s->p1.p, s->q.p, nullptr};
+    TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
+    TmaTiles tt{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_hoff.p, s->d_cpair.p, s->d_fpair.p,
+                s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p};
     int it = 0;
     const int chunk = 8;
     iters_out = -1;
@@ -401,14 +469,15 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         for (; it < end; ++it) {
-            LAUNCH(DXPBD_K_CG_VERTEX, k_cg_vertex<<<nblk(V), kBlock, 0, st>>>(V, it, s->p.p, s->r.p, s->q.p, xw, Qc, cs));
+            if (s->use_tma)
+                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(it, tt, V, s->hcap, Qc, bufs, xw, cs));
+            else if (s->qf == 1)
+                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
+            else
+                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<0><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             ++launches;
-            if (E) {
-                LAUNCH(DXPBD_K_CG_DIST, k_cg_dist<<<nblk(E), kBlock, 0, st>>>(E, it, s->d_idx.p, s->Qd.p, s->p.p, s->q.p, xw, cs));
-                ++launches;
-            }
             launches += tet_cg_matvec(s->tets, it, s->p.p, s->q.p, xw, cs, st);
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update<<<nblk(V), kBlock, 0, st>>>(V, it, s->ax.p, s->r.p, s->p.p, s->q.p, xw, cs));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update2<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, cs));
             ++launches;
         }
         // convergence check: rr of the last completed iteration
@@ -504,34 +573,166 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     s->pd = d->pd_projection;
     s->cg_tol = d->cg_tol > 0 ? d->cg_tol : 1e-6f;
     s->cg_max_iter = d->cg_max_iter > 0 ? d->cg_max_iter : 500;
+    s->qf = (s->iterations == 1 && s->pd) ? 1 : 0;
+
     cudaStream_t st = 0;
 
+    // vertex order: Morton order of the rest positions (host, create time)
+    morton_order(d->x_rest, V, s->vperm_h);
+    std::vector<int32_t> vinv(V);
+    for (int i = 0; i < V; ++i) vinv[s->vperm_h[i]] = i;
+    s->vperm.alloc(V);
+    upload(s->vperm.p, s->vperm_h.data(), sizeof(int32_t) * V, DXPBD_MEM_HOST, st);
+    s->ntiles = (V + kTileV - 1) / kTileV;
+    DBuf<float> tmpu;
+    tmpu.alloc((size_t)V * 3);
+    upload(tmpu.p, d->inv_mass, sizeof(float) * V, DXPBD_MEM_HOST, st);
     s->inv_mass.alloc(V);
-    upload(s->inv_mass.p, d->inv_mass, sizeof(float) * V, DXPBD_MEM_HOST, st);
-    DBuf<float> xr3;
+    k_gather1<<<nblk(V), kBlock, 0, st>>>(V, tmpu.p, s->vperm.p, s->inv_mass.p);
+    DBuf<float> xr3;   // internal order
     xr3.alloc((size_t)V * 3);
-    upload(xr3.p, d->x_rest, sizeof(float) * V * 3, DXPBD_MEM_HOST, st);
+    upload(tmpu.p, d->x_rest, sizeof(float) * V * 3, DXPBD_MEM_HOST, st);
+    k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, tmpu.p, s->vperm.p, xr3.p);
+    DX_CHECK_CUDA(cudaStreamSynchronize(st));
 
-    // distance constraints: greedy colors, color sort, SoA
+    // distance constraints: greedy colors in user order (R1), then sorted by (color, owner tile)
+    // with each constraint oriented (a < b) in internal ids; owner tile = a / kTileV.
     if (s->E) {
-        int nc = greedy_colors(s->E, 2, d->dist_idx, V, s->dist_color_h);
+        const int E = s->E;
+        int nc = greedy_colors(E, 2, d->dist_idx, V, s->dist_color_h);
         if (nc < 0) throw Err{DXPBD_ERR_LIMIT, "distance coloring needs more than 256 colors"};
         s->n_dist_colors = nc;
-        color_sort(s->dist_color_h, nc, s->dist_perm_h, s->dist_off);
-        DBuf<int32_t> idx_u;
+        const int nt = s->ntiles;
+        const size_t nkeys = (size_t)nc * nt;
+        std::vector<int2> ab(E);
+        std::vector<int64_t> cnt(nkeys + 1, 0);
+        std::vector<int32_t> key(E);
+        for (int j = 0; j < E; ++j) {
+            int a = vinv[d->dist_idx[2 * j]], b = vinv[d->dist_idx[2 * j + 1]];
+            if (a > b) std::swap(a, b);
+            ab[j] = make_int2(a, b);
+            key[j] = s->dist_color_h[j] * nt + a / kTileV;
+            cnt[key[j] + 1]++;
+        }
+        for (size_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
+        std::vector<int> seg((size_t)nc * (nt + 1));
+        s->dist_off.assign(nc + 1, 0);
+        for (int c = 0; c < nc; ++c) {
+            for (int t = 0; t <= nt; ++t) seg[(size_t)c * (nt + 1) + t] = (int)cnt[(size_t)c * nt + t];
+            s->dist_off[c] = (int)cnt[(size_t)c * nt];
+        }
+        s->dist_off[nc] = E;
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        s->dist_perm_h.assign(E, 0);
+        std::vector<int2> ab_sorted(E);
+        for (int j = 0; j < E; ++j) {
+            int64_t q = pos[key[j]]++;
+            s->dist_perm_h[q] = j;
+        }
+        // within each (color, tile) segment order by internal a (vertex-disjoint within a color, so
+        // a is unique there): consecutive threads touch consecutive Morton vertices (no smem bank
+        // conflicts in the tiled matvec); the Gauss-Seidel result does not depend on this order.
+        for (size_t kk = 0; kk < nkeys; ++kk)
+            std::sort(s->dist_perm_h.begin() + cnt[kk], s->dist_perm_h.begin() + cnt[kk + 1],
+                      [&](int32_t x, int32_t y) { return ab[x].x < ab[y].x; });
+        for (int q = 0; q < E; ++q) ab_sorted[q] = ab[s->dist_perm_h[q]];
+        s->d_seg.alloc(seg.size());
+        upload(s->d_seg.p, seg.data(), sizeof(int) * seg.size(), DXPBD_MEM_HOST, st);
+        // foreign lists: constraints whose b lies in another tile than a, keyed (color, tile(b))
+        {
+            std::vector<int64_t> fc(nkeys + 1, 0);
+            for (int q = 0; q < E; ++q) {
+                int ta = ab_sorted[q].x / kTileV, tb = ab_sorted[q].y / kTileV;
+                if (ta != tb) fc[(size_t)s->dist_color_h[s->dist_perm_h[q]] * nt + tb + 1]++;
+            }
+            for (size_t k = 0; k < nkeys; ++k) fc[k + 1] += fc[k];
+            std::vector<int> fseg((size_t)nc * (nt + 1));
+            for (int c = 0; c < nc; ++c)
+                for (int t = 0; t <= nt; ++t) fseg[(size_t)c * (nt + 1) + t] = (int)fc[(size_t)c * nt + t];
+            std::vector<int> fidx(std::max<int64_t>(fc[nkeys], 1));
+            std::vector<int64_t> fp(fc.begin(), fc.end() - 1);
+            for (int q = 0; q < E; ++q) {
+                int ta = ab_sorted[q].x / kTileV, tb = ab_sorted[q].y / kTileV;
+                if (ta != tb) fidx[fp[(size_t)s->dist_color_h[s->dist_perm_h[q]] * nt + tb]++] = q;
+            }
+            for (size_t kk = 0; kk < nkeys; ++kk)
+                std::sort(fidx.begin() + fc[kk], fidx.begin() + fc[kk + 1],
+                          [&](int x, int y) { return ab_sorted[x].y < ab_sorted[y].y; });
+            s->d_fseg.alloc(fseg.size());
+            upload(s->d_fseg.p, fseg.data(), sizeof(int) * fseg.size(), DXPBD_MEM_HOST, st);
+            s->d_fidx.alloc(fidx.size());
+            upload(s->d_fidx.p, fidx.data(), sizeof(int) * fidx.size(), DXPBD_MEM_HOST, st);
+            std::vector<int4> fent(fidx.size());
+            for (size_t q = 0; q < fidx.size(); ++q)
+                fent[q] = make_int4(fidx[q], ab_sorted[fidx[q]].x, ab_sorted[fidx[q]].y, 0);
+            s->d_fent.alloc(fent.size());
+            upload(s->d_fent.p, fent.data(), sizeof(int4) * fent.size(), DXPBD_MEM_HOST, st);
+            s->n_foreign = fc[nkeys];
+            // CG-local tile structure for the TMA-staged kernels (kernels.cuh "TMA-staged")
+            std::vector<std::vector<int>> halo(nt);
+            for (int q = 0; q < E; ++q) {
+                int a = ab_sorted[q].x, bb = ab_sorted[q].y, ta = a / kTileV, tb = bb / kTileV;
+                if (ta != tb) { halo[ta].push_back(bb); halo[tb].push_back(a); }
+            }
+            std::vector<int> hoff(nt + 1, 0);
+            int hmax = 0;
+            for (int t = 0; t < nt; ++t) {
+                std::sort(halo[t].begin(), halo[t].end());
+                halo[t].erase(std::unique(halo[t].begin(), halo[t].end()), halo[t].end());
+                hoff[t + 1] = hoff[t] + (int)halo[t].size();
+                hmax = std::max(hmax, (int)halo[t].size());
+            }
+            auto slot = [&](int t, int v) {
+                return (int)(std::lower_bound(halo[t].begin(), halo[t].end(), v) - halo[t].begin());
+            };
+            s->hcap = (hmax + 31) / 32 * 32;
+            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors;
+            if (s->use_tma) {
+                std::vector<int> hlist(std::max(hoff[nt], 1));
+                for (int t = 0; t < nt; ++t) std::copy(halo[t].begin(), halo[t].end(), hlist.begin() + hoff[t]);
+                std::vector<uint32_t> cpair(E + 4, 0), fpair((size_t)std::max<int64_t>(fc[nkeys], 1) + 4, 0);
+                std::vector<int> fposv(E, -1);
+                for (int q = 0; q < E; ++q) {
+                    int a = ab_sorted[q].x, bb = ab_sorted[q].y, ta = a / kTileV, tb = bb / kTileV;
+                    uint32_t la = (uint32_t)(a - ta * kTileV);
+                    uint32_t lb = ta == tb ? (uint32_t)(bb - ta * kTileV) : (uint32_t)(kTileV + slot(ta, bb));
+                    cpair[q] = la | (lb << 16);
+                }
+                for (int64_t k2 = 0; k2 < fc[nkeys]; ++k2) {
+                    int q = fidx[k2];
+                    int a = ab_sorted[q].x, bb = ab_sorted[q].y, tb = bb / kTileV;
+                    fpair[k2] = (uint32_t)(kTileV + slot(tb, a)) | ((uint32_t)(bb - tb * kTileV) << 16);
+                    fposv[q] = (int)k2;
+                }
+                s->d_hoff.alloc(hoff.size());
+                upload(s->d_hoff.p, hoff.data(), sizeof(int) * hoff.size(), DXPBD_MEM_HOST, st);
+                s->d_hlist.alloc(hlist.size());
+                upload(s->d_hlist.p, hlist.data(), sizeof(int) * hlist.size(), DXPBD_MEM_HOST, st);
+                s->d_cpair.alloc(cpair.size());
+                upload(s->d_cpair.p, cpair.data(), sizeof(uint32_t) * cpair.size(), DXPBD_MEM_HOST, st);
+                s->d_fpair.alloc(fpair.size());
+                upload(s->d_fpair.p, fpair.data(), sizeof(uint32_t) * fpair.size(), DXPBD_MEM_HOST, st);
+                s->d_fpos.alloc(E);
+                upload(s->d_fpos.p, fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
+                s->d_fQ.alloc((size_t)std::max<int64_t>(fc[nkeys], 1));
+                s->tma_smem = tma_smem_bytes(s->hcap);
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaStreamSynchronize(st));
+            }
+        }
         DBuf<float> alpha_u;
-        idx_u.alloc((size_t)2 * s->E);
-        alpha_u.alloc(s->E);
-        upload(idx_u.p, d->dist_idx, sizeof(int32_t) * 2 * s->E, DXPBD_MEM_HOST, st);
-        upload(alpha_u.p, d->dist_compliance, sizeof(float) * s->E, DXPBD_MEM_HOST, st);
-        s->d_perm.alloc(s->E);
-        upload(s->d_perm.p, s->dist_perm_h.data(), sizeof(int32_t) * s->E, DXPBD_MEM_HOST, st);
-        s->d_idx.alloc(s->E);
-        s->d_rest.alloc(s->E);
-        s->d_alpha.alloc(s->E);
-        k_gather_i2<<<nblk(s->E), kBlock, 0, st>>>(s->E, idx_u.p, s->d_perm.p, s->d_idx.p);
-        k_gather_f<<<nblk(s->E), kBlock, 0, st>>>(s->E, alpha_u.p, s->d_perm.p, s->d_alpha.p);
-        k_rest_len<<<nblk(s->E), kBlock, 0, st>>>(s->E, s->d_idx.p, xr3.p, s->d_rest.p);
+        alpha_u.alloc(E);
+        upload(alpha_u.p, d->dist_compliance, sizeof(float) * E, DXPBD_MEM_HOST, st);
+        s->d_perm.alloc(E);
+        upload(s->d_perm.p, s->dist_perm_h.data(), sizeof(int32_t) * E, DXPBD_MEM_HOST, st);
+        s->d_idx.alloc(E + 2);   // +2: the bulk copies round segment ends up to 16 bytes
+        DX_CHECK_CUDA(cudaMemsetAsync(s->d_idx.p, 0, sizeof(int2) * (E + 2), st));
+        upload(s->d_idx.p, ab_sorted.data(), sizeof(int2) * E, DXPBD_MEM_HOST, st);
+        s->d_rest.alloc(E);
+        s->d_alpha.alloc(E);
+        k_gather_f<<<nblk(E), kBlock, 0, st>>>(E, alpha_u.p, s->d_perm.p, s->d_alpha.p);
+        k_rest_len<<<nblk(E), kBlock, 0, st>>>(E, s->d_idx.p, xr3.p, s->d_rest.p);
         DX_CHECK_CUDA(cudaGetLastError());
         DX_CHECK_CUDA(cudaStreamSynchronize(st));
     }
@@ -595,14 +796,24 @@ int dxpbd_forward(dxpbd_scene *s, const float *x0, const float *v0, const float 
     DX_CHECK_CUDA(cudaSetDevice(s->device));
     cudaStream_t st = (cudaStream_t)stream;
     const int V = s->V;
-    upload(s->tmp3.p, x0, sizeof(float) * V * 3, mem, st);
-    k_pack4d<<<nblk(V), kBlock, 0, st>>>(V, s->tmp3.p, s->inv_mass.p, state(s, 0));
-    upload(s->tmp3.p, v0, sizeof(float) * V * 3, mem, st);
-    k_pack4<<<nblk(V), kBlock, 0, st>>>(V, s->tmp3.p, nullptr, s->v0.p);
+    // user vertex order -> internal (Morton) order at the boundary
+    const float *src = x0;
+    if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, x0, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
+    k_pack4d<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->inv_mass.p, state(s, 0));
+    src = v0;
+    if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, v0, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
+    k_pack4g<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->v0.p);
     s->have_forces = forces != nullptr;
     if (forces) {
         if (s->forces.n < (size_t)s->max_frames * V * 3) s->forces.alloc((size_t)s->max_frames * V * 3);
-        upload(s->forces.p, forces, sizeof(float) * (size_t)num_frames * V * 3, mem, st);
+        if (mem == DXPBD_MEM_HOST) {
+            for (int f = 0; f < num_frames; ++f) {
+                upload(s->tmp3.p, forces + (size_t)f * V * 3, sizeof(float) * V * 3, mem, st);
+                k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->tmp3.p, s->vperm.p, s->forces.p + (size_t)f * V * 3);
+            }
+        } else {
+            k_gather3<<<nblk((int64_t)V * num_frames), kBlock, 0, st>>>(V, num_frames, forces, s->vperm.p, s->forces.p);
+        }
     }
     int launches = 4;
     const int N = num_frames * s->substeps;
@@ -620,8 +831,12 @@ int dxpbd_positions(dxpbd_scene *s, int32_t frame, float *out, int32_t mem, void
     DX_REQUIRE(s->frames_done >= 0 && frame >= 0 && frame <= s->frames_done, DXPBD_ERR_STATE, "frame not simulated");
     DX_CHECK_CUDA(cudaSetDevice(s->device));
     cudaStream_t st = (cudaStream_t)stream;
-    k_unpack3<<<nblk(s->V), kBlock, 0, st>>>(s->V, state(s, frame * s->substeps), s->tmp3.p);
-    download(out, s->tmp3.p, sizeof(float) * s->V * 3, mem, st);
+    if (mem == DXPBD_MEM_HOST) {
+        k_unpack3<<<nblk(s->V), kBlock, 0, st>>>(s->V, state(s, frame * s->substeps), s->vperm.p, s->tmp3.p);
+        download(out, s->tmp3.p, sizeof(float) * s->V * 3, mem, st);
+    } else {
+        k_unpack3<<<nblk(s->V), kBlock, 0, st>>>(s->V, state(s, frame * s->substeps), s->vperm.p, out);
+    }
     DX_API_END
 }
 
@@ -640,7 +855,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     // buffers
     if (s->xr.n < (size_t)V) s->xr.alloc(V);
     auto ensure4 = [&](DBuf<float4> &b) { if (b.n < (size_t)V) b.alloc(V); };
-    ensure4(s->ax); ensure4(s->av); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q);
+    ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
     if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);
     const bool g_comp = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
     const bool g_forces = (s->grad_flags >> DXPBD_GRAD_FORCES) & 1;
@@ -664,12 +879,18 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     // targets
     if (num_keys) {
         if (s->targets.n < (size_t)num_keys * V * 3) s->targets.alloc((size_t)num_keys * V * 3);
-        upload(s->targets.p, targets, sizeof(float) * (size_t)num_keys * V * 3, mem, st);
+        for (int k = 0; k < num_keys; ++k) {
+            const float *src = targets + (size_t)k * V * 3;
+            if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, src, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
+            k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, src, s->vperm.p, s->targets.p + (size_t)k * V * 3);
+        }
     }
     const float *wts = nullptr;
     if (weights) {
         if (s->weights.n < (size_t)V) s->weights.alloc(V);
-        upload(s->weights.p, weights, sizeof(float) * V, mem, st);
+        const float *src = weights;
+        if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, weights, sizeof(float) * V, mem, st); src = s->tmp3.p; }
+        k_gather1<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->weights.p);
         wts = s->weights.p;
     }
     // gradient accumulators
@@ -701,12 +922,20 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         const int frame = n / sub;
         float *gf = g_forces ? s->g_force.p + (size_t)frame * V * 3 : nullptr;
         launches += replay_substep(s, n, st);
-        // b = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1}
-        LAUNCH(DXPBD_K_RHS, k_rhs_vertex<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, Qc, state(s, n + 1), tgt(n + 1), wts,
-                                                 s->rhs.p));
-        ++launches;
-        if (E) {
-            LAUNCH(DXPBD_K_RHS, k_rhs_dist<<<nblk(E), kBlock, 0, st>>>(E, s->d_idx.p, s->Qd.p, s->y.p, s->rhs.p, s->inv_mass.p));
+        // b = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1}   (one tiled pass, own vertices stored once)
+        {
+            TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
+            TmaTiles tt{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_hoff.p, s->d_cpair.p, s->d_fpair.p,
+                        s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p};
+            if (s->use_tma)
+                LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(
+                    tt, V, s->hcap, Qc, s->ax.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p));
+            else if (s->qf == 1)
+                LAUNCH(DXPBD_K_RHS, k_rhs_tiled<1><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->y.p,
+                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p));
+            else
+                LAUNCH(DXPBD_K_RHS, k_rhs_tiled<0><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->y.p,
+                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p));
             ++launches;
         }
         launches += tet_rhs(s->tets, s->y.p, s->rhs.p, s->inv_mass.p, st);
@@ -774,13 +1003,26 @@ int dxpbd_grads(dxpbd_scene *s, int32_t kind, float *out, int64_t out_len, int32
         case DXPBD_GRAD_X0:
         case DXPBD_GRAD_V0: {
             DX_REQUIRE(out_len == (int64_t)V * 3, DXPBD_ERR_ARG, "out_len must be 3V");
-            download(out, kind == DXPBD_GRAD_X0 ? s->g_x0.p : s->g_v0.p, sizeof(float) * V * 3, mem, st);
+            const float *g = kind == DXPBD_GRAD_X0 ? s->g_x0.p : s->g_v0.p;
+            if (mem == DXPBD_MEM_HOST) {
+                k_scatter3<<<nblk(V), kBlock, 0, st>>>(V, 1, g, s->vperm.p, s->tmp3.p);
+                download(out, s->tmp3.p, sizeof(float) * V * 3, mem, st);
+            } else {
+                k_scatter3<<<nblk(V), kBlock, 0, st>>>(V, 1, g, s->vperm.p, out);
+            }
             break;
         }
         case DXPBD_GRAD_FORCES: {
-            int64_t n = (int64_t)std::max(s->frames_done, 1) * V * 3;
-            DX_REQUIRE(out_len == n, DXPBD_ERR_ARG, "out_len must be frames*3V");
-            download(out, s->g_force.p, sizeof(float) * n, mem, st);
+            const int nf = std::max(s->frames_done, 1);
+            DX_REQUIRE(out_len == (int64_t)nf * V * 3, DXPBD_ERR_ARG, "out_len must be frames*3V");
+            if (mem == DXPBD_MEM_HOST) {
+                for (int f = 0; f < nf; ++f) {
+                    k_scatter3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->g_force.p + (size_t)f * V * 3, s->vperm.p, s->tmp3.p);
+                    download(out + (size_t)f * V * 3, s->tmp3.p, sizeof(float) * V * 3, mem, st);
+                }
+            } else {
+                k_scatter3<<<nblk((int64_t)V * nf), kBlock, 0, st>>>(V, nf, s->g_force.p, s->vperm.p, out);
+            }
             break;
         }
         case DXPBD_GRAD_SHAPE:

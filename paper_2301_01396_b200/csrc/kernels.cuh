@@ -121,12 +121,32 @@ struct DistScratch {   // per-constraint running state for iterations > 1 (SoA)
     float *lam, *sig, *B, *T, *e;   // lam[E], sig[3E], B[6E], T[E], e[3E]
 };
 
-template <bool FIRST, bool LAST>
+// Q formats: QF = 0 symmetric 3x3 in 6 SoA arrays; QF = 1 (K = 1 with PD projection only) the exact
+// closed form of psd(-B) for a single projection from lambda = 0: with sigma_s = -n/J,
+// -B = n n^T / J - (dl/len)(I - n n^T), so Q = c I + s n n^T, c = max(-dl/len, 0), s = 1/J - c,
+// stored as one float4 (u = n sqrt|s|, c with the sign of s; s < 0 implies c > 0).
+DX_INLINE float4 qpack_iso_rank1(float3 n, float dl, float inv_len, float J) {
+    float c = fmaxf(-dl * inv_len, 0.f);
+    float sv = 1.f / J - c;
+    float r = sqrtf(fabsf(sv));
+    return make_float4(r * n.x, r * n.y, r * n.z, sv >= 0.f ? c : -c);
+}
+DX_INLINE float3 qmul_iso_rank1(float4 Q, float3 d) {
+    float c = fabsf(Q.w);
+    float3 u = make_float3(Q.x, Q.y, Q.z);
+    float ud = dot3(u, d);
+    if (Q.w < 0.f) ud = -ud;
+    return make_float3(c * d.x + ud * u.x, c * d.y + ud * u.y, c * d.z + ud * u.z);
+}
+
+template <bool FIRST, bool LAST, int QF = 0>
 __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, int E, const int2 *__restrict__ idx,
                                                         const float *__restrict__ rest,
                                                         const float *__restrict__ alpha, float inv_dt2,
                                                         DistScratch sc, int pd, float *__restrict__ Qout,
-                                                        float *__restrict__ eout, double4 *__restrict__ x) {
+                                                        float *__restrict__ eout, double4 *__restrict__ x,
+                                                        const int *__restrict__ fpos = nullptr,
+                                                        float4 *__restrict__ fQ = nullptr) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= count) return;
     int j = begin + t;
@@ -161,7 +181,16 @@ __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, in
         x[ev.x] = pa;
         x[ev.y] = pb;
     }
-    if (LAST) {
+    if (LAST && QF == 1) {
+        // K = 1, PD projection on (host guarantees): closed form, no eigen-solve
+        float4 q4 = ok ? qpack_iso_rank1(o.n, o.dl, (float)(1.0 / o.len), o.J) : make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4 *>(Qout)[j] = q4;
+        if (fpos) {
+            const int fp = fpos[j];
+            if (fp >= 0) fQ[fp] = q4;   // copy for the tile of b (TMA-staged foreign list)
+        }
+        if (eout) { eout[j] = ec.x; eout[E + j] = ec.y; eout[2 * E + j] = ec.z; }
+    } else if (LAST) {
         Sym3 mB = Sym3{-B.xx, -B.xy, -B.xz, -B.yy, -B.yz, -B.zz};
         Sym3 Q = pd ? sym3_psd(mB) : mB;
         Qout[j] = Q.xx; Qout[E + j] = Q.xy; Qout[2 * E + j] = Q.xz;
@@ -420,84 +449,542 @@ __global__ void k_cg_init(int V, const float4 *__restrict__ b, float4 *__restric
     block_reduce_add<3>(acc, s.sc);   // slot 0
 }
 
-// per-vertex part of q = A p: q = M p + Qc p (contacts), and the p.q partial of these terms.
-// For it > 0 first updates p = M^-1 r + beta p with beta = rz(it)/rz(it-1) (slots it, it-1).
-__global__ void k_cg_vertex(int V, int it, float4 *__restrict__ p, const float4 *__restrict__ r,
-                            float4 *__restrict__ q, const float *__restrict__ wv,
-                            const float *__restrict__ Qc, CGState s) {
-    // slot index: sc slot (it+1) accumulates this iteration's p.q; slot it holds the current rz
+// distance-constraint part of q += sgn * Sum_j P_j^T Q_j P_j p (pinned rows filtered), tiled:
+// vertices are stored in Morton order; every constraint is oriented
+// (a < b) and owned by the tile of a; within each color the constraints are sorted by owner tile,
+// seg[c*(ntiles+1) + t] is the first constraint of color c owned by tile >= t.  One CTA per tile
+// walks its segment of every color, accumulates q for its own vertices in shared memory and
+// flushes each owned vertex with one vector reduction; only endpoints outside the tile (halo)
+// use global reductions.  With DOT it also accumulates p.(A p) = Sum_j d^T Q_j d.
+constexpr int kTileV = 1024;
+
+template <int QF>
+struct QVal {
+    Sym3 A;
+};
+template <>
+struct QVal<1> {
+    float4 A;
+};
+template <int QF>
+DX_INLINE QVal<QF> qload(const float *__restrict__ Q, int j, size_t E) {
+    QVal<QF> v;
+    if constexpr (QF == 1) {
+        v.A = reinterpret_cast<const float4 *>(Q)[j];
+    } else {
+        v.A = Sym3{Q[j], Q[E + j], Q[2 * E + j], Q[3 * E + j], Q[4 * E + j], Q[5 * E + j]};
+    }
+    return v;
+}
+template <int QF>
+DX_INLINE float3 qapply(const QVal<QF> &v, float3 d) {
+    if constexpr (QF == 1) return qmul_iso_rank1(v.A, d);
+    else return sym3_mul(v.A, d);
+}
+template <int QF>
+DX_INLINE float3 qmul(const float *__restrict__ Q, int j, size_t E, float3 d) {
+    if (QF == 1) return qmul_iso_rank1(reinterpret_cast<const float4 *>(Q)[j], d);
+    const Sym3 A = Sym3{Q[j], Q[E + j], Q[2 * E + j], Q[3 * E + j], Q[4 * E + j], Q[5 * E + j]};
+    return sym3_mul(A, d);
+}
+
+// Fused PCG iteration `it` (2 launches).  k_cg_matvec computes the new search direction
+//   p_it = M^-1 r_it + beta_it p_{it-1}   (beta_it = rz_it / rz_{it-1}; p_0 = M^-1 r_0 from init)
+// for its own vertices (stored to pbuf[it&1]) and on the fly for halo endpoints, then
+//   q = M p + Qc p + Sum_j P_j^T Q_j P_j p
+// for its own vertices completely: own constraints (a in tile) and "foreign" constraints (b in
+// tile, a outside; fidx lists them per color) are walked color by color; within one color the
+// constraints are vertex-disjoint (R1), so the shared-memory accumulation is a plain
+// read-modify-write with one barrier per color and no atomics; q is stored once per vertex.
+// p.q is accumulated over own vertices and own constraints only.
+struct CGBufs {
+    float4 *u, *r, *p0, *p1, *q, *qh;
+};
+struct TileLists {
+    int ncol, ntiles;
+    const int *seg;    // [ncol*(ntiles+1)] own-constraint ranges (sweep order)
+    const int *fseg;   // [ncol*(ntiles+1)] ranges into fidx
+    const int *fidx;   // foreign constraint ids
+    const int4 *fent;  // foreign entries {j, a, b, 0} (same order as fidx)
+};
+
+DX_INLINE float3 halo_p(int it, int v, float beta, const float4 *__restrict__ r, const float4 *__restrict__ pold,
+                        const float4 *__restrict__ pnew, const float *__restrict__ wv) {
+    if (it == 0) return f3(pnew[v]);
+    const float w = wv[v];
+    if (!(w > 0.f)) return make_float3(0.f, 0.f, 0.f);
+    const float4 rv = r[v], po = pold[v];
+    return make_float3(w * rv.x + beta * po.x, w * rv.y + beta * po.y, w * rv.z + beta * po.z);
+}
+
+template <int QF>
+__global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V, const int2 *__restrict__ idx,
+                                                      const float *__restrict__ Q, int E,
+                                                      const float *__restrict__ Qc, CGBufs B,
+                                                      const float *__restrict__ wv, CGState s) {
     if (cg_done(s, it + 1)) return;
-    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ float sp[3][kTileV];
+    __shared__ float sq[3][kTileV];
+    const int t = blockIdx.x;
+    const int v0 = t * kTileV;
+    const int nv = min(kTileV, V - v0);
+    const float4 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;   // p_{it-1}
+    float4 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;         // p_it
+    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
-    if (v < V) {
-        float w = wv[v];
-        float4 pv = p[v];
-        if (it > 0) {
-            double beta = s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1];
-            float bf = (float)beta;
-            float4 rv = r[v];
-            pv = make_float4(w * rv.x + bf * pv.x, w * rv.y + bf * pv.y, w * rv.z + bf * pv.z, 0.f);
-            p[v] = pv;
-        }
-        float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (w > 0.f) {
-            float m = 1.f / w;
-            float3 pp = f3(pv);
-            float3 qq = m * pp;
-            if (Qc) {
-                Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
-                              Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
-                qq = qq + sym3_mul(A, pp);
+    for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
+        float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 qv = make_float3(0.f, 0.f, 0.f);
+        if (i < nv) {
+            const int v = v0 + i;
+            const float w = wv[v];
+            if (it > 0) {
+                if (w > 0.f) {
+                    float4 rv = B.r[v], po = pold[v];
+                    pv = make_float4(w * rv.x + beta * po.x, w * rv.y + beta * po.y, w * rv.z + beta * po.z, 0.f);
+                }
+                pnew[v] = pv;
+            } else {
+                pv = pnew[v];
             }
-            qv = make_float4(qq.x, qq.y, qq.z, 0.f);
-            acc[0] = dot3(pp, qq);
+            if (w > 0.f) {
+                float3 pp = f3(pv);
+                qv = (1.f / w) * pp;
+                if (Qc) {
+                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                                  Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                    qv = qv + sym3_mul(A, pp);
+                }
+                acc[0] += dot3(pp, qv);
+            }
         }
-        q[v] = qv;
+        sp[0][i] = pv.x;
+        sp[1][i] = pv.y;
+        sp[2][i] = pv.z;
+        sq[0][i] = qv.x;
+        sq[1][i] = qv.y;
+        sq[2][i] = qv.z;
+    }
+    __syncthreads();
+    const int stride = L.ntiles + 1;
+    for (int c = 0; c < L.ncol; ++c) {
+        const int b = L.seg[c * stride + t], e = L.seg[c * stride + t + 1];
+        for (int j = b + threadIdx.x; j < e; j += blockDim.x) {
+            const int2 ab = idx[j];
+            const int la = ab.x - v0, lb = ab.y - v0;
+            const bool bl = lb < nv;
+            const float3 pa = make_float3(sp[0][la], sp[1][la], sp[2][la]);
+            const float3 pb = bl ? make_float3(sp[0][lb], sp[1][lb], sp[2][lb]) : halo_p(it, ab.y, beta, B.r, pold, pnew, wv);
+            const float3 d = pa - pb;
+            const float3 y = qmul<QF>(Q, j, E, d);
+            acc[0] += dot3(d, y);
+            sq[0][la] += y.x;
+            sq[1][la] += y.y;
+            sq[2][la] += y.z;
+            if (bl) {
+                sq[0][lb] -= y.x;
+                sq[1][lb] -= y.y;
+                sq[2][lb] -= y.z;
+            }
+        }
+        const int fb = L.fseg[c * stride + t], fe = L.fseg[c * stride + t + 1];
+        for (int k = fb + threadIdx.x; k < fe; k += blockDim.x) {
+            const int4 f4 = L.fent[k];   // {j, a, b}: b in tile, a outside
+            const int lb = f4.z - v0;
+            const float3 pa = halo_p(it, f4.y, beta, B.r, pold, pnew, wv);
+            const float3 d = pa - make_float3(sp[0][lb], sp[1][lb], sp[2][lb]);
+            const float3 y = qmul<QF>(Q, f4.x, E, d);
+            sq[0][lb] -= y.x;
+            sq[1][lb] -= y.y;
+            sq[2][lb] -= y.z;
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        const int v = v0 + i;
+        B.q[v] = wv[v] > 0.f ? make_float4(sq[0][i], sq[1][i], sq[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// distance-constraint part of q = A p: q_a += Q d, q_b -= Q d with d = p_a - p_b (pinned rows
-// filtered), and its p.q partial d^T Q d.
-__global__ void __launch_bounds__(kBlock) k_cg_dist(int E, int it, const int2 *__restrict__ idx,
-                                                    const float *__restrict__ Q, const float4 *__restrict__ p,
-                                                    float4 *__restrict__ q, const float *__restrict__ wv,
-                                                    CGState s) {
+// ---------------------------------------------------------------------------------------------
+// TMA-staged tiled kernels (QF = 1).  CG-local tile structure (built at create):
+//   halo list of tile t: every vertex outside the tile touched by a constraint that updates a
+//   vertex of the tile; its values are loaded once into shared-memory slots kTileV + h.
+//   cpair[j] (own constraint j, a in tile): la | lb' << 16, lb' = b - v0 or kTileV + halo slot.
+//   fpair[k] (foreign entry k, b in tile, a outside): (kTileV + slot(a)) | (b - v0) << 16, with its
+//   own copy fQ[k] of Q_j written by the replay; foreign entries are grouped by (color, tile).
+// Per color c the own range [seg(c,t), seg(c,t+1)) of cpair / Q and the foreign range
+// [fseg(c,t), fseg(c,t+1)) of fpair / fQ are contiguous: thread 0 stages them with bulk async
+// copies (cp.async.bulk -> mbarrier complete_tx) kTmaStages colors ahead; all threads then work
+// purely in shared memory (plain read-modify-write of the accumulator, one barrier per color,
+// vertex-disjoint within a color by R1).
+constexpr int kTmaStages = 3;
+constexpr int kFCap = 256;
+constexpr int kTmaThreads = 512;
+
+struct TmaTiles {
+    int ncol, ntiles;
+    const int *seg, *fseg, *hoff;
+    const uint32_t *cpair, *fpair;
+    const int *hlist;
+    const float4 *Q4, *fQ;
+};
+
+struct TmaStage {
+    uint32_t cp[kTileV + 4];
+    float4 q[kTileV];
+    uint32_t fp[kFCap + 4];
+    float4 fq[kFCap];
+};
+// dynamic smem: [bars][stages][sq 3*kTileV][sp 3*(kTileV + hcap)]
+__host__ __device__ inline size_t tma_smem_bytes(int hcap) {
+    return 64 + sizeof(TmaStage) * kTmaStages + sizeof(float) * 3 * kTileV + sizeof(float) * 3 * (kTileV + hcap);
+}
+
+constexpr int kMaxColors = 64;   // bounds table in shared memory (more colors: generic kernel)
+
+DX_INLINE void tma_issue(uint64_t *bar, TmaStage &S, int c, const int *sb, const TmaTiles &T) {
+    const int b = sb[4 * c], e = sb[4 * c + 1];
+    const int fb = sb[4 * c + 2], fe = sb[4 * c + 3];
+    const int nf = min(fe - fb, kFCap);
+    uint32_t tot = 0;
+    size_t c0 = 0, c1 = 0, f0 = 0, f1 = 0;
+    if (e > b) {
+        c0 = ((size_t)b * 4) & ~(size_t)15;
+        c1 = ((size_t)e * 4 + 15) & ~(size_t)15;
+        tot += (uint32_t)(c1 - c0) + (uint32_t)(e - b) * 16u;
+    }
+    if (nf > 0) {
+        f0 = ((size_t)fb * 4) & ~(size_t)15;
+        f1 = ((size_t)(fb + nf) * 4 + 15) & ~(size_t)15;
+        tot += (uint32_t)(f1 - f0) + (uint32_t)nf * 16u;
+    }
+    mbar_expect_tx(bar, tot);
+    if (e > b) {
+        bulk_g2s(S.cp, reinterpret_cast<const char *>(T.cpair) + c0, (uint32_t)(c1 - c0), bar);
+        bulk_g2s(S.q, T.Q4 + b, (uint32_t)(e - b) * 16u, bar);
+    }
+    if (nf > 0) {
+        bulk_g2s(S.fp, reinterpret_cast<const char *>(T.fpair) + f0, (uint32_t)(f1 - f0), bar);
+        bulk_g2s(S.fq, T.fQ + fb, (uint32_t)nf * 16u, bar);
+    }
+}
+
+// Walk all colors of tile t.  sp: values (own then halo slots), sq: own accumulator.
+// SIGN +1: sq += A_dist sp (CG, also accumulates sp.(A sp) over own constraints); SIGN -1: sq -= ...
+template <int SIGN>
+DX_INLINE float tma_tile_colors(uint64_t *bars, TmaStage *stages, float (*sp)[1], int spn, float *sq0, const int *sb,
+                                const TmaTiles &T) {
+    float dotacc = 0.f;
+    float *sp0 = &sp[0][0];
+    float *sp1 = sp0 + spn, *sp2 = sp0 + 2 * spn;
+    float *sq1 = sq0 + kTileV, *sq2 = sq0 + 2 * kTileV;
+    for (int c = 0; c < T.ncol; ++c) {
+        const int st = c % kTmaStages;
+        TmaStage &S = stages[st];
+        mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
+        const int b = sb[4 * c], e = sb[4 * c + 1];
+        const int off = (int)((((size_t)b * 4) & 15) >> 2);
+        for (int i = threadIdx.x; i < e - b; i += blockDim.x) {
+            const uint32_t pr = S.cp[off + i];
+            const float4 q4 = S.q[i];
+            const int la = pr & 0xffff, lb = pr >> 16;
+            const float3 d = make_float3(sp0[la] - sp0[lb], sp1[la] - sp1[lb], sp2[la] - sp2[lb]);
+            float3 y = qmul_iso_rank1(q4, d);
+            if (SIGN > 0) dotacc += dot3(d, y);
+            else y = -y;
+            sq0[la] += y.x;
+            sq1[la] += y.y;
+            sq2[la] += y.z;
+            if (lb < kTileV) {
+                sq0[lb] -= y.x;
+                sq1[lb] -= y.y;
+                sq2[lb] -= y.z;
+            }
+        }
+        const int fb = sb[4 * c + 2], fe = sb[4 * c + 3];
+        const int foff = (int)((((size_t)fb * 4) & 15) >> 2);
+        for (int i = threadIdx.x; i < fe - fb; i += blockDim.x) {
+            const uint32_t pr = i < kFCap ? S.fp[foff + i] : T.fpair[fb + i];
+            const float4 q4 = i < kFCap ? S.fq[i] : T.fQ[fb + i];
+            const int la = pr & 0xffff, lb = pr >> 16;   // la: halo slot of a, lb: own b
+            const float3 d = make_float3(sp0[la] - sp0[lb], sp1[la] - sp1[lb], sp2[la] - sp2[lb]);
+            float3 y = qmul_iso_rank1(q4, d);
+            if (SIGN < 0) y = -y;
+            sq0[lb] -= y.x;
+            sq1[lb] -= y.y;
+            sq2[lb] -= y.z;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && c + kTmaStages < T.ncol) {
+            fence_proxy_async();
+            tma_issue(&bars[st], S, c + kTmaStages, sb, T);
+        }
+    }
+    return dotacc;
+}
+
+// Fused PCG matvec (see k_cg_matvec): p_it update for own and halo vertices, q = A p, p.q.
+__global__ void __launch_bounds__(kTmaThreads, 2) k_cg_matvec_tma(int it, TmaTiles T, int V, int hcap,
+                                                                  const float *__restrict__ Qc, CGBufs B,
+                                                                  const float *__restrict__ wv, CGState s) {
     if (cg_done(s, it + 1)) return;
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 64);
+    float *sq = reinterpret_cast<float *>(smem_raw + 64 + sizeof(TmaStage) * kTmaStages);
+    float *sp = sq + 3 * kTileV;
+    const int spn = kTileV + hcap;
+    const int t = blockIdx.x;
+    const int v0 = t * kTileV;
+    const int nv = min(kTileV, V - v0);
+    __shared__ int sb[4 * kMaxColors];   // per-color (b, e, fb, fe) of this tile
+    {
+        const int stride = T.ntiles + 1;
+        for (int c = threadIdx.x; c < T.ncol; c += blockDim.x) {
+            sb[4 * c] = T.seg[c * stride + t];
+            sb[4 * c + 1] = T.seg[c * stride + t + 1];
+            sb[4 * c + 2] = T.fseg[c * stride + t];
+            sb[4 * c + 3] = T.fseg[c * stride + t + 1];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
+        fence_mbar_init();
+        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages[c], c, sb, T);
+    }
+    const float4 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
+    float4 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
+    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
-    if (j < E) {
-        int2 e = idx[j];
-        float4 pa = p[e.x], pb = p[e.y];   // p is zero on pinned vertices
-        float3 d = f3(pa) - f3(pb);
-        Sym3 A = Sym3{Q[j], Q[E + j], Q[2 * (size_t)E + j], Q[3 * (size_t)E + j], Q[4 * (size_t)E + j],
-                      Q[5 * (size_t)E + j]};
-        float3 y = sym3_mul(A, d);
-        acc[0] = dot3(d, y);
-        if (wv[e.x] > 0.f) red_add_f4(q + e.x, make_float4(y.x, y.y, y.z, 0.f));
-        if (wv[e.y] > 0.f) red_add_f4(q + e.y, make_float4(-y.x, -y.y, -y.z, 0.f));
+    for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
+        float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 qv = make_float3(0.f, 0.f, 0.f);
+        if (i < nv) {
+            const int v = v0 + i;
+            const float w = wv[v];
+            if (it > 0) {
+                if (w > 0.f) {
+                    float4 rv = B.r[v], po = pold[v];
+                    pv = make_float4(w * rv.x + beta * po.x, w * rv.y + beta * po.y, w * rv.z + beta * po.z, 0.f);
+                }
+                pnew[v] = pv;
+            } else {
+                pv = pnew[v];
+            }
+            if (w > 0.f) {
+                float3 pp = f3(pv);
+                qv = (1.f / w) * pp;
+                if (Qc) {
+                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                                  Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                    qv = qv + sym3_mul(A, pp);
+                }
+                acc[0] += dot3(pp, qv);
+            }
+        }
+        sp[i] = pv.x;
+        sp[spn + i] = pv.y;
+        sp[2 * spn + i] = pv.z;
+        sq[i] = qv.x;
+        sq[kTileV + i] = qv.y;
+        sq[2 * kTileV + i] = qv.z;
+    }
+    const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
+    for (int h = threadIdx.x; h < nh; h += blockDim.x) {
+        const int v = T.hlist[h0 + h];
+        const float3 pv = halo_p(it, v, beta, B.r, pold, pnew, wv);
+        sp[kTileV + h] = pv.x;
+        sp[spn + kTileV + h] = pv.y;
+        sp[2 * spn + kTileV + h] = pv.z;
+    }
+    __syncthreads();
+    acc[0] += tma_tile_colors<1>(bars, stages, reinterpret_cast<float (*)[1]>(sp), spn, sq, sb, T);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        const int v = v0 + i;
+        B.q[v] = wv[v] > 0.f ? make_float4(sq[i], sq[kTileV + i], sq[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// y += alpha p, r -= alpha q, alpha = rz(it) / pq(it+1); accumulates rz and rr into slot it+1.
-__global__ void k_cg_update(int V, int it, float4 *__restrict__ y, float4 *__restrict__ r,
-                            const float4 *__restrict__ p, const float4 *__restrict__ q,
-                            const float *__restrict__ wv, CGState s) {
+// Increment-system right-hand side: b = M u + dphi - Qc y - A_dist y (own vertices).
+__global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
+                                                            const float4 *__restrict__ u, const float4 *__restrict__ y,
+                                                            const double4 *__restrict__ xkey, const float *__restrict__ target,
+                                                            const float *__restrict__ weights, const float *__restrict__ wv,
+                                                            float4 *__restrict__ bout) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 64);
+    float *sq = reinterpret_cast<float *>(smem_raw + 64 + sizeof(TmaStage) * kTmaStages);
+    float *sp = sq + 3 * kTileV;
+    const int spn = kTileV + hcap;
+    const int t = blockIdx.x;
+    const int v0 = t * kTileV;
+    const int nv = min(kTileV, V - v0);
+    __shared__ int sb[4 * kMaxColors];   // per-color (b, e, fb, fe) of this tile
+    {
+        const int stride = T.ntiles + 1;
+        for (int c = threadIdx.x; c < T.ncol; c += blockDim.x) {
+            sb[4 * c] = T.seg[c * stride + t];
+            sb[4 * c + 1] = T.seg[c * stride + t + 1];
+            sb[4 * c + 2] = T.fseg[c * stride + t];
+            sb[4 * c + 3] = T.fseg[c * stride + t + 1];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
+        fence_mbar_init();
+        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages[c], c, sb, T);
+    }
+    for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
+        float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 rr = make_float3(0.f, 0.f, 0.f);
+        if (i < nv) {
+            const int v = v0 + i;
+            const float w = wv[v];
+            yv = y[v];
+            if (w > 0.f) {
+                rr = (1.f / w) * f3(u[v]);
+                if (Qc) {
+                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                                  Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                    rr = rr - sym3_mul(A, f3(yv));
+                }
+                if (target) {
+                    double4 x = xkey[v];
+                    float W = weights ? weights[v] : 1.f;
+                    rr = rr + W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
+                                              (float)(x.z - target[3 * v + 2]));
+                }
+            }
+        }
+        sp[i] = yv.x;
+        sp[spn + i] = yv.y;
+        sp[2 * spn + i] = yv.z;
+        sq[i] = rr.x;
+        sq[kTileV + i] = rr.y;
+        sq[2 * kTileV + i] = rr.z;
+    }
+    const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
+    for (int h = threadIdx.x; h < nh; h += blockDim.x) {
+        const float4 yv = y[T.hlist[h0 + h]];
+        sp[kTileV + h] = yv.x;
+        sp[spn + kTileV + h] = yv.y;
+        sp[2 * spn + kTileV + h] = yv.z;
+    }
+    __syncthreads();
+    tma_tile_colors<-1>(bars, stages, reinterpret_cast<float (*)[1]>(sp), spn, sq, sb, T);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        const int v = v0 + i;
+        bout[v] = wv[v] > 0.f ? make_float4(sq[i], sq[kTileV + i], sq[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// right-hand side of the increment system (kernels "adjoint"):
+//   b = M u_next + dphi/dx_{n+1} - Qc y_next - Sum_j P_j^T Q_j P_j y_next   (own vertices, one store)
+template <int QF>
+__global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const int2 *__restrict__ idx,
+                                                      const float *__restrict__ Q, int E, const float *__restrict__ Qc,
+                                                      const float4 *__restrict__ u, const float4 *__restrict__ y,
+                                                      const double4 *__restrict__ xkey, const float *__restrict__ target,
+                                                      const float *__restrict__ weights, const float *__restrict__ wv,
+                                                      float4 *__restrict__ b) {
+    __shared__ float sy[3][kTileV];
+    __shared__ float sq[3][kTileV];
+    const int t = blockIdx.x;
+    const int v0 = t * kTileV;
+    const int nv = min(kTileV, V - v0);
+    for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
+        float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 r = make_float3(0.f, 0.f, 0.f);
+        if (i < nv) {
+            const int v = v0 + i;
+            const float w = wv[v];
+            yv = y[v];
+            if (w > 0.f) {
+                r = (1.f / w) * f3(u[v]);
+                if (Qc) {
+                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                                  Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                    r = r - sym3_mul(A, f3(yv));
+                }
+                if (target) {
+                    double4 x = xkey[v];
+                    float W = weights ? weights[v] : 1.f;
+                    r = r + W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
+                                            (float)(x.z - target[3 * v + 2]));
+                }
+            }
+        }
+        sy[0][i] = yv.x;
+        sy[1][i] = yv.y;
+        sy[2][i] = yv.z;
+        sq[0][i] = r.x;
+        sq[1][i] = r.y;
+        sq[2][i] = r.z;
+    }
+    __syncthreads();
+    const int stride = L.ntiles + 1;
+    for (int c = 0; c < L.ncol; ++c) {
+        const int bb = L.seg[c * stride + t], e = L.seg[c * stride + t + 1];
+        for (int j = bb + threadIdx.x; j < e; j += blockDim.x) {
+            const int2 ab = idx[j];
+            const int la = ab.x - v0, lb = ab.y - v0;
+            const bool bl = lb < nv;
+            const float3 d = make_float3(sy[0][la], sy[1][la], sy[2][la]) -
+                             (bl ? make_float3(sy[0][lb], sy[1][lb], sy[2][lb]) : f3(y[ab.y]));
+            const float3 q = qmul<QF>(Q, j, E, d);
+            sq[0][la] -= q.x;
+            sq[1][la] -= q.y;
+            sq[2][la] -= q.z;
+            if (bl) {
+                sq[0][lb] += q.x;
+                sq[1][lb] += q.y;
+                sq[2][lb] += q.z;
+            }
+        }
+        const int fb = L.fseg[c * stride + t], fe = L.fseg[c * stride + t + 1];
+        for (int k = fb + threadIdx.x; k < fe; k += blockDim.x) {
+            const int j = L.fidx[k];
+            const int2 ab = idx[j];
+            const int lb = ab.y - v0;
+            const float3 d = f3(y[ab.x]) - make_float3(sy[0][lb], sy[1][lb], sy[2][lb]);
+            const float3 q = qmul<QF>(Q, j, E, d);
+            sq[0][lb] += q.x;
+            sq[1][lb] += q.y;
+            sq[2][lb] += q.z;
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        const int v = v0 + i;
+        b[v] = wv[v] > 0.f ? make_float4(sq[0][i], sq[1][i], sq[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// u += alpha p_it, r -= alpha q; accumulates rz = r.M^-1 r and rr = r.r (slot it+1)
+__global__ void k_cg_update2(int V, int it, CGBufs B, const float *__restrict__ wv, CGState s) {
     if (cg_done(s, it + 1)) return;
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     float acc[2] = {0.f, 0.f};
     if (v < V) {
+        const float4 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
         double pq = s.sc[(it + 1) * 4 + 0];
         float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
         float w = wv[v];
-        float4 yv = y[v], rv = r[v], pv = p[v], qv = q[v];
-        yv.x += alpha * pv.x; yv.y += alpha * pv.y; yv.z += alpha * pv.z;
+        float4 uv = B.u[v], rv = B.r[v], pv = p[v], qv = B.q[v];
+        uv.x += alpha * pv.x; uv.y += alpha * pv.y; uv.z += alpha * pv.z;
         rv.x -= alpha * qv.x; rv.y -= alpha * qv.y; rv.z -= alpha * qv.z;
-        y[v] = yv;
-        r[v] = rv;
-        acc[0] = w * (rv.x * rv.x + rv.y * rv.y + rv.z * rv.z);
-        acc[1] = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
+        if (!(w > 0.f)) rv = make_float4(0.f, 0.f, 0.f, 0.f);
+        B.u[v] = uv;
+        B.r[v] = rv;
+        float r2 = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
+        acc[0] = w * r2;
+        acc[1] = r2;
     }
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
 }
@@ -510,48 +997,6 @@ __global__ void k_cg_update(int V, int it, float4 *__restrict__ y, float4 *__res
 //   A_n u_n = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1},   y_n = y_{n+1} + u_n,
 // algebraically identical, but the PCG tolerance is relative to the (small) increment instead of
 // being integrated twice by the second difference.  Pinned rows are filtered (R11).
-// b = M u_next + dphi_{n+1} - Qc y_next   (vertex part)
-__global__ void k_rhs_vertex(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
-                             const float4 *__restrict__ y, const float *__restrict__ Qc,
-                             const double4 *__restrict__ xkey, const float *__restrict__ target,
-                             const float *__restrict__ weights, float4 *__restrict__ b) {
-    int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= V) return;
-    float w = wv[v];
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (w > 0.f) {
-        float3 r = (1.f / w) * f3(u[v]);
-        if (Qc) {
-            Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v], Qc[4 * (size_t)V + v],
-                          Qc[5 * (size_t)V + v]};
-            r = r - sym3_mul(A, f3(y[v]));
-        }
-        if (target) {
-            double4 x = xkey[v];
-            float W = weights ? weights[v] : 1.f;
-            r = r + W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
-                                    (float)(x.z - target[3 * v + 2]));
-        }
-        o = make_float4(r.x, r.y, r.z, 0.f);
-    }
-    b[v] = o;
-}
-
-// b_a -= Q_j (y_a - y_b), b_b += Q_j (y_a - y_b)   (distance-constraint part of -Q y)
-__global__ void __launch_bounds__(kBlock) k_rhs_dist(int E, const int2 *__restrict__ idx, const float *__restrict__ Q,
-                                                     const float4 *__restrict__ y, float4 *__restrict__ b,
-                                                     const float *__restrict__ wv) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= E) return;
-    int2 e = idx[j];
-    float3 d = f3(y[e.x]) - f3(y[e.y]);
-    Sym3 A = Sym3{Q[j], Q[E + j], Q[2 * (size_t)E + j], Q[3 * (size_t)E + j], Q[4 * (size_t)E + j],
-                  Q[5 * (size_t)E + j]};
-    float3 q = sym3_mul(A, d);
-    if (wv[e.x] > 0.f) red_add_f4(b + e.x, make_float4(-q.x, -q.y, -q.z, 0.f));
-    if (wv[e.y] > 0.f) red_add_f4(b + e.y, make_float4(q.x, q.y, q.z, 0.f));
-}
-
 // after the solve: y_n = y_{n+1} + u_n ; dphi/df_frame += dt^2 y_n (R8)
 __global__ void k_adjoint_accum(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
                                 float4 *__restrict__ y, float *__restrict__ gforce, float dt) {
