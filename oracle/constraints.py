@@ -140,13 +140,13 @@ def tet_hyd_F(F: np.ndarray, gamma: np.ndarray):
     return C, P, HF
 
 
-def tet(xs: np.ndarray, Dminv: np.ndarray, G: np.ndarray, kind: str, gamma=None):
-    """Returns C, g (T,12) = G^T dC/dvecF, H (T,12,12) = G^T H_F G."""
+def tet(xs: np.ndarray, Dminv: np.ndarray, G: np.ndarray, kind: str, gamma=None, need_H=True):
+    """Returns C, g (T,12) = G^T dC/dvecF, H (T,12,12) = G^T H_F G (None if not need_H)."""
     F = tet_F(xs, Dminv)
     if kind == "D":
         C, P, HF = tet_dev_F(F)
     else:
         C, P, HF = tet_hyd_F(F, gamma)
     g = np.einsum("nij,ni->nj", G, P)
-    H = np.einsum("nai,nab,nbj->nij", G, HF, G)
+    H = np.einsum("nai,nab,nbj->nij", G, HF, G) if need_H else None
     return C, g, H

@@ -207,7 +207,7 @@ class OracleModel:
         return _rows1(dict(C=C, g=g, H=H, len=l, dCdu=np.zeros((n, 1)), dgdu=np.zeros((n, 1, 6)),
                            datdu=np.full((n, 1), 1.0 / self.dt ** 2)))
 
-    def ev_tet(self, x, grp):
+    def ev_tet(self, x, grp, need_H=True):
         """stable Neo-Hookean block (PAPER.md Sec.5.2, R6): rows (C_D, C_H) solved together;
         controls u = (a, b), mu = a^2, lambda = b^2, alpha_D = 1/(mu V), alpha_H = 1/(lambda V),
         gamma = 1 + mu/lambda."""
@@ -215,14 +215,15 @@ class OracleModel:
         a, b, V = self.ta[grp], self.tb[grp], self.vol[grp]
         dt2 = self.dt ** 2
         st = self.tet_idx[grp]
-        CD, gD, HD = cf.tet(x[st], self.Dminv[grp], self.G[grp], "D")
-        CH, gH, HH = cf.tet(x[st], self.Dminv[grp], self.G[grp], "H", self.gamma[grp])
+        CD, gD, HD = cf.tet(x[st], self.Dminv[grp], self.G[grp], "D", need_H=need_H)
+        CH, gH, HH = cf.tet(x[st], self.Dminv[grp], self.G[grp], "H", self.gamma[grp], need_H=need_H)
         z = np.zeros(n)
         datdu = np.stack([np.stack([-2.0 / (a ** 3 * V * dt2), z], 1),        # d/da (rows D, H)
                           np.stack([z, -2.0 / (b ** 3 * V * dt2)], 1)], 1)     # d/db
         dCdu = np.stack([np.stack([z, -2.0 * a / b ** 2], 1),                  # d(-gamma)/da
                          np.stack([z, 2.0 * a ** 2 / b ** 3], 1)], 1)          # d(-gamma)/db
-        return dict(C=np.stack([CD, CH], 1), g=np.stack([gD, gH], 1), H=np.stack([HD, HH], 1),
+        return dict(C=np.stack([CD, CH], 1), g=np.stack([gD, gH], 1),
+                    H=np.stack([HD, HH], 1) if need_H else None,
                     len=np.ones(n), dCdu=dCdu, dgdu=np.zeros((n, 2, 2, 12)), datdu=datdu)
 
     def ev_sphere(self, x, ci, verts):
@@ -272,7 +273,8 @@ class OracleModel:
             # 2) tetrahedra, color by color; (C_D, C_H) as one 2-row block per tet (R6)
             for grp in self.tet_groups:
                 at = np.stack([self.at_D[grp], self.at_H[grp]], 1)
-                self._project(x, self.tet_idx[grp], self.ev_tet(x, grp), at, lam_t, rec, "tet", grp)
+                self._project(x, self.tet_idx[grp], self.ev_tet(x, grp, need_H=rec is not None), at, lam_t, rec,
+                              "tet", grp)
             # 3) collisions: per free vertex, colliders in order (spheres, capsules), C<0 only (R7)
             for ci in range(nsph):
                 ev = self.ev_sphere(x, ci, freev)

@@ -15,9 +15,6 @@
 #include "../../include/dxpbd.h"
 #include "kernels.cuh"
 #include "tet_kernels.cuh"
-#ifndef DX_HAVE_TETS
-#define DX_HAVE_TETS 0
-#endif
 
 using namespace dx;
 
@@ -184,6 +181,20 @@ __global__ void k_scatter_f(int n, const float *__restrict__ src, const int32_t 
     if (j >= n) return;
     dst[perm[j]] = src[j];
 }
+// [T][2] sorted -> user order / user (a, b) pairs -> sorted split arrays
+__global__ void k_scatter_pair(int n, const float *__restrict__ src, const int32_t *__restrict__ perm, float *__restrict__ dst) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    dst[2 * perm[j]] = src[2 * j];
+    dst[2 * perm[j] + 1] = src[2 * j + 1];
+}
+__global__ void k_gather_pair_split(int n, const float *__restrict__ src, const int32_t *__restrict__ perm,
+                                    float *__restrict__ a, float *__restrict__ b) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    a[j] = src[2 * perm[j]];
+    b[j] = src[2 * perm[j] + 1];
+}
 // rest length L_j = |x_rest[a] - x_rest[b]|
 __global__ void k_rest_len(int n, const int2 *__restrict__ idx, const float *__restrict__ xr, float *__restrict__ rest) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -243,6 +254,7 @@ struct dxpbd_scene {
     int device = 0;
     int V = 0, E = 0, T = 0, NS = 0, NCAP = 0, NSH = 0, NC = 0;
     float dt = 0, inv_dt = 0, frame_dt = 0;
+    double dtd = 0, inv_dt2d = 0;   // fp64 time step for the position-state arithmetic
     int substeps = 1, iterations = 1, max_frames = 0;
     float3 gravity{0, 0, 0};
     float h = 0, coll_alpha = 0;
@@ -269,12 +281,17 @@ struct dxpbd_scene {
     // CG-local tile structure (TMA-staged matvec, QF = 1)
     bool use_tma = false;
     int hcap = 0;
-    size_t tma_smem = 0;
+    size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hoff, d_hlist, d_fpos;
     DBuf<uint32_t> d_cpair, d_fpair;
     DBuf<float4> d_fQ;
-    // tets
-    TetData tets;
+    // tets (color-sorted, internal vertex ids)
+    DBuf<int4> t_idx;
+    DBuf<double> t_Dm, t_vol;
+    DBuf<float> t_a, t_b, t_Q, t_e, t_g, lam_t;
+    DBuf<int32_t> t_perm;
+    DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
+    TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
     // colliders
     DBuf<float> sph, cap_c, cap_a, cap_r0, cap_L0, cap_Rb, cap_Lb, beta;
     DBuf<Collider> cols;
@@ -366,7 +383,7 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     double4 *xo = state(s, n + 1);
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
     LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
-                                                                   (double)s->dt, 1.0 / (double)s->dt, s->gravity, xo));
+                                                                   s->dtd, 1.0 / s->dtd, s->gravity, xo));
     int launches = 1;
     const float inv_dt2 = s->inv_dt * s->inv_dt;
     const int K = s->iterations;
@@ -385,7 +402,16 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
                 LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo));
             ++launches;
         }
-        launches += tet_forward_sweep(s->tets, k, K, inv_dt2, s->dt, xo, st);
+        for (int c = 0; c < s->n_tet_colors; ++c) {
+            int b = s->tet_off[c], cnt = s->tet_off[c + 1] - b;
+            if (!cnt) continue;
+            const int tb = (cnt + 127) / 128;
+            if (!rd && !wr) LAUNCH(DXPBD_K_TET_PROJECT, k_tet_project<false, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, s->lam_t.p, xo));
+            else if (!rd && wr) LAUNCH(DXPBD_K_TET_PROJECT, k_tet_project<false, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, s->lam_t.p, xo));
+            else if (rd && wr) LAUNCH(DXPBD_K_TET_PROJECT, k_tet_project<true, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, s->lam_t.p, xo));
+            else LAUNCH(DXPBD_K_TET_PROJECT, k_tet_project<true, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, s->lam_t.p, xo));
+            ++launches;
+        }
         if (s->NC) {
             float at = s->coll_alpha * inv_dt2;
             if (!rd && !wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
@@ -406,7 +432,7 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
     double4 *x = s->xr.p;
     LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
-                                                                   (double)s->dt, 1.0 / (double)s->dt, s->gravity, x));
+                                                                   s->dtd, 1.0 / s->dtd, s->gravity, x));
     int launches = 1;
     const float inv_dt2 = s->inv_dt * s->inv_dt;
     const int K = s->iterations;
@@ -433,7 +459,20 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             ++launches;
         }
-        launches += tet_replay_sweep(s->tets, k, K, inv_dt2, s->dt, s->pd, x, st);
+        if (s->T) {
+            TetScratch tsc{s->ts_lam.p, s->ts_S.p, s->ts_Dt.p, s->ts_Tu.p, s->ts_e.p};
+            float *teo = ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) ? s->t_e.p : nullptr;
+            for (int c = 0; c < s->n_tet_colors; ++c) {
+                int b = s->tet_off[c], cnt = s->tet_off[c + 1] - b;
+                if (!cnt) continue;
+                const int tb = (cnt + 127) / 128;
+                if (first && last) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<true, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
+                else if (first) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<true, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
+                else if (last) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
+                else LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
+                ++launches;
+            }
+        }
         if (s->NC) {
             float at = s->coll_alpha * inv_dt2;
             float *eo = want_ce ? s->ec.p : nullptr;
@@ -450,12 +489,13 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
 
 // ------------------------------------------------------------------ filtered PCG
 int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_out) {
+    // warm-started PCG: s->ax holds u_{n+1} (initial guess), s->r the residual r0 and s->rhs the
+    // system right-hand side b (both from the rhs kernel); cg_sc was zeroed before the rhs kernel.
     const int V = s->V, E = s->E;
     const int maxit = s->cg_max_iter;
-    DX_CHECK_CUDA(cudaMemsetAsync(s->cg_sc.p, 0, sizeof(double) * (size_t)(maxit + 2) * 4, st));
-    CGState cs{s->cg_sc.p, s->cg_sc.p + 2, s->cg_tol * s->cg_tol};
+    CGState cs{s->cg_sc.p, s->cg_sc.p + (size_t)(maxit + 1) * 4, s->cg_tol * s->cg_tol};
     const float *xw = s->inv_mass.p;
-    LAUNCH(DXPBD_K_CG_INIT, k_cg_init<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->ax.p, s->r.p, s->p.p, xw, cs));
+    LAUNCH(DXPBD_K_CG_INIT, k_cg_start<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->r.p, s->p.p, xw, cs));
     int launches = 1;
     const float *Qc = s->NC ? s->Qc.p : nullptr;
     CGBufs bufs{s->ax.p, s->r.p, s->p.p, s->p1.p, s->q.p, nullptr};
@@ -476,14 +516,17 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             else
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<0><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             ++launches;
-            launches += tet_cg_matvec(s->tets, it, s->p.p, s->q.p, xw, cs, st);
+            if (s->T) {
+                LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), s->t_Q.p, bufs, xw, cs));
+                ++launches;
+            }
             LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update2<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, cs));
             ++launches;
         }
-        // convergence check: rr of the last completed iteration
-        DX_CHECK_CUDA(cudaMemcpyAsync(s->h_scal, s->cg_sc.p, sizeof(double) * (size_t)(it + 1) * 4, cudaMemcpyDeviceToHost, st));
+        // convergence check: rr of the last completed iteration against |b|^2
+        DX_CHECK_CUDA(cudaMemcpyAsync(s->h_scal, s->cg_sc.p, sizeof(double) * (size_t)(maxit + 2) * 4, cudaMemcpyDeviceToHost, st));
         DX_CHECK_CUDA(cudaStreamSynchronize(st));
-        double bb = s->h_scal[2];
+        double bb = s->h_scal[(size_t)(maxit + 1) * 4];
         double tol2 = (double)s->cg_tol * s->cg_tol;
         if (bb == 0.0) { iters_out = 0; relres_out = 0.0; break; }
         for (int k = 0; k <= it; ++k) {
@@ -549,7 +592,6 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         DX_REQUIRE(d->dist_idx[2 * j] != d->dist_idx[2 * j + 1], DXPBD_ERR_ARG, "degenerate distance constraint");
     for (int j = 0; j < 4 * d->num_tets; ++j)
         DX_REQUIRE(d->tet_idx[j] >= 0 && d->tet_idx[j] < V, DXPBD_ERR_ARG, "tet_idx out of range");
-    DX_REQUIRE(d->num_tets == 0 || DX_HAVE_TETS, DXPBD_ERR_ARG, "tet constraints not built into this library");
     DX_CHECK_CUDA(cudaSetDevice(d->device));
     s = new dxpbd_scene();
     s->device = d->device;
@@ -565,6 +607,8 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     s->iterations = d->iterations;
     s->dt = d->frame_dt / d->substeps;
     s->inv_dt = 1.0f / s->dt;
+    s->dtd = (double)d->frame_dt / (double)d->substeps;
+    s->inv_dt2d = 1.0 / (s->dtd * s->dtd);
     s->gravity = make_float3(d->gravity[0], d->gravity[1], d->gravity[2]);
     s->h = d->thickness;
     s->coll_alpha = d->collision_compliance;
@@ -716,8 +760,9 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 upload(s->d_fpos.p, fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
                 s->d_fQ.alloc((size_t)std::max<int64_t>(fc[nkeys], 1));
                 s->tma_smem = tma_smem_bytes(s->hcap);
+                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
                 DX_CHECK_CUDA(cudaStreamSynchronize(st));
             }
         }
@@ -738,12 +783,41 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     }
     // tets
     if (s->T) {
-        int nc = greedy_colors(s->T, 4, d->tet_idx, V, s->tet_color_h);
+        const int T = s->T;
+        int nc = greedy_colors(T, 4, d->tet_idx, V, s->tet_color_h);
         if (nc < 0) throw Err{DXPBD_ERR_LIMIT, "tet coloring needs more than 256 colors"};
         s->n_tet_colors = nc;
         color_sort(s->tet_color_h, nc, s->tet_perm_h, s->tet_off);
-        tet_create(s->tets, s->T, d->tet_idx, d->tet_a, d->tet_b, xr3.p, s->tet_perm_h, s->tet_off,
-                   s->iterations, s->dt, (s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1, st);
+        // within a color, order by the smallest internal vertex id (locality of the gathers)
+        std::vector<int4> ti(T);
+        for (int j = 0; j < T; ++j)
+            ti[j] = make_int4(vinv[d->tet_idx[4 * j]], vinv[d->tet_idx[4 * j + 1]], vinv[d->tet_idx[4 * j + 2]],
+                              vinv[d->tet_idx[4 * j + 3]]);
+        auto mn = [&](int j) { return std::min(std::min(ti[j].x, ti[j].y), std::min(ti[j].z, ti[j].w)); };
+        for (int c = 0; c < nc; ++c)
+            std::sort(s->tet_perm_h.begin() + s->tet_off[c], s->tet_perm_h.begin() + s->tet_off[c + 1],
+                      [&](int32_t x, int32_t y) { return mn(x) < mn(y); });
+        std::vector<int4> ts(T);
+        for (int q = 0; q < T; ++q) ts[q] = ti[s->tet_perm_h[q]];
+        s->t_idx.alloc(T);
+        upload(s->t_idx.p, ts.data(), sizeof(int4) * T, DXPBD_MEM_HOST, st);
+        s->t_perm.alloc(T);
+        upload(s->t_perm.p, s->tet_perm_h.data(), sizeof(int32_t) * T, DXPBD_MEM_HOST, st);
+        DBuf<float> tmpab;
+        tmpab.alloc(T);
+        s->t_a.alloc(T);
+        s->t_b.alloc(T);
+        upload(tmpab.p, d->tet_a, sizeof(float) * T, DXPBD_MEM_HOST, st);
+        k_gather_f<<<nblk(T), kBlock, 0, st>>>(T, tmpab.p, s->t_perm.p, s->t_a.p);
+        DX_CHECK_CUDA(cudaStreamSynchronize(st));
+        upload(tmpab.p, d->tet_b, sizeof(float) * T, DXPBD_MEM_HOST, st);
+        k_gather_f<<<nblk(T), kBlock, 0, st>>>(T, tmpab.p, s->t_perm.p, s->t_b.p);
+        s->t_Dm.alloc((size_t)9 * T);
+        s->t_vol.alloc(T);
+        k_tet_rest<<<nblk(T), kBlock, 0, st>>>(T, s->t_idx.p, xr3.p, s->t_Dm.p, s->t_vol.p);
+        if (s->iterations > 1) s->lam_t.alloc((size_t)2 * T);
+        DX_CHECK_CUDA(cudaGetLastError());
+        DX_CHECK_CUDA(cudaStreamSynchronize(st));
     }
     // colliders
     if (s->NC) {
@@ -875,7 +949,15 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     if (s->cg_sc.n < (size_t)(s->cg_max_iter + 2) * 4) s->cg_sc.alloc((size_t)(s->cg_max_iter + 2) * 4);
     const size_t nacc = 1 + 4 * (size_t)std::max(s->NC, 1);
     if (s->acc.n < nacc) s->acc.alloc(nacc);
-    tet_backward_alloc(s->tets, s->iterations, st);
+    if (s->T) {
+        const size_t T = s->T;
+        if (s->t_Q.n < 45 * T) s->t_Q.alloc(45 * T);
+        if (((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) && s->t_e.n < 18 * T) s->t_e.alloc(18 * T);
+        if (s->t_g.n < 2 * T) s->t_g.alloc(2 * T);
+        if (s->iterations > 1 && s->ts_lam.n < 2 * T) {
+            s->ts_lam.alloc(2 * T); s->ts_S.alloc(18 * T); s->ts_Dt.alloc(45 * T); s->ts_Tu.alloc(4 * T); s->ts_e.alloc(18 * T);
+        }
+    }
     // targets
     if (num_keys) {
         if (s->targets.n < (size_t)num_keys * V * 3) s->targets.alloc((size_t)num_keys * V * 3);
@@ -901,7 +983,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         DX_CHECK_CUDA(cudaMemsetAsync(s->g_force.p, 0, sizeof(float) * nf, st));
     }
     DX_CHECK_CUDA(cudaMemsetAsync(s->acc.p, 0, sizeof(double) * nacc, st));
-    tet_grad_reset(s->tets, st);
+    if (s->T) DX_CHECK_CUDA(cudaMemsetAsync(s->t_g.p, 0, sizeof(float) * 2 * s->T, st));
     // state index -> keyframe slot
     std::vector<int> key_of(N + 1, -1);
     for (int k = 0; k < num_keys; ++k) key_of[key_frames[k] * sub] = k;   // duplicates: last wins
@@ -922,23 +1004,31 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         const int frame = n / sub;
         float *gf = g_forces ? s->g_force.p + (size_t)frame * V * 3 : nullptr;
         launches += replay_substep(s, n, st);
-        // b = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1}   (one tiled pass, own vertices stored once)
+        // b = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1} and the warm-start residual r0 = b - A_n u_{n+1}
+        // (one tiled pass, own vertices stored once); the PCG then starts from u_n := u_{n+1}.
+        DX_CHECK_CUDA(cudaMemsetAsync(s->cg_sc.p, 0, sizeof(double) * (size_t)(s->cg_max_iter + 2) * 4, st));
         {
             TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
             TmaTiles tt{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_hoff.p, s->d_cpair.p, s->d_fpair.p,
                         s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p};
             if (s->use_tma)
-                LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(
-                    tt, V, s->hcap, Qc, s->ax.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p));
+                LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_rhs_smem, st>>>(
+                    tt, V, s->hcap, Qc, s->ax.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p, s->r.p));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tiled<1><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->y.p,
-                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p));
+                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p,
+                                                                                 s->rhs.p, s->r.p));
             else
                 LAUNCH(DXPBD_K_RHS, k_rhs_tiled<0><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->y.p,
-                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p));
+                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p,
+                                                                                 s->rhs.p, s->r.p));
             ++launches;
         }
-        launches += tet_rhs(s->tets, s->y.p, s->rhs.p, s->inv_mass.p, st);
+        if (s->T) {
+            LAUNCH(DXPBD_K_RHS, k_rhs_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->t_Q.p, s->y.p, s->ax.p, s->rhs.p, s->r.p,
+                                                                        s->inv_mass.p));
+            ++launches;
+        }
         int iters = 0;
         double rel = 0.0;
         launches += pcg_solve(s, st, iters, rel);   // u_n into s->ax
@@ -956,7 +1046,10 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             LAUNCH(DXPBD_K_GRADS, k_grad_colliders<<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->ec.p, s->y.p, s->acc.p + 1));
             ++launches;
         }
-        launches += tet_grads(s->tets, s->y.p, st);
+        if (s->T && ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1)) {
+            LAUNCH(DXPBD_K_GRADS, k_grad_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->t_e.p, s->y.p, s->t_g.p));
+            ++launches;
+        }
     }
     if (s->g_x0.n < (size_t)3 * V) s->g_x0.alloc((size_t)3 * V);
     if (s->g_v0.n < (size_t)3 * V) s->g_v0.alloc((size_t)3 * V);
@@ -1044,7 +1137,11 @@ int dxpbd_grads(dxpbd_scene *s, int32_t kind, float *out, int64_t out_len, int32
         }
         case DXPBD_GRAD_MATERIAL: {
             DX_REQUIRE(out_len == 2 * (int64_t)s->T, DXPBD_ERR_ARG, "out_len must be 2T");
-            tet_grad_out(s->tets, out, mem, st);
+            DBuf<float> tmp;
+            tmp.alloc(2 * (size_t)s->T);
+            k_scatter_pair<<<nblk(s->T), kBlock, 0, st>>>(s->T, s->t_g.p, s->t_perm.p, tmp.p);
+            download(out, tmp.p, sizeof(float) * 2 * s->T, mem, st);
+            DX_CHECK_CUDA(cudaStreamSynchronize(st));
             break;
         }
     }
@@ -1076,10 +1173,15 @@ int dxpbd_set_params(dxpbd_scene *s, int32_t kind, const float *data, int64_t le
             upload(s->sph.p, data, sizeof(float) * 4 * s->NSH, mem, st);
             apply_shape(s, st);
             break;
-        case DXPBD_PARAM_MATERIAL:
+        case DXPBD_PARAM_MATERIAL: {
             DX_REQUIRE(len == 2 * (int64_t)s->T, DXPBD_ERR_ARG, "len must be 2T");
-            tet_set_material(s->tets, data, mem, st);
+            DBuf<float> tmp;
+            tmp.alloc(2 * (size_t)s->T);
+            upload(tmp.p, data, sizeof(float) * 2 * s->T, mem, st);
+            k_gather_pair_split<<<nblk(s->T), kBlock, 0, st>>>(s->T, tmp.p, s->t_perm.p, s->t_a.p, s->t_b.p);
+            DX_CHECK_CUDA(cudaStreamSynchronize(st));
             break;
+        }
         default:
             throw Err{DXPBD_ERR_ARG, "bad parameter kind"};
     }

@@ -809,22 +809,27 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cg_matvec_tma(int it, TmaTil
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// Increment-system right-hand side: b = M u + dphi - Qc y - A_dist y (own vertices).
-__global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
+// Increment-system right-hand side with warm start (kernels "adjoint"): for own vertices
+//   b  = M u + dphi - (Qc + A) y              (the system right-hand side, for its norm)
+//   r0 = b - (M + Qc + A) u = dphi - (Qc + A)(y + u)   (residual at the warm start u_n := u_{n+1})
+// A_dist is applied to y and to z = y + u in the same pass (Q read once).  Writes b, r0.
+__global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
                                                             const float4 *__restrict__ u, const float4 *__restrict__ y,
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                             const float *__restrict__ weights, const float *__restrict__ wv,
-                                                            float4 *__restrict__ bout) {
+                                                            float4 *__restrict__ bout, float4 *__restrict__ r0out) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 64);
-    float *sq = reinterpret_cast<float *>(smem_raw + 64 + sizeof(TmaStage) * kTmaStages);
-    float *sp = sq + 3 * kTileV;
+    float *sqb = reinterpret_cast<float *>(smem_raw + 64 + sizeof(TmaStage) * kTmaStages);
+    float *sqr = sqb + 3 * kTileV;
     const int spn = kTileV + hcap;
+    float *sy = sqr + 3 * kTileV;
+    float *sz = sy + 3 * spn;
     const int t = blockIdx.x;
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
-    __shared__ int sb[4 * kMaxColors];   // per-color (b, e, fb, fe) of this tile
+    __shared__ int sb[4 * kMaxColors];
     {
         const int stride = T.ntiles + 1;
         for (int c = threadIdx.x; c < T.ncol; c += blockDim.x) {
@@ -841,128 +846,204 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages[c], c, sb, T);
     }
     for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
-        float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
-        float3 rr = make_float3(0.f, 0.f, 0.f);
+        float3 yv = make_float3(0.f, 0.f, 0.f), zv = yv, bb = yv, rr = yv;
         if (i < nv) {
             const int v = v0 + i;
             const float w = wv[v];
-            yv = y[v];
+            yv = f3(y[v]);
+            const float3 uv = f3(u[v]);
+            zv = yv + uv;
             if (w > 0.f) {
-                rr = (1.f / w) * f3(u[v]);
+                bb = (1.f / w) * uv;
                 if (Qc) {
                     Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
                                   Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
-                    rr = rr - sym3_mul(A, f3(yv));
+                    bb = bb - sym3_mul(A, yv);
+                    rr = rr - sym3_mul(A, zv);
                 }
                 if (target) {
                     double4 x = xkey[v];
                     float W = weights ? weights[v] : 1.f;
-                    rr = rr + W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
-                                              (float)(x.z - target[3 * v + 2]));
+                    float3 g = W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
+                                               (float)(x.z - target[3 * v + 2]));
+                    bb = bb + g;
+                    rr = rr + g;
                 }
             }
         }
-        sp[i] = yv.x;
-        sp[spn + i] = yv.y;
-        sp[2 * spn + i] = yv.z;
-        sq[i] = rr.x;
-        sq[kTileV + i] = rr.y;
-        sq[2 * kTileV + i] = rr.z;
+        sy[i] = yv.x; sy[spn + i] = yv.y; sy[2 * spn + i] = yv.z;
+        sz[i] = zv.x; sz[spn + i] = zv.y; sz[2 * spn + i] = zv.z;
+        sqb[i] = bb.x; sqb[kTileV + i] = bb.y; sqb[2 * kTileV + i] = bb.z;
+        sqr[i] = rr.x; sqr[kTileV + i] = rr.y; sqr[2 * kTileV + i] = rr.z;
     }
     const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
     for (int h = threadIdx.x; h < nh; h += blockDim.x) {
-        const float4 yv = y[T.hlist[h0 + h]];
-        sp[kTileV + h] = yv.x;
-        sp[spn + kTileV + h] = yv.y;
-        sp[2 * spn + kTileV + h] = yv.z;
+        const int v = T.hlist[h0 + h];
+        const float3 yv = f3(y[v]), zv = yv + f3(u[v]);
+        sy[kTileV + h] = yv.x; sy[spn + kTileV + h] = yv.y; sy[2 * spn + kTileV + h] = yv.z;
+        sz[kTileV + h] = zv.x; sz[spn + kTileV + h] = zv.y; sz[2 * spn + kTileV + h] = zv.z;
     }
     __syncthreads();
-    tma_tile_colors<-1>(bars, stages, reinterpret_cast<float (*)[1]>(sp), spn, sq, sb, T);
+    for (int c = 0; c < T.ncol; ++c) {
+        const int st = c % kTmaStages;
+        TmaStage &S = stages[st];
+        mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
+        const int b = sb[4 * c], e = sb[4 * c + 1];
+        const int off = (int)((((size_t)b * 4) & 15) >> 2);
+        for (int i = threadIdx.x; i < e - b; i += blockDim.x) {
+            const uint32_t pr = S.cp[off + i];
+            const float4 q4 = S.q[i];
+            const int la = pr & 0xffff, lb = pr >> 16;
+            const float3 qy = qmul_iso_rank1(q4, make_float3(sy[la] - sy[lb], sy[spn + la] - sy[spn + lb],
+                                                             sy[2 * spn + la] - sy[2 * spn + lb]));
+            const float3 qz = qmul_iso_rank1(q4, make_float3(sz[la] - sz[lb], sz[spn + la] - sz[spn + lb],
+                                                             sz[2 * spn + la] - sz[2 * spn + lb]));
+            sqb[la] -= qy.x; sqb[kTileV + la] -= qy.y; sqb[2 * kTileV + la] -= qy.z;
+            sqr[la] -= qz.x; sqr[kTileV + la] -= qz.y; sqr[2 * kTileV + la] -= qz.z;
+            if (lb < kTileV) {
+                sqb[lb] += qy.x; sqb[kTileV + lb] += qy.y; sqb[2 * kTileV + lb] += qy.z;
+                sqr[lb] += qz.x; sqr[kTileV + lb] += qz.y; sqr[2 * kTileV + lb] += qz.z;
+            }
+        }
+        const int fb = sb[4 * c + 2], fe = sb[4 * c + 3];
+        const int foff = (int)((((size_t)fb * 4) & 15) >> 2);
+        for (int i = threadIdx.x; i < fe - fb; i += blockDim.x) {
+            const uint32_t pr = i < kFCap ? S.fp[foff + i] : T.fpair[fb + i];
+            const float4 q4 = i < kFCap ? S.fq[i] : T.fQ[fb + i];
+            const int la = pr & 0xffff, lb = pr >> 16;   // la: halo slot of a, lb: own b
+            const float3 qy = qmul_iso_rank1(q4, make_float3(sy[la] - sy[lb], sy[spn + la] - sy[spn + lb],
+                                                             sy[2 * spn + la] - sy[2 * spn + lb]));
+            const float3 qz = qmul_iso_rank1(q4, make_float3(sz[la] - sz[lb], sz[spn + la] - sz[spn + lb],
+                                                             sz[2 * spn + la] - sz[2 * spn + lb]));
+            sqb[lb] += qy.x; sqb[kTileV + lb] += qy.y; sqb[2 * kTileV + lb] += qy.z;
+            sqr[lb] += qz.x; sqr[kTileV + lb] += qz.y; sqr[2 * kTileV + lb] += qz.z;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && c + kTmaStages < T.ncol) {
+            fence_proxy_async();
+            tma_issue(&bars[st], S, c + kTmaStages, sb, T);
+        }
+    }
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i;
-        bout[v] = wv[v] > 0.f ? make_float4(sq[i], sq[kTileV + i], sq[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool fr = wv[v] > 0.f;
+        bout[v] = fr ? make_float4(sqb[i], sqb[kTileV + i], sqb[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        r0out[v] = fr ? make_float4(sqr[i], sqr[kTileV + i], sqr[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
-// right-hand side of the increment system (kernels "adjoint"):
-//   b = M u_next + dphi/dx_{n+1} - Qc y_next - Sum_j P_j^T Q_j P_j y_next   (own vertices, one store)
+__host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap) {
+    return 64 + sizeof(TmaStage) * kTmaStages + sizeof(float) * 6 * kTileV + sizeof(float) * 6 * (kTileV + hcap);
+}
+
+// PCG start from the warm start: r = r0 (filtered), p_0 = M^-1 r; slot 0 gets r.z and r.r;
+// the reference norm |b|^2 goes to s.bnorm2.
+__global__ void k_cg_start(int V, const float4 *__restrict__ b, float4 *__restrict__ r, float4 *__restrict__ p,
+                           const float *__restrict__ wv, CGState s) {
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc[3] = {0.f, 0.f, 0.f};
+    if (v < V) {
+        const float w = wv[v];
+        float4 rv = r[v], bv = b[v];
+        if (!(w > 0.f)) rv = bv = make_float4(0.f, 0.f, 0.f, 0.f);
+        r[v] = rv;
+        p[v] = make_float4(w * rv.x, w * rv.y, w * rv.z, 0.f);
+        const float r2 = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
+        acc[0] = w * r2;
+        acc[1] = r2;
+        acc[2] = bv.x * bv.x + bv.y * bv.y + bv.z * bv.z;
+    }
+    float a2[2] = {acc[0], acc[1]};
+    block_reduce_add<2>(a2, s.sc + 1);
+    float bb[1] = {acc[2]};
+    block_reduce_add<1>(bb, s.bnorm2);
+}
+
+// Generic (non-TMA) version of k_rhs_tma: writes b and the warm-start residual r0.
 template <int QF>
 __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const int2 *__restrict__ idx,
                                                       const float *__restrict__ Q, int E, const float *__restrict__ Qc,
                                                       const float4 *__restrict__ u, const float4 *__restrict__ y,
                                                       const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                       const float *__restrict__ weights, const float *__restrict__ wv,
-                                                      float4 *__restrict__ b) {
-    __shared__ float sy[3][kTileV];
-    __shared__ float sq[3][kTileV];
+                                                      float4 *__restrict__ bout, float4 *__restrict__ r0out) {
+    __shared__ float sy[3][kTileV], sz[3][kTileV], sqb[3][kTileV], sqr[3][kTileV];
     const int t = blockIdx.x;
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
     for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
-        float4 yv = make_float4(0.f, 0.f, 0.f, 0.f);
-        float3 r = make_float3(0.f, 0.f, 0.f);
+        float3 yv = make_float3(0.f, 0.f, 0.f), zv = yv, bb = yv, rr = yv;
         if (i < nv) {
             const int v = v0 + i;
             const float w = wv[v];
-            yv = y[v];
+            yv = f3(y[v]);
+            const float3 uv = f3(u[v]);
+            zv = yv + uv;
             if (w > 0.f) {
-                r = (1.f / w) * f3(u[v]);
+                bb = (1.f / w) * uv;
                 if (Qc) {
                     Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
                                   Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
-                    r = r - sym3_mul(A, f3(yv));
+                    bb = bb - sym3_mul(A, yv);
+                    rr = rr - sym3_mul(A, zv);
                 }
                 if (target) {
                     double4 x = xkey[v];
                     float W = weights ? weights[v] : 1.f;
-                    r = r + W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
-                                            (float)(x.z - target[3 * v + 2]));
+                    float3 g = W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
+                                               (float)(x.z - target[3 * v + 2]));
+                    bb = bb + g;
+                    rr = rr + g;
                 }
             }
         }
-        sy[0][i] = yv.x;
-        sy[1][i] = yv.y;
-        sy[2][i] = yv.z;
-        sq[0][i] = r.x;
-        sq[1][i] = r.y;
-        sq[2][i] = r.z;
+        sy[0][i] = yv.x; sy[1][i] = yv.y; sy[2][i] = yv.z;
+        sz[0][i] = zv.x; sz[1][i] = zv.y; sz[2][i] = zv.z;
+        sqb[0][i] = bb.x; sqb[1][i] = bb.y; sqb[2][i] = bb.z;
+        sqr[0][i] = rr.x; sqr[1][i] = rr.y; sqr[2][i] = rr.z;
     }
     __syncthreads();
     const int stride = L.ntiles + 1;
     for (int c = 0; c < L.ncol; ++c) {
-        const int bb = L.seg[c * stride + t], e = L.seg[c * stride + t + 1];
-        for (int j = bb + threadIdx.x; j < e; j += blockDim.x) {
+        const int bb0 = L.seg[c * stride + t], e = L.seg[c * stride + t + 1];
+        for (int j = bb0 + threadIdx.x; j < e; j += blockDim.x) {
             const int2 ab = idx[j];
             const int la = ab.x - v0, lb = ab.y - v0;
             const bool bl = lb < nv;
-            const float3 d = make_float3(sy[0][la], sy[1][la], sy[2][la]) -
-                             (bl ? make_float3(sy[0][lb], sy[1][lb], sy[2][lb]) : f3(y[ab.y]));
-            const float3 q = qmul<QF>(Q, j, E, d);
-            sq[0][la] -= q.x;
-            sq[1][la] -= q.y;
-            sq[2][la] -= q.z;
+            float3 yb, zb;
             if (bl) {
-                sq[0][lb] += q.x;
-                sq[1][lb] += q.y;
-                sq[2][lb] += q.z;
+                yb = make_float3(sy[0][lb], sy[1][lb], sy[2][lb]);
+                zb = make_float3(sz[0][lb], sz[1][lb], sz[2][lb]);
+            } else {
+                yb = f3(y[ab.y]);
+                zb = yb + f3(u[ab.y]);
+            }
+            const float3 qy = qmul<QF>(Q, j, E, make_float3(sy[0][la], sy[1][la], sy[2][la]) - yb);
+            const float3 qz = qmul<QF>(Q, j, E, make_float3(sz[0][la], sz[1][la], sz[2][la]) - zb);
+            sqb[0][la] -= qy.x; sqb[1][la] -= qy.y; sqb[2][la] -= qy.z;
+            sqr[0][la] -= qz.x; sqr[1][la] -= qz.y; sqr[2][la] -= qz.z;
+            if (bl) {
+                sqb[0][lb] += qy.x; sqb[1][lb] += qy.y; sqb[2][lb] += qy.z;
+                sqr[0][lb] += qz.x; sqr[1][lb] += qz.y; sqr[2][lb] += qz.z;
             }
         }
         const int fb = L.fseg[c * stride + t], fe = L.fseg[c * stride + t + 1];
-        for (int k = fb + threadIdx.x; k < fe; k += blockDim.x) {
-            const int j = L.fidx[k];
-            const int2 ab = idx[j];
-            const int lb = ab.y - v0;
-            const float3 d = f3(y[ab.x]) - make_float3(sy[0][lb], sy[1][lb], sy[2][lb]);
-            const float3 q = qmul<QF>(Q, j, E, d);
-            sq[0][lb] += q.x;
-            sq[1][lb] += q.y;
-            sq[2][lb] += q.z;
+        for (int k2 = fb + threadIdx.x; k2 < fe; k2 += blockDim.x) {
+            const int4 f4 = L.fent[k2];   // {j, a, b}: b in tile
+            const int lb = f4.z - v0;
+            const float3 ya = f3(y[f4.y]), za = ya + f3(u[f4.y]);
+            const float3 qy = qmul<QF>(Q, f4.x, E, ya - make_float3(sy[0][lb], sy[1][lb], sy[2][lb]));
+            const float3 qz = qmul<QF>(Q, f4.x, E, za - make_float3(sz[0][lb], sz[1][lb], sz[2][lb]));
+            sqb[0][lb] += qy.x; sqb[1][lb] += qy.y; sqb[2][lb] += qy.z;
+            sqr[0][lb] += qz.x; sqr[1][lb] += qz.y; sqr[2][lb] += qz.z;
         }
         __syncthreads();
     }
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i;
-        b[v] = wv[v] > 0.f ? make_float4(sq[0][i], sq[1][i], sq[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool fr = wv[v] > 0.f;
+        bout[v] = fr ? make_float4(sqb[0][i], sqb[1][i], sqb[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        r0out[v] = fr ? make_float4(sqr[0][i], sqr[1][i], sqr[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -989,14 +1070,6 @@ __global__ void k_cg_update2(int V, int it, CGBufs B, const float *__restrict__ 
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
 }
 
-// ============================================================================ adjoint
-// Increment form of Eq. adjointXPBD (R3/R4): with A_n = M + Sum_j Q_j(n),
-// y_n = M^-1 xhat_n and the paper's right-hand side 2 xhat_{n+1} - vhat_{n+1}/dt + dphi/dx (l.155)
-//   A_n y_n = M (2 y_{n+1} - y_{n+2}) + dphi/dx_{n+1}
-// is solved for u_n = y_n - y_{n+1}:
-//   A_n u_n = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1},   y_n = y_{n+1} + u_n,
-// algebraically identical, but the PCG tolerance is relative to the (small) increment instead of
-// being integrated twice by the second difference.  Pinned rows are filtered (R11).
 // after the solve: y_n = y_{n+1} + u_n ; dphi/df_frame += dt^2 y_n (R8)
 __global__ void k_adjoint_accum(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
                                 float4 *__restrict__ y, float *__restrict__ gforce, float dt) {

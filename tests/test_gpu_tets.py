@@ -1,0 +1,75 @@
+"""GPU parity for the tetrahedral stable Neo-Hookean blocks (configs[2] regime: 1.03 cm spacing,
+dt = 1/1200 s, E ~ U(1e4, 1e6) Pa, nu ~ U(0.3, 0.45)): positions within 1e-4 and material /
+initial-state gradients within 1e-3 relative L2 vs the fp64 oracle.
+
+Horizons: with one Gauss-Seidel iteration per substep the stiff block is chaotic in the fp64
+oracle itself (a 1e-9 m perturbation of x0 grows to ~1e-1 relative within 40 substeps;
+DESIGN.md "Conditioning"), so parity at the config's stiffness is asserted over 2-3 substeps, and
+over a full 20-substep frame for E <= 1e5 Pa where the oracle's own sensitivity stays ~1e-6."""
+import numpy as np
+import pytest
+
+from synth import volumetric_block
+from tests.gpu_helpers import f32, gpu_run, oracle_run, rel_l2
+from tests.test_gpu_cloth import _compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _block(n, substeps, iterations=1, soft=False, frames=1):
+    """configs[2] regime at reduced vertex count; `substeps` substeps of dt = 1/1200 s per frame."""
+    s = volumetric_block(n=n, frames=frames, substeps=substeps, iterations=iterations, side=0.4 * (n - 1) / 39)
+    s = s.replace(frame_dt=substeps / 1200.0)
+    if soft:
+        rng = np.random.default_rng(7)
+        E = rng.uniform(1e4, 1e5, size=len(s.tet_a))
+        nu = rng.uniform(0.3, 0.45, size=len(s.tet_a))
+        s = s.replace(tet_a=np.sqrt(E / (2 * (1 + nu))), tet_b=np.sqrt(E * nu / ((1 + nu) * (1 - 2 * nu))))
+    return f32(s)
+
+
+@pytest.mark.parametrize("iters", [1, 2])
+def test_volumetric_stiff_short(iters):
+    s = _block(6, 3, iters)
+    g = gpu_run(s, ("material",))
+    o = oracle_run(s)
+    _compare(g, o, ("material", "v0", "x0"))
+
+
+def test_volumetric_soft_frame():
+    s = _block(6, 20, soft=True)
+    g = gpu_run(s, ("material",))
+    o = oracle_run(s)
+    assert np.abs(o["x"][-1] - o["x"][0]).max() > 1e-4   # the block actually deforms
+    _compare(g, o, ("material", "v0", "x0"))
+
+
+def test_volumetric_no_pd():
+    s = _block(5, 2)
+    g = gpu_run(s, ("material",), pd=0)
+    o = oracle_run(s, pd=False)
+    _compare(g, o, ("material", "v0", "x0"))
+
+
+def test_tet_coloring_bit_exact():
+    from oracle import greedy_color
+    from paper_2301_01396_b200 import api
+    s = f32(volumetric_block(n=9, frames=1))
+    g = gpu_run(s, frames=1, backward=False)
+    np.testing.assert_array_equal(api.dxpbd_coloring(g["scene"], 1), greedy_color(s.tet_idx, s.num_vertices))
+
+
+def test_volumetric_mid_size_soft_forward():
+    """16^3 vertices (16875 tets), softer material, 1 frame x 20 substeps."""
+    s = _block(16, 20, soft=True)
+    g = gpu_run(s, backward=False)
+    o = oracle_run(s, backward=False)
+    assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
+
+
+def test_volumetric_full_size_forward_substeps():
+    """configs[2] at full size (40^3 vertices, ~300k tets), 2 substeps at its dt."""
+    s = _block(40, 2)
+    g = gpu_run(s, backward=False)
+    o = oracle_run(s, backward=False)
+    assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
