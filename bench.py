@@ -27,6 +27,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "constraint solves/s & ms/step fwd+adjoint at ~26M DoF cloth; HBM GB/s vs peak"
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed `ncu --set full`
+# capture of the dominant kernel at configs[4] size (profiles/ncu/)
+TRAFFIC = {"cg_dist": 1.479445e9 + 0.266695e9}
 UNIT = "constraint solves/s"
 
 
@@ -153,22 +156,21 @@ def run_reference(a):
 
 
 # ----------------------------------------------------------------------------- our arm
-# algorithmic (compulsory) HBM bytes per launch of each kernel class
-def algo_bytes(cls, E, V, count, grads_comp=False):
-    if cls == "dist_project":      # per constraint: idx 8 + rest 4 + alpha 4 + 2 x (32 B read + 32 B write)
-        return 144.0 * E / count
-    if cls == "dist_replay":       # + Q 24 (+ e 12)
-        return (168.0 + (12.0 if grads_comp else 0.0)) * E / count
-    if cls == "cg_dist":           # per constraint idx 8 + Q 24; per vertex p 16 + q r/w 32 + w 4
-        return 32.0 * E + 52.0 * V
-    if cls == "cg_vertex":         # p r/w 32, r 16, q w 16, w 4
-        return 68.0 * V
-    if cls == "cg_update":         # y r/w 32, r r/w 32, p 16, q 16, w 4
+# Algorithmic (compulsory) HBM bytes per launch of the kernel classes:
+# every array element the launch must read or write, counted once.
+def algo_bytes(cls, st, units_per_launch=None):
+    E, V, NF, H = st["E"], st["V"], st["n_foreign"], st["halo_total"]
+    if cls == "dist_project":   # per constraint: idx 8 + rest 4 + alpha 4 + 2 x (32 B read + 32 B write) fp64 state
+        return 144.0 * units_per_launch
+    if cls == "dist_replay":    # + Q 16 + foreign slot 4 (+ its fQ copy for foreign constraints)
+        return (164.0 + 16.0 * NF / max(E, 1)) * units_per_launch
+    if cls == "cg_dist":        # TMA matvec: cpair 4 + Q 16 per constraint, fpair 4 + fQ 16 per foreign entry,
+        # hlist 4 + (r, p_old 32 + w 4) per halo slot, own r 16 + p_old 16 + w 4 + p_new 16 + q 16
+        return 20.0 * E + 20.0 * NF + 40.0 * H + 68.0 * V
+    if cls == "cg_update":      # u r/w 32, r r/w 32, p 16, q 16, w 4
         return 100.0 * V
-    if cls == "predict":           # x_n 32, x_{n-1} 32, f 12, out 32
+    if cls == "predict":        # x_n 32, x_{n-1} 32, f 12, out 32
         return 108.0 * V
-    if cls == "rhs":
-        return (32.0 * E + 52.0 * V) / 2
     return None
 
 
@@ -292,16 +294,16 @@ def run_ours(a):
     if ktimes:
         dom = max(ktimes, key=lambda k: ktimes[k][0])
         ms, cnt = ktimes[dom]
-        b = algo_bytes(dom, E, V, max(cnt // max(1, a.steps), 1) if dom in ("dist_project", "dist_replay") else cnt)
-        if dom in ("dist_project", "dist_replay"):
-            # bytes per launch = per-constraint bytes x constraints of one color launch (average)
-            per_launch_units = E * a.iterations * substeps_total / max(cnt / a.steps, 1)
-            b = algo_bytes(dom, per_launch_units, V, 1)
+        sst = api.dxpbd_stats(sc)
+        # color launches: constraints of one launch on average
+        per_launch_units = E * a.iterations * substeps_total / max(cnt / a.steps, 1)
+        b = algo_bytes(dom, sst, per_launch_units)
         avg_ms = ms / cnt
         ach = (b / (avg_ms / 1e3)) / 1e9 if b else None
         share = ms / sum(v[0] for v in ktimes.values())
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": None, "kernel": dom,
+                "frac": (ach / peak) if ach else None, "traffic": TRAFFIC.get(dom), "kernel": dom,
+                "algorithmic_bytes_per_launch": b,
                 "avg_launch_ms": avg_ms, "launches": cnt, "share_of_kernel_time": share,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"}
 

@@ -144,10 +144,11 @@ int dxpbd_set_params(dxpbd_scene *scene, int32_t kind, const float *data, int64_
 int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out_len,
                    int32_t *num_colors);
 
-/* Statistics of the last calls: HOST out[0..n): see DXPBD_STAT_* in dxpbd.cu docs
- * (0: total PCG iterations of the last backward, 1: max PCG iterations of one solve,
- *  2: number of kernel launches of the last forward, 3: of the last backward,
- *  4: substeps solved, 5: worst final relative residual). */
+/* Statistics into HOST out[0..n), n <= 16:
+ *  0: total PCG iterations of the last backward, 1: max PCG iterations of one solve,
+ *  2: kernel launches of the last forward, 3: of the last backward, 4: substeps solved,
+ *  5: worst final relative residual, 6: last loss, 7: foreign constraint entries (tiled PCG),
+ *  8: halo slots summed over tiles, 9: E, 10: V, 11: T, 12: vertex tiles, 13: TMA path on. */
 int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
 
 /* Kernel classes timed by the opt-in event profiler (dxpbd_profile / dxpbd_kernel_times). */

@@ -274,7 +274,7 @@ struct dxpbd_scene {
     std::vector<int32_t> vperm_h;         // internal -> user vertex
     DBuf<int32_t> vperm;
     int ntiles = 0;
-    int64_t n_foreign = 0;
+    int64_t n_foreign = 0, halo_total = 0;
     DBuf<int> d_seg;                      // [(n_dist_colors) * (ntiles+1)] (color, owner tile) offsets
     DBuf<int> d_fseg, d_fidx;             // foreign (b-endpoint) constraint lists per (color, tile)
     DBuf<int4> d_fent;                    // foreign entries {j, a, b, 0}
@@ -321,7 +321,7 @@ struct dxpbd_scene {
     bool have_grads = false;
 
     // stats
-    double stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double stats[16] = {0};
     // opt-in event profiler
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -730,6 +730,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 return (int)(std::lower_bound(halo[t].begin(), halo[t].end(), v) - halo[t].begin());
             };
             s->hcap = (hmax + 31) / 32 * 32;
+            s->halo_total = hoff[nt];
             s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors;
             if (s->use_tma) {
                 std::vector<int> hlist(std::max(hoff[nt], 1));
@@ -1227,7 +1228,14 @@ int dxpbd_kernel_times(dxpbd_scene *s, double *ms, double *count, int32_t n) {
 int dxpbd_stats(dxpbd_scene *s, double *out, int32_t n) {
     DX_API_BEGIN
     DX_REQUIRE(s && out, DXPBD_ERR_ARG, "null argument");
-    for (int k = 0; k < n && k < 8; ++k) out[k] = s->stats[k];
+    s->stats[7] = (double)s->n_foreign;
+    s->stats[8] = (double)s->halo_total;
+    s->stats[9] = (double)s->E;
+    s->stats[10] = (double)s->V;
+    s->stats[11] = (double)s->T;
+    s->stats[12] = (double)s->ntiles;
+    s->stats[13] = s->use_tma ? 1.0 : 0.0;
+    for (int k = 0; k < n && k < 16; ++k) out[k] = s->stats[k];
     DX_API_END
 }
 

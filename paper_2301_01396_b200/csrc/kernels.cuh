@@ -456,7 +456,7 @@ __global__ void k_cg_init(int V, const float4 *__restrict__ b, float4 *__restric
 // walks its segment of every color, accumulates q for its own vertices in shared memory and
 // flushes each owned vertex with one vector reduction; only endpoints outside the tile (halo)
 // use global reductions.  With DOT it also accumulates p.(A p) = Sum_j d^T Q_j d.
-constexpr int kTileV = 1024;
+constexpr int kTileV = 512;
 
 template <int QF>
 struct QVal {
@@ -620,8 +620,8 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
 // purely in shared memory (plain read-modify-write of the accumulator, one barrier per color,
 // vertex-disjoint within a color by R1).
 constexpr int kTmaStages = 3;
-constexpr int kFCap = 256;
-constexpr int kTmaThreads = 512;
+constexpr int kFCap = 128;
+constexpr int kTmaThreads = 256;
 
 struct TmaTiles {
     int ncol, ntiles;
@@ -726,7 +726,7 @@ DX_INLINE float tma_tile_colors(uint64_t *bars, TmaStage *stages, float (*sp)[1]
 }
 
 // Fused PCG matvec (see k_cg_matvec): p_it update for own and halo vertices, q = A p, p.q.
-__global__ void __launch_bounds__(kTmaThreads, 2) k_cg_matvec_tma(int it, TmaTiles T, int V, int hcap,
+__global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTiles T, int V, int hcap,
                                                                   const float *__restrict__ Qc, CGBufs B,
                                                                   const float *__restrict__ wv, CGState s) {
     if (cg_done(s, it + 1)) return;
@@ -759,22 +759,48 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cg_matvec_tma(int it, TmaTil
     float4 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
     const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
-    for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
+    // vertex phase: all loads of a thread (own vertices and halo slots) are issued as one batch,
+    // unconditionally, before any use (no load behind a w > 0 branch)
+    constexpr int NO = kTileV / kTmaThreads;
+    float wo[NO];
+    float4 ro[NO], po[NO];
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int i = threadIdx.x + u * kTmaThreads;
+        const int v = min(v0 + i, V - 1);
+        wo[u] = wv[v];
+        ro[u] = it > 0 ? B.r[v] : pnew[v];
+        po[u] = it > 0 ? pold[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
+    constexpr int NH = 2;
+    int hv[NH];
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        const int h = threadIdx.x + u * kTmaThreads;
+        hv[u] = h < nh ? T.hlist[h0 + h] : -1;
+    }
+    float hw[NH];
+    float4 hr[NH], hp[NH];
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        const int v = max(hv[u], 0);
+        hw[u] = wv[v];
+        hr[u] = it > 0 ? B.r[v] : pnew[v];
+        hp[u] = it > 0 ? pold[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int i = threadIdx.x + u * kTmaThreads;
         float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
         float3 qv = make_float3(0.f, 0.f, 0.f);
         if (i < nv) {
             const int v = v0 + i;
-            const float w = wv[v];
-            if (it > 0) {
-                if (w > 0.f) {
-                    float4 rv = B.r[v], po = pold[v];
-                    pv = make_float4(w * rv.x + beta * po.x, w * rv.y + beta * po.y, w * rv.z + beta * po.z, 0.f);
-                }
-                pnew[v] = pv;
-            } else {
-                pv = pnew[v];
-            }
+            const float w = wo[u];
             if (w > 0.f) {
+                pv = it > 0 ? make_float4(w * ro[u].x + beta * po[u].x, w * ro[u].y + beta * po[u].y,
+                                          w * ro[u].z + beta * po[u].z, 0.f)
+                            : ro[u];
                 float3 pp = f3(pv);
                 qv = (1.f / w) * pp;
                 if (Qc) {
@@ -784,6 +810,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cg_matvec_tma(int it, TmaTil
                 }
                 acc[0] += dot3(pp, qv);
             }
+            if (it > 0) pnew[v] = pv;
         }
         sp[i] = pv.x;
         sp[spn + i] = pv.y;
@@ -792,8 +819,21 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cg_matvec_tma(int it, TmaTil
         sq[kTileV + i] = qv.y;
         sq[2 * kTileV + i] = qv.z;
     }
-    const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
-    for (int h = threadIdx.x; h < nh; h += blockDim.x) {
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        const int h = threadIdx.x + u * kTmaThreads;
+        if (hv[u] >= 0) {
+            float3 pv = make_float3(0.f, 0.f, 0.f);
+            if (hw[u] > 0.f)
+                pv = it > 0 ? make_float3(hw[u] * hr[u].x + beta * hp[u].x, hw[u] * hr[u].y + beta * hp[u].y,
+                                          hw[u] * hr[u].z + beta * hp[u].z)
+                            : f3(hr[u]);
+            sp[kTileV + h] = pv.x;
+            sp[spn + kTileV + h] = pv.y;
+            sp[2 * spn + kTileV + h] = pv.z;
+        }
+    }
+    for (int h = threadIdx.x + NH * kTmaThreads; h < nh; h += blockDim.x) {   // rare: large halos
         const int v = T.hlist[h0 + h];
         const float3 pv = halo_p(it, v, beta, B.r, pold, pnew, wv);
         sp[kTileV + h] = pv.x;
@@ -813,7 +853,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cg_matvec_tma(int it, TmaTil
 //   b  = M u + dphi - (Qc + A) y              (the system right-hand side, for its norm)
 //   r0 = b - (M + Qc + A) u = dphi - (Qc + A)(y + u)   (residual at the warm start u_n := u_{n+1})
 // A_dist is applied to y and to z = y + u in the same pass (Q read once).  Writes b, r0.
-__global__ void __launch_bounds__(kTmaThreads, 1) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
+__global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
                                                             const float4 *__restrict__ u, const float4 *__restrict__ y,
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                             const float *__restrict__ weights, const float *__restrict__ wv,
