@@ -1,0 +1,125 @@
+"""GPU edge cases and full-size checks of the C-ABI path against the oracle (or against
+properties that hold at any size where the oracle cannot run: zero goal => zero gradients,
+linearity of the adjoint in dphi/dq)."""
+import numpy as np
+import pytest
+
+from synth import Scene, tiny_cloth, large_cloth, garment, medium_cloth
+from synth.scenes import _base
+from tests.gpu_helpers import f32, gpu_run, oracle_run, rel_l2
+from tests.test_gpu_cloth import _compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    from paper_2301_01396_b200 import api
+    return api
+
+
+def test_contacts_only_no_constraints():
+    """E = 0: a free particle cloud falling onto a sphere (contact path alone)."""
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-0.2, 0.2, size=(300, 3)) + np.array([0, 0.32, 0])
+    d = _base("pts", 300, x_rest=x, inv_mass=np.full(300, 1000.0), spheres=np.array([[0, 0, 0, 0.3]]))
+    s = f32(Scene(**d, frame_dt=1 / 60, substeps=5, iterations=1, frames=3, thickness=0.005,
+                  collision_compliance=1e-9, key_frames=np.array([3], np.int32), targets=(x - 0.05)[None]))
+    g = gpu_run(s, ("sphere",))
+    o = oracle_run(s)
+    _compare(g, o, ("sphere", "x0", "v0"))
+
+
+def test_zero_keyframes_and_keyframe_at_frame0():
+    api = _api()
+    s = f32(tiny_cloth(n=8, frames=2))
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=2, grad_flags=api.flags("compliance", "v0"))
+    api.dxpbd_forward(sc, s.x0, s.v0, None, 2)
+    loss = api.dxpbd_backward(sc, [], np.zeros((0, s.num_vertices, 3), np.float32))
+    assert loss == 0.0
+    assert np.abs(api.dxpbd_grads(sc, "compliance")).max() == 0.0
+    assert np.abs(api.dxpbd_grads(sc, "v0")).max() == 0.0
+    # keyframe at frame 0 only: dphi/dx0 = W (x0 - x*), every other gradient 0
+    tgt = s.x0 + 0.01
+    loss = api.dxpbd_backward(sc, [0], tgt[None])
+    gx = api.dxpbd_grads(sc, "x0")
+    free = s.inv_mass > 0
+    np.testing.assert_allclose(gx[free], (s.x0 - tgt)[free], rtol=1e-6, atol=1e-9)
+    assert np.abs(api.dxpbd_grads(sc, "v0")).max() == 0.0
+    assert loss == pytest.approx(0.5 * (0.01 ** 2) * 3 * s.num_vertices, rel=1e-5)
+
+
+def test_all_pinned_and_zero_frames():
+    api = _api()
+    s = f32(tiny_cloth(n=4, frames=1))
+    s = s.replace(inv_mass=np.zeros_like(s.inv_mass))
+    g = gpu_run(s, ("compliance", "v0"))
+    np.testing.assert_array_equal(g["x"][-1], g["x"][0])
+    assert np.abs(g["compliance"]).max() == 0.0 and np.abs(g["v0"]).max() == 0.0
+    s2 = f32(tiny_cloth(n=4, frames=1))
+    sc = api.dxpbd_create(**api.scene_kwargs(s2), max_frames=1)
+    api.dxpbd_forward(sc, s2.x0, s2.v0, None, 0)
+    np.testing.assert_array_equal(api.dxpbd_positions(sc, 0), s2.x0.astype(np.float32))
+
+
+def test_errors_are_reported():
+    api = _api()
+    s = f32(tiny_cloth(n=4, frames=1))
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=1)
+    with pytest.raises(api.DxpbdError):
+        api.dxpbd_backward(sc, [1], s.targets)          # backward before forward
+    with pytest.raises(api.DxpbdError):
+        api.dxpbd_forward(sc, s.x0, s.v0, None, 5)      # exceeds max_frames
+    bad = s.dist_idx.copy()
+    bad[0, 0] = s.num_vertices + 3
+    kw = api.scene_kwargs(s)
+    kw["dist_idx"] = bad
+    with pytest.raises(api.DxpbdError):
+        api.dxpbd_create(**kw, max_frames=1)
+
+
+def test_large_cloth_full_size_one_substep():
+    """configs[4] at full size (2944^2, 26M DoF), one substep with its forces: all positions."""
+    s = f32(large_cloth(frames=1, substeps=1, key_frames=(1,)).replace(frame_dt=1 / 600))
+    g = gpu_run(s, backward=False)
+    o = oracle_run(s, backward=False)
+    assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
+    # the step itself, to the float32 output quantum (|x| ~ 5 m -> ulp 4.8e-7 m)
+    step_err = np.abs((g["x"][-1] - g["x"][0]) - (o["x"][-1] - o["x"][0])).max()
+    assert step_err < 1e-6, step_err
+
+
+def test_large_cloth_full_size_adjoint_properties():
+    """configs[4] at full size, 2 frames: the adjoint is linear in dphi/dq (g(x* - 2d) - g0 =
+    2 (g(x* - d) - g0) to PCG tolerance) and a goal at the simulated state (up to the float32
+    output quantum, ~1e-7 m) gives gradients 1e-4 smaller than a 1e-3 m residual."""
+    api = _api()
+    s = f32(large_cloth(frames=2, key_frames=(2,)))
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=2, grad_flags=api.flags("forces"))
+    api.dxpbd_forward(sc, s.x0, s.v0, s.forces, 2)
+    x2 = api.dxpbd_positions(sc, 2)
+    api.dxpbd_backward(sc, [2], x2[None])
+    g0 = api.dxpbd_grads(sc, "forces")
+    d = np.random.default_rng(0).standard_normal(x2.shape).astype(np.float32) * 1e-3
+    api.dxpbd_backward(sc, [2], (x2 - d)[None])
+    g1 = api.dxpbd_grads(sc, "forces")
+    api.dxpbd_backward(sc, [2], (x2 - 2 * d)[None])
+    g2 = api.dxpbd_grads(sc, "forces")
+    assert np.isfinite(g1).all() and np.abs(g1).max() > 0
+    assert np.abs(g0).max() < 1e-3 * np.abs(g1).max()
+    assert rel_l2(g2 - g0, 2 * (g1 - g0)) < 1e-4
+
+
+def test_garment_full_size_one_frame_forward():
+    """configs[3] at full size (512x512 tube, 12 capsules), 1 frame x 10 substeps."""
+    s = f32(garment(frames=1))
+    g = gpu_run(s, backward=False)
+    o = oracle_run(s, backward=False)
+    assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
+
+
+def test_medium_cloth_full_size_backward_short():
+    """configs[1] at full size (256^2, sphere), one substep at its dt: gradients of compliance and x0."""
+    s = f32(medium_cloth(frames=1, substeps=1).replace(frame_dt=1 / 600))
+    g = gpu_run(s, ("compliance", "x0"))
+    o = oracle_run(s)
+    _compare(g, o, ("compliance", "x0", "v0"))
