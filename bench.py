@@ -177,21 +177,18 @@ def algo_bytes(cls, st, units_per_launch=None):
 def run_ours(a):
     import numpy as np
     import torch
-    import torch.distributed as dist
     from paper_2301_01396_b200 import api
     from synth import large_cloth
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+    from paper_2301_01396_b200 import parallel as par
+    env = par.init("nccl")
+    world, rank, local = env.world, env.rank, env.local_rank
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
     side = 10.0 * (a.n - 1) / 2943.0
-    s = large_cloth(n=a.n, frames=a.frames, substeps=a.substeps, iterations=a.iterations, seed=4 + rank,
+    s = large_cloth(n=a.n, frames=a.frames, substeps=a.substeps, iterations=a.iterations, seed=par.scene_seed(4, rank),
                     side=side, with_forces=False, key_frames=tuple(k for k in (10, 20, 30) if k <= a.frames)
                     or (a.frames,))
     V, E = s.num_vertices, len(s.dist_idx)
@@ -221,8 +218,7 @@ def run_ours(a):
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    par.barrier()
     clocks = Clocks(local)
     clocks.start()
     if not a.no_profile:
@@ -231,8 +227,7 @@ def run_ours(a):
            torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     launches, cg_iters = 0, 0
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    par.barrier()
     for i in range(a.steps):
         ev[i][0].record(stream)
         loss = step(ev[i][1])
@@ -241,22 +236,17 @@ def run_ours(a):
         launches += int(st["fwd_launches"] + st["bwd_launches"]) + 1
         cg_iters += int(st["cg_iters_total"])
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    par.barrier()
     clk = clocks.stop()
     t_steps = [ev[i][0].elapsed_time(ev[i][2]) for i in range(a.steps)]
     t_fwds = [ev[i][0].elapsed_time(ev[i][1]) for i in range(a.steps)]
     ktimes = api.dxpbd_kernel_times(sc) if not a.no_profile else {}
     api.dxpbd_profile(sc, False)
-    total_ms = sum(t_steps)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = par.reduce_max(sum(t_steps), device=dev)
     ms_per_step = total_ms / a.steps
     substeps_total = a.frames * a.substeps
     solves_per_step = E * a.iterations * substeps_total
-    value = world * solves_per_step / (ms_per_step / 1e3)
+    value = par.job_throughput(solves_per_step, ms_per_step, world)
 
     # ---- e2e through the public API with pinned host buffers (copies inside the timed region)
     e2e = None
@@ -264,8 +254,7 @@ def run_ours(a):
         gforce_h = torch.empty((a.frames, V, 3), dtype=torch.float32).pin_memory()
         n_e2e = max(1, min(2, a.steps))
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        par.barrier()
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -277,14 +266,10 @@ def run_ours(a):
         e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        e2e_ms = max(e0.elapsed_time(e1), 1e3 * wall) / n_e2e
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = par.reduce_max(max(e0.elapsed_time(e1), 1e3 * wall) / n_e2e, device=dev)
         h2d = 4 * (x0_h.numel() + v0_h.numel() + forces_h.numel() + tg_h.numel())
         d2h = 4 * gforce_h.numel() + 4
-        e2e = {"value": world * solves_per_step / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": par.job_throughput(solves_per_step, e2e_ms, world), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
     # ---- roofline of the dominant kernel class
@@ -334,8 +319,7 @@ def run_ours(a):
             "kernel_ms_per_step": {k: v[0] / a.steps for k, v in ktimes.items()},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    par.shutdown()
 
 
 def main():
