@@ -309,7 +309,7 @@ struct dxpbd_scene {
 
     // backward
     DBuf<double4> xr;
-    DBuf<float4> ax, rhs, y, r, p, q, p1;
+    DBuf<float4> ax, rhs, y, r, p, q, p1, uprev, u0;
     int qf = 0;   // Q format: 0 = sym6 SoA, 1 = iso+rank1 float4 (K = 1 with PD projection)
     DBuf<float> Qd, ed, Qc, ec;
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
@@ -931,6 +931,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     if (s->xr.n < (size_t)V) s->xr.alloc(V);
     auto ensure4 = [&](DBuf<float4> &b) { if (b.n < (size_t)V) b.alloc(V); };
     ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
+    ensure4(s->uprev); ensure4(s->u0);
     if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);
     const bool g_comp = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
     const bool g_forces = (s->grad_flags >> DXPBD_GRAD_FORCES) & 1;
@@ -995,6 +996,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     auto tgt = [&](int n) -> const float * { return key_of[n] >= 0 ? s->targets.p + (size_t)key_of[n] * V * 3 : nullptr; };
     DX_CHECK_CUDA(cudaMemsetAsync(s->y.p, 0, sizeof(float4) * V, st));
     DX_CHECK_CUDA(cudaMemsetAsync(s->ax.p, 0, sizeof(float4) * V, st));   // ax holds u
+    DX_CHECK_CUDA(cudaMemsetAsync(s->uprev.p, 0, sizeof(float4) * V, st));
     int last_key_state = -1;
     for (int n = 0; n <= N; ++n) if (key_of[n] >= 0) last_key_state = n;
     int launches = num_keys + 2, total_it = 0, max_it = 0;
@@ -1014,25 +1016,29 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
                         s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p};
             if (s->use_tma)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_rhs_smem, st>>>(
-                    tt, V, s->hcap, Qc, s->ax.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p, s->r.p));
+                    tt, V, s->hcap, Qc, s->ax.p, s->uprev.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
+                    s->r.p, s->u0.p));
             else if (s->qf == 1)
-                LAUNCH(DXPBD_K_RHS, k_rhs_tiled<1><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->y.p,
-                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p,
-                                                                                 s->rhs.p, s->r.p));
+                LAUNCH(DXPBD_K_RHS, k_rhs_tiled<1><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->uprev.p,
+                                                                                 s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p,
+                                                                                 s->rhs.p, s->r.p, s->u0.p));
             else
-                LAUNCH(DXPBD_K_RHS, k_rhs_tiled<0><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->y.p,
-                                                                                 state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p,
-                                                                                 s->rhs.p, s->r.p));
+                LAUNCH(DXPBD_K_RHS, k_rhs_tiled<0><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->uprev.p,
+                                                                                 s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p,
+                                                                                 s->rhs.p, s->r.p, s->u0.p));
             ++launches;
         }
         if (s->T) {
-            LAUNCH(DXPBD_K_RHS, k_rhs_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->t_Q.p, s->y.p, s->ax.p, s->rhs.p, s->r.p,
+            LAUNCH(DXPBD_K_RHS, k_rhs_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->t_Q.p, s->y.p, s->u0.p, s->rhs.p, s->r.p,
                                                                         s->inv_mass.p));
             ++launches;
         }
         int iters = 0;
         double rel = 0.0;
+        // rotate: the PCG iterates on the warm start u0; afterwards ax = u_n, uprev = u_{n+1}
+        std::swap(s->ax.p, s->u0.p);      // ax <- u0 (solution buffer), u0 <- u_{n+1}
         launches += pcg_solve(s, st, iters, rel);   // u_n into s->ax
+        std::swap(s->uprev.p, s->u0.p);   // uprev <- u_{n+1}, u0 <- u_{n+2} (free)
         total_it += iters;
         max_it = std::max(max_it, iters);
         worst = std::max(worst, rel);

@@ -849,15 +849,18 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// Increment-system right-hand side with warm start (kernels "adjoint"): for own vertices
+// Increment-system right-hand side with warm start (kernels "adjoint"): for own vertices, with
+// u = u_{n+1}, uprev = u_{n+2} and the extrapolated initial guess u0 = 2u - uprev,
 //   b  = M u + dphi - (Qc + A) y              (the system right-hand side, for its norm)
-//   r0 = b - (M + Qc + A) u = dphi - (Qc + A)(y + u)   (residual at the warm start u_n := u_{n+1})
-// A_dist is applied to y and to z = y + u in the same pass (Q read once).  Writes b, r0.
+//   r0 = b - (M + Qc + A) u0 = dphi - M (u - uprev) - (Qc + A)(y + u0)
+// A_dist is applied to y and to z = y + u0 in the same pass (Q read once).  Writes b, r0, u0.
 __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
-                                                            const float4 *__restrict__ u, const float4 *__restrict__ y,
+                                                            const float4 *__restrict__ u, const float4 *__restrict__ uprev,
+                                                            const float4 *__restrict__ y,
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                             const float *__restrict__ weights, const float *__restrict__ wv,
-                                                            float4 *__restrict__ bout, float4 *__restrict__ r0out) {
+                                                            float4 *__restrict__ bout, float4 *__restrict__ r0out,
+                                                            float4 *__restrict__ u0out) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 64);
@@ -892,9 +895,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
             const float w = wv[v];
             yv = f3(y[v]);
             const float3 uv = f3(u[v]);
-            zv = yv + uv;
+            const float3 dv = uv - f3(uprev[v]);          // warm start u0 = u + (u - uprev)
+            const float3 u0 = uv + dv;
+            zv = yv + u0;
+            u0out[v] = w > 0.f ? make_float4(u0.x, u0.y, u0.z, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
             if (w > 0.f) {
                 bb = (1.f / w) * uv;
+                rr = (-1.f / w) * dv;
                 if (Qc) {
                     Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
                                   Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
@@ -919,7 +926,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
     const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
     for (int h = threadIdx.x; h < nh; h += blockDim.x) {
         const int v = T.hlist[h0 + h];
-        const float3 yv = f3(y[v]), zv = yv + f3(u[v]);
+        const float3 uh = f3(u[v]);
+        const float3 yv = f3(y[v]), zv = yv + uh + (uh - f3(uprev[v]));
         sy[kTileV + h] = yv.x; sy[spn + kTileV + h] = yv.y; sy[2 * spn + kTileV + h] = yv.z;
         sz[kTileV + h] = zv.x; sz[spn + kTileV + h] = zv.y; sz[2 * spn + kTileV + h] = zv.z;
     }
@@ -1003,10 +1011,12 @@ __global__ void k_cg_start(int V, const float4 *__restrict__ b, float4 *__restri
 template <int QF>
 __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const int2 *__restrict__ idx,
                                                       const float *__restrict__ Q, int E, const float *__restrict__ Qc,
-                                                      const float4 *__restrict__ u, const float4 *__restrict__ y,
+                                                      const float4 *__restrict__ u, const float4 *__restrict__ uprev,
+                                                      const float4 *__restrict__ y,
                                                       const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                       const float *__restrict__ weights, const float *__restrict__ wv,
-                                                      float4 *__restrict__ bout, float4 *__restrict__ r0out) {
+                                                      float4 *__restrict__ bout, float4 *__restrict__ r0out,
+                                                      float4 *__restrict__ u0out) {
     __shared__ float sy[3][kTileV], sz[3][kTileV], sqb[3][kTileV], sqr[3][kTileV];
     const int t = blockIdx.x;
     const int v0 = t * kTileV;
@@ -1018,9 +1028,13 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const 
             const float w = wv[v];
             yv = f3(y[v]);
             const float3 uv = f3(u[v]);
-            zv = yv + uv;
+            const float3 dv = uv - f3(uprev[v]);          // warm start u0 = u + (u - uprev)
+            const float3 u0 = uv + dv;
+            zv = yv + u0;
+            u0out[v] = w > 0.f ? make_float4(u0.x, u0.y, u0.z, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
             if (w > 0.f) {
                 bb = (1.f / w) * uv;
+                rr = (-1.f / w) * dv;
                 if (Qc) {
                     Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
                                   Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
@@ -1056,7 +1070,8 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const 
                 zb = make_float3(sz[0][lb], sz[1][lb], sz[2][lb]);
             } else {
                 yb = f3(y[ab.y]);
-                zb = yb + f3(u[ab.y]);
+                const float3 ub = f3(u[ab.y]);
+                zb = yb + ub + (ub - f3(uprev[ab.y]));
             }
             const float3 qy = qmul<QF>(Q, j, E, make_float3(sy[0][la], sy[1][la], sy[2][la]) - yb);
             const float3 qz = qmul<QF>(Q, j, E, make_float3(sz[0][la], sz[1][la], sz[2][la]) - zb);
@@ -1071,7 +1086,8 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const 
         for (int k2 = fb + threadIdx.x; k2 < fe; k2 += blockDim.x) {
             const int4 f4 = L.fent[k2];   // {j, a, b}: b in tile
             const int lb = f4.z - v0;
-            const float3 ya = f3(y[f4.y]), za = ya + f3(u[f4.y]);
+            const float3 ua = f3(u[f4.y]);
+            const float3 ya = f3(y[f4.y]), za = ya + ua + (ua - f3(uprev[f4.y]));
             const float3 qy = qmul<QF>(Q, f4.x, E, ya - make_float3(sy[0][lb], sy[1][lb], sy[2][lb]));
             const float3 qz = qmul<QF>(Q, f4.x, E, za - make_float3(sz[0][lb], sz[1][lb], sz[2][lb]));
             sqb[0][lb] += qy.x; sqb[1][lb] += qy.y; sqb[2][lb] += qy.z;

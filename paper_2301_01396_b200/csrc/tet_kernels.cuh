@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// Tet part of the increment rhs: b -= G^T Qt~ G y, r0 -= G^T Qt~ G (y + u)
+// Tet part of the increment rhs: b -= G^T Qt~ G y, r0 -= G^T Qt~ G (y + u0), u0 = warm start
 __global__ void __launch_bounds__(kBlock) k_rhs_tet(TetDev D, const float *__restrict__ Qt, const float4 *__restrict__ y,
                                                     const float4 *__restrict__ u, float4 *__restrict__ b,
                                                     float4 *__restrict__ r0, const float *__restrict__ wv) {
