@@ -165,10 +165,10 @@ def algo_bytes(cls, st, units_per_launch=None):
     if cls == "dist_replay":    # + Q 16 + foreign slot 4 (+ its fQ copy for foreign constraints)
         return (164.0 + 16.0 * NF / max(E, 1)) * units_per_launch
     if cls == "cg_dist":        # TMA matvec: cpair 4 + Q 16 per constraint, fpair 4 + fQ 16 per foreign entry,
-        # hlist 4 + (r, p_old 32 + w 4) per halo slot, own r 16 + p_old 16 + w 4 + p_new 16 + q 16
-        return 20.0 * E + 20.0 * NF + 40.0 * H + 68.0 * V
-    if cls == "cg_update":      # u r/w 32, r r/w 32, p 16, q 16, w 4
-        return 100.0 * V
+        # hlist 4 + (r, p_old 24 + w 4) per halo slot, own r 12 + p_old 12 + w 4 + p_new 12 + q 12 (float3 fields)
+        return 20.0 * E + 20.0 * NF + 32.0 * H + 52.0 * V
+    if cls == "cg_update":      # u r/w 24, r r/w 24, p 12, q 12, w 4
+        return 76.0 * V
     if cls == "predict":        # x_n 32, x_{n-1} 32, f 12, out 32
         return 108.0 * V
     return None

@@ -7,6 +7,7 @@
 
 // ---------------------------------------------------------------- float3 helpers
 DX_INLINE float3 f3(float4 a) { return make_float3(a.x, a.y, a.z); }
+DX_INLINE float3 f3(float3 a) { return a; }
 DX_INLINE float3 operator+(float3 a, float3 b) { return make_float3(a.x + b.x, a.y + b.y, a.z + b.z); }
 DX_INLINE float3 operator-(float3 a, float3 b) { return make_float3(a.x - b.x, a.y - b.y, a.z - b.z); }
 DX_INLINE float3 operator*(float s, float3 a) { return make_float3(s * a.x, s * a.y, s * a.z); }
@@ -157,6 +158,14 @@ DX_INLINE void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *ba
 }
 DX_INLINE void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 DX_INLINE void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// packed float3 (12 B) vector fields: componentwise global reductions
+DX_INLINE void red_add_f3(float3 *addr, float3 v) {
+    float *a = reinterpret_cast<float *>(addr);
+    atomicAdd(a, v.x);
+    atomicAdd(a + 1, v.y);
+    atomicAdd(a + 2, v.z);
+}
 
 // ---------------------------------------------------------------- reductions
 DX_INLINE float warp_sum(float v) {

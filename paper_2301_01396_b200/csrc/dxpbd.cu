@@ -309,7 +309,7 @@ struct dxpbd_scene {
 
     // backward
     DBuf<double4> xr;
-    DBuf<float4> ax, rhs, y, r, p, q, p1, uprev, u0;
+    DBuf<float3> ax, rhs, y, r, p, q, p1, uprev, u0;   // packed 12 B vector fields
     int qf = 0;   // Q format: 0 = sym6 SoA, 1 = iso+rank1 float4 (K = 1 with PD projection)
     DBuf<float> Qd, ed, Qc, ec;
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
@@ -929,7 +929,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         DX_REQUIRE(key_frames[k] >= 0 && key_frames[k] <= s->frames_done, DXPBD_ERR_ARG, "key frame out of range");
     // buffers
     if (s->xr.n < (size_t)V) s->xr.alloc(V);
-    auto ensure4 = [&](DBuf<float4> &b) { if (b.n < (size_t)V) b.alloc(V); };
+    auto ensure4 = [&](DBuf<float3> &b) { if (b.n < (size_t)V) b.alloc(V); };
     ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
     ensure4(s->uprev); ensure4(s->u0);
     if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);
@@ -994,9 +994,9 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         LAUNCH(DXPBD_K_OTHER, k_loss<<<nblk(V), kBlock, 0, st>>>(V, state(s, key_frames[k] * sub), s->targets.p + (size_t)k * V * 3, wts, s->acc.p));
     // increment-form adjoint (kernels.cuh "adjoint"): y = u = 0 beyond the horizon
     auto tgt = [&](int n) -> const float * { return key_of[n] >= 0 ? s->targets.p + (size_t)key_of[n] * V * 3 : nullptr; };
-    DX_CHECK_CUDA(cudaMemsetAsync(s->y.p, 0, sizeof(float4) * V, st));
-    DX_CHECK_CUDA(cudaMemsetAsync(s->ax.p, 0, sizeof(float4) * V, st));   // ax holds u
-    DX_CHECK_CUDA(cudaMemsetAsync(s->uprev.p, 0, sizeof(float4) * V, st));
+    DX_CHECK_CUDA(cudaMemsetAsync(s->y.p, 0, sizeof(float3) * V, st));
+    DX_CHECK_CUDA(cudaMemsetAsync(s->ax.p, 0, sizeof(float3) * V, st));   // ax holds u
+    DX_CHECK_CUDA(cudaMemsetAsync(s->uprev.p, 0, sizeof(float3) * V, st));
     int last_key_state = -1;
     for (int n = 0; n <= N; ++n) if (key_of[n] >= 0) last_key_state = n;
     int launches = num_keys + 2, total_it = 0, max_it = 0;

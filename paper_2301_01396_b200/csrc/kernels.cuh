@@ -431,23 +431,6 @@ DX_INLINE bool cg_done(const CGState &s, int it) {
 
 // init: r = b (filtered), y = 0, p = M^-1 r ; slot[-1] rz = r.M^-1 r stored in sc[...] of "it=-1"
 // we store it in slot 0 field 1 of a dedicated init slot: sc layout shifted by one (slot 0 = init).
-__global__ void k_cg_init(int V, const float4 *__restrict__ b, float4 *__restrict__ y, float4 *__restrict__ r,
-                          float4 *__restrict__ p, const float *__restrict__ wv, CGState s) {
-    int v = blockIdx.x * blockDim.x + threadIdx.x;
-    float acc[3] = {0.f, 0.f, 0.f};
-    if (v < V) {
-        float w = wv[v];
-        float4 bb = b[v];
-        if (!(w > 0.f)) bb = make_float4(0.f, 0.f, 0.f, 0.f);
-        y[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        r[v] = bb;
-        float4 pp = make_float4(w * bb.x, w * bb.y, w * bb.z, 0.f);
-        p[v] = pp;
-        acc[1] = bb.x * pp.x + bb.y * pp.y + bb.z * pp.z;   // r.z
-        acc[2] = bb.x * bb.x + bb.y * bb.y + bb.z * bb.z;   // r.r
-    }
-    block_reduce_add<3>(acc, s.sc);   // slot 0
-}
 
 // distance-constraint part of q += sgn * Sum_j P_j^T Q_j P_j p (pinned rows filtered), tiled:
 // vertices are stored in Morton order; every constraint is oriented
@@ -497,8 +480,8 @@ DX_INLINE float3 qmul(const float *__restrict__ Q, int j, size_t E, float3 d) {
 // constraints are vertex-disjoint (R1), so the shared-memory accumulation is a plain
 // read-modify-write with one barrier per color and no atomics; q is stored once per vertex.
 // p.q is accumulated over own vertices and own constraints only.
-struct CGBufs {
-    float4 *u, *r, *p0, *p1, *q, *qh;
+struct CGBufs {   // packed float3 (12 B) vector fields
+    float3 *u, *r, *p0, *p1, *q, *qh;
 };
 struct TileLists {
     int ncol, ntiles;
@@ -508,12 +491,12 @@ struct TileLists {
     const int4 *fent;  // foreign entries {j, a, b, 0} (same order as fidx)
 };
 
-DX_INLINE float3 halo_p(int it, int v, float beta, const float4 *__restrict__ r, const float4 *__restrict__ pold,
-                        const float4 *__restrict__ pnew, const float *__restrict__ wv) {
+DX_INLINE float3 halo_p(int it, int v, float beta, const float3 *__restrict__ r, const float3 *__restrict__ pold,
+                        const float3 *__restrict__ pnew, const float *__restrict__ wv) {
     if (it == 0) return f3(pnew[v]);
     const float w = wv[v];
     if (!(w > 0.f)) return make_float3(0.f, 0.f, 0.f);
-    const float4 rv = r[v], po = pold[v];
+    const float3 rv = r[v], po = pold[v];
     return make_float3(w * rv.x + beta * po.x, w * rv.y + beta * po.y, w * rv.z + beta * po.z);
 }
 
@@ -528,20 +511,20 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
     const int t = blockIdx.x;
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
-    const float4 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;   // p_{it-1}
-    float4 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;         // p_it
+    const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;   // p_{it-1}
+    float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;         // p_it
     const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
     for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
-        float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 pv = make_float3(0.f, 0.f, 0.f);
         float3 qv = make_float3(0.f, 0.f, 0.f);
         if (i < nv) {
             const int v = v0 + i;
             const float w = wv[v];
             if (it > 0) {
                 if (w > 0.f) {
-                    float4 rv = B.r[v], po = pold[v];
-                    pv = make_float4(w * rv.x + beta * po.x, w * rv.y + beta * po.y, w * rv.z + beta * po.z, 0.f);
+                    float3 rv = B.r[v], po = pold[v];
+                    pv = make_float3(w * rv.x + beta * po.x, w * rv.y + beta * po.y, w * rv.z + beta * po.z);
                 }
                 pnew[v] = pv;
             } else {
@@ -602,7 +585,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
     }
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i;
-        B.q[v] = wv[v] > 0.f ? make_float4(sq[0][i], sq[1][i], sq[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        B.q[v] = wv[v] > 0.f ? make_float3(sq[0][i], sq[1][i], sq[2][i]) : make_float3(0.f, 0.f, 0.f);
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
@@ -755,22 +738,22 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
         fence_mbar_init();
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages[c], c, sb, T);
     }
-    const float4 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
-    float4 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
+    const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
+    float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
     const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
     // vertex phase: all loads of a thread (own vertices and halo slots) are issued as one batch,
     // unconditionally, before any use (no load behind a w > 0 branch)
     constexpr int NO = kTileV / kTmaThreads;
     float wo[NO];
-    float4 ro[NO], po[NO];
+    float3 ro[NO], po[NO];
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
         const int i = threadIdx.x + u * kTmaThreads;
         const int v = min(v0 + i, V - 1);
         wo[u] = wv[v];
         ro[u] = it > 0 ? B.r[v] : pnew[v];
-        po[u] = it > 0 ? pold[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        po[u] = it > 0 ? pold[v] : make_float3(0.f, 0.f, 0.f);
     }
     const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
     constexpr int NH = 2;
@@ -781,25 +764,25 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
         hv[u] = h < nh ? T.hlist[h0 + h] : -1;
     }
     float hw[NH];
-    float4 hr[NH], hp[NH];
+    float3 hr[NH], hp[NH];
 #pragma unroll
     for (int u = 0; u < NH; ++u) {
         const int v = max(hv[u], 0);
         hw[u] = wv[v];
         hr[u] = it > 0 ? B.r[v] : pnew[v];
-        hp[u] = it > 0 ? pold[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        hp[u] = it > 0 ? pold[v] : make_float3(0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
         const int i = threadIdx.x + u * kTmaThreads;
-        float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 pv = make_float3(0.f, 0.f, 0.f);
         float3 qv = make_float3(0.f, 0.f, 0.f);
         if (i < nv) {
             const int v = v0 + i;
             const float w = wo[u];
             if (w > 0.f) {
-                pv = it > 0 ? make_float4(w * ro[u].x + beta * po[u].x, w * ro[u].y + beta * po[u].y,
-                                          w * ro[u].z + beta * po[u].z, 0.f)
+                pv = it > 0 ? make_float3(w * ro[u].x + beta * po[u].x, w * ro[u].y + beta * po[u].y,
+                                          w * ro[u].z + beta * po[u].z)
                             : ro[u];
                 float3 pp = f3(pv);
                 qv = (1.f / w) * pp;
@@ -844,7 +827,7 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
     acc[0] += tma_tile_colors<1>(bars, stages, reinterpret_cast<float (*)[1]>(sp), spn, sq, sb, T);
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i;
-        B.q[v] = wv[v] > 0.f ? make_float4(sq[i], sq[kTileV + i], sq[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        B.q[v] = wv[v] > 0.f ? make_float3(sq[i], sq[kTileV + i], sq[2 * kTileV + i]) : make_float3(0.f, 0.f, 0.f);
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
@@ -855,12 +838,12 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
 //   r0 = b - (M + Qc + A) u0 = dphi - M (u - uprev) - (Qc + A)(y + u0)
 // A_dist is applied to y and to z = y + u0 in the same pass (Q read once).  Writes b, r0, u0.
 __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
-                                                            const float4 *__restrict__ u, const float4 *__restrict__ uprev,
-                                                            const float4 *__restrict__ y,
+                                                            const float3 *__restrict__ u, const float3 *__restrict__ uprev,
+                                                            const float3 *__restrict__ y,
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                             const float *__restrict__ weights, const float *__restrict__ wv,
-                                                            float4 *__restrict__ bout, float4 *__restrict__ r0out,
-                                                            float4 *__restrict__ u0out) {
+                                                            float3 *__restrict__ bout, float3 *__restrict__ r0out,
+                                                            float3 *__restrict__ u0out) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 64);
@@ -898,7 +881,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
             const float3 dv = uv - f3(uprev[v]);          // warm start u0 = u + (u - uprev)
             const float3 u0 = uv + dv;
             zv = yv + u0;
-            u0out[v] = w > 0.f ? make_float4(u0.x, u0.y, u0.z, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+            u0out[v] = w > 0.f ? u0 : make_float3(0.f, 0.f, 0.f);
             if (w > 0.f) {
                 bb = (1.f / w) * uv;
                 rr = (-1.f / w) * dv;
@@ -975,8 +958,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i;
         const bool fr = wv[v] > 0.f;
-        bout[v] = fr ? make_float4(sqb[i], sqb[kTileV + i], sqb[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
-        r0out[v] = fr ? make_float4(sqr[i], sqr[kTileV + i], sqr[2 * kTileV + i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        bout[v] = fr ? make_float3(sqb[i], sqb[kTileV + i], sqb[2 * kTileV + i]) : make_float3(0.f, 0.f, 0.f);
+        r0out[v] = fr ? make_float3(sqr[i], sqr[kTileV + i], sqr[2 * kTileV + i]) : make_float3(0.f, 0.f, 0.f);
     }
 }
 
@@ -986,16 +969,16 @@ __host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap) {
 
 // PCG start from the warm start: r = r0 (filtered), p_0 = M^-1 r; slot 0 gets r.z and r.r;
 // the reference norm |b|^2 goes to s.bnorm2.
-__global__ void k_cg_start(int V, const float4 *__restrict__ b, float4 *__restrict__ r, float4 *__restrict__ p,
+__global__ void k_cg_start(int V, const float3 *__restrict__ b, float3 *__restrict__ r, float3 *__restrict__ p,
                            const float *__restrict__ wv, CGState s) {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     float acc[3] = {0.f, 0.f, 0.f};
     if (v < V) {
         const float w = wv[v];
-        float4 rv = r[v], bv = b[v];
-        if (!(w > 0.f)) rv = bv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 rv = r[v], bv = b[v];
+        if (!(w > 0.f)) rv = bv = make_float3(0.f, 0.f, 0.f);
         r[v] = rv;
-        p[v] = make_float4(w * rv.x, w * rv.y, w * rv.z, 0.f);
+        p[v] = make_float3(w * rv.x, w * rv.y, w * rv.z);
         const float r2 = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
         acc[0] = w * r2;
         acc[1] = r2;
@@ -1011,12 +994,12 @@ __global__ void k_cg_start(int V, const float4 *__restrict__ b, float4 *__restri
 template <int QF>
 __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const int2 *__restrict__ idx,
                                                       const float *__restrict__ Q, int E, const float *__restrict__ Qc,
-                                                      const float4 *__restrict__ u, const float4 *__restrict__ uprev,
-                                                      const float4 *__restrict__ y,
+                                                      const float3 *__restrict__ u, const float3 *__restrict__ uprev,
+                                                      const float3 *__restrict__ y,
                                                       const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                       const float *__restrict__ weights, const float *__restrict__ wv,
-                                                      float4 *__restrict__ bout, float4 *__restrict__ r0out,
-                                                      float4 *__restrict__ u0out) {
+                                                      float3 *__restrict__ bout, float3 *__restrict__ r0out,
+                                                      float3 *__restrict__ u0out) {
     __shared__ float sy[3][kTileV], sz[3][kTileV], sqb[3][kTileV], sqr[3][kTileV];
     const int t = blockIdx.x;
     const int v0 = t * kTileV;
@@ -1031,7 +1014,7 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const 
             const float3 dv = uv - f3(uprev[v]);          // warm start u0 = u + (u - uprev)
             const float3 u0 = uv + dv;
             zv = yv + u0;
-            u0out[v] = w > 0.f ? make_float4(u0.x, u0.y, u0.z, 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+            u0out[v] = w > 0.f ? u0 : make_float3(0.f, 0.f, 0.f);
             if (w > 0.f) {
                 bb = (1.f / w) * uv;
                 rr = (-1.f / w) * dv;
@@ -1098,8 +1081,8 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const 
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i;
         const bool fr = wv[v] > 0.f;
-        bout[v] = fr ? make_float4(sqb[0][i], sqb[1][i], sqb[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
-        r0out[v] = fr ? make_float4(sqr[0][i], sqr[1][i], sqr[2][i], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        bout[v] = fr ? make_float3(sqb[0][i], sqb[1][i], sqb[2][i]) : make_float3(0.f, 0.f, 0.f);
+        r0out[v] = fr ? make_float3(sqr[0][i], sqr[1][i], sqr[2][i]) : make_float3(0.f, 0.f, 0.f);
     }
 }
 
@@ -1109,14 +1092,14 @@ __global__ void k_cg_update2(int V, int it, CGBufs B, const float *__restrict__ 
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     float acc[2] = {0.f, 0.f};
     if (v < V) {
-        const float4 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
+        const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
         double pq = s.sc[(it + 1) * 4 + 0];
         float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
         float w = wv[v];
-        float4 uv = B.u[v], rv = B.r[v], pv = p[v], qv = B.q[v];
+        float3 uv = B.u[v], rv = B.r[v], pv = p[v], qv = B.q[v];
         uv.x += alpha * pv.x; uv.y += alpha * pv.y; uv.z += alpha * pv.z;
         rv.x -= alpha * qv.x; rv.y -= alpha * qv.y; rv.z -= alpha * qv.z;
-        if (!(w > 0.f)) rv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!(w > 0.f)) rv = make_float3(0.f, 0.f, 0.f);
         B.u[v] = uv;
         B.r[v] = rv;
         float r2 = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
@@ -1127,12 +1110,12 @@ __global__ void k_cg_update2(int V, int it, CGBufs B, const float *__restrict__ 
 }
 
 // after the solve: y_n = y_{n+1} + u_n ; dphi/df_frame += dt^2 y_n (R8)
-__global__ void k_adjoint_accum(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
-                                float4 *__restrict__ y, float *__restrict__ gforce, float dt) {
+__global__ void k_adjoint_accum(int V, const float *__restrict__ wv, const float3 *__restrict__ u,
+                                float3 *__restrict__ y, float *__restrict__ gforce, float dt) {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
     if (!(wv[v] > 0.f)) return;
-    float4 uv = u[v], yv = y[v];
+    float3 uv = u[v], yv = y[v];
     yv.x += uv.x; yv.y += uv.y; yv.z += uv.z;
     y[v] = yv;
     if (gforce) {
@@ -1144,8 +1127,8 @@ __global__ void k_adjoint_accum(int V, const float *__restrict__ wv, const float
 }
 
 // dphi/dx_0 = xbar_0 = M u_0 + dphi/dx_0(direct) ; dphi/dv_0 = vbar_0 = dt M y_0   (Eq. rawAdjoint)
-__global__ void k_adjoint_final(int V, const float *__restrict__ wv, const float4 *__restrict__ u,
-                                const float4 *__restrict__ y, const double4 *__restrict__ x0,
+__global__ void k_adjoint_final(int V, const float *__restrict__ wv, const float3 *__restrict__ u,
+                                const float3 *__restrict__ y, const double4 *__restrict__ x0,
                                 const float *__restrict__ target, const float *__restrict__ weights, float dt,
                                 float *__restrict__ gx0, float *__restrict__ gv0) {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1184,7 +1167,7 @@ __global__ void k_loss(int V, const double4 *__restrict__ x, const float *__rest
 
 // dphi/dalpha_j += e_j . (y_a - y_b)   (Eq. gradientRule; e_j is the a-part of M dDx/dalpha_j)
 __global__ void k_grad_compliance(int E, const int2 *__restrict__ idx, const float *__restrict__ e,
-                                  const float4 *__restrict__ y, float *__restrict__ g) {
+                                  const float3 *__restrict__ y, float *__restrict__ g) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= E) return;
     int2 id = idx[j];
@@ -1193,7 +1176,7 @@ __global__ void k_grad_compliance(int E, const int2 *__restrict__ idx, const flo
 }
 
 // collider parameter gradients: acc[c*4 + u] += Sum_v e_{c,v,u} . y_v
-__global__ void k_grad_colliders(int V, int NC, const float *__restrict__ e, const float4 *__restrict__ y,
+__global__ void k_grad_colliders(int V, int NC, const float *__restrict__ e, const float3 *__restrict__ y,
                                  double *acc) {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t NV = (size_t)NC * V;

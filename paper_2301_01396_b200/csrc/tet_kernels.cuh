@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     float acc[1] = {0.f};
     if (j < D.T) {
-        const float4 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
+        const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
         const int4 id = D.idx[j];
         const int vid[4] = {id.x, id.y, id.z, id.w};
         float3 pv[4];
@@ -456,16 +456,16 @@ __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float
         for (int v = 0; v < 4; ++v) {
             if (!(wv[vid[v]] > 0.f)) continue;
             float3 g = c[v][0] * f3at(q, 0) + c[v][1] * f3at(q, 1) + c[v][2] * f3at(q, 2);
-            red_add_f4(B.q + vid[v], make_float4(g.x, g.y, g.z, 0.f));
+            red_add_f3(B.q + vid[v], g);
         }
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
 // Tet part of the increment rhs: b -= G^T Qt~ G y, r0 -= G^T Qt~ G (y + u0), u0 = warm start
-__global__ void __launch_bounds__(kBlock) k_rhs_tet(TetDev D, const float *__restrict__ Qt, const float4 *__restrict__ y,
-                                                    const float4 *__restrict__ u, float4 *__restrict__ b,
-                                                    float4 *__restrict__ r0, const float *__restrict__ wv) {
+__global__ void __launch_bounds__(kBlock) k_rhs_tet(TetDev D, const float *__restrict__ Qt, const float3 *__restrict__ y,
+                                                    const float3 *__restrict__ u, float3 *__restrict__ b,
+                                                    float3 *__restrict__ r0, const float *__restrict__ wv) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= D.T) return;
     const int4 id = D.idx[j];
@@ -488,13 +488,13 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tet(TetDev D, const float *__res
         if (!(wv[vid[v]] > 0.f)) continue;
         float3 gy = c[v][0] * f3at(qy, 0) + c[v][1] * f3at(qy, 1) + c[v][2] * f3at(qy, 2);
         float3 gz = c[v][0] * f3at(qz, 0) + c[v][1] * f3at(qz, 1) + c[v][2] * f3at(qz, 2);
-        red_add_f4(b + vid[v], make_float4(-gy.x, -gy.y, -gy.z, 0.f));
-        red_add_f4(r0 + vid[v], make_float4(-gz.x, -gz.y, -gz.z, 0.f));
+        red_add_f3(b + vid[v], make_float3(-gy.x, -gy.y, -gy.z));
+        red_add_f3(r0 + vid[v], make_float3(-gz.x, -gz.y, -gz.z));
     }
 }
 
 // dphi/d(a,b)_t += e~_u . vec F(y)   (Eq. gradientRule)
-__global__ void k_grad_tet(TetDev D, const float *__restrict__ e, const float4 *__restrict__ y, float *__restrict__ g) {
+__global__ void k_grad_tet(TetDev D, const float *__restrict__ e, const float3 *__restrict__ y, float *__restrict__ g) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= D.T) return;
     const int4 id = D.idx[j];
