@@ -8,6 +8,7 @@
 #include <cmath>
 #include <stdexcept>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -279,7 +280,9 @@ struct dxpbd_scene {
     DBuf<int> d_fseg, d_fidx;             // foreign (b-endpoint) constraint lists per (color, tile)
     DBuf<int4> d_fent;                    // foreign entries {j, a, b, 0}
     // CG-local tile structure (TMA-staged matvec, QF = 1)
-    bool use_tma = false;
+    bool use_tma = false, use_pers = false;
+    int pers_grid = 0;
+    size_t pers_smem = 0;
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hoff, d_hlist, d_fpos;
@@ -509,7 +512,9 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         for (; it < end; ++it) {
-            if (s->use_tma)
+            if (s->use_pers)
+                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_pers<<<s->pers_grid, kPersThreads, s->pers_smem, st>>>(it, tt, V, s->hcap, Qc, bufs, xw, cs));
+            else if (s->use_tma)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(it, tt, V, s->hcap, Qc, bufs, xw, cs));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
@@ -762,6 +767,20 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 s->d_fQ.alloc((size_t)std::max<int64_t>(fc[nkeys], 1));
                 s->tma_smem = tma_smem_bytes(s->hcap);
                 s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap);
+                // persistent warp-specialized matvec: grid = SMs x resident CTAs
+                s->pers_smem = pers_smem_bytes(s->hcap);
+                // opt-in (DXPBD_MATVEC=pers): measured slower than the per-tile TMA kernel
+                const char *envp = getenv("DXPBD_MATVEC");
+                if (envp && std::string(envp) == "pers" && s->pers_smem <= 113 * 1024) {
+                    DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pers, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pers_smem));
+                    int per_sm = 0, nsm = 0;
+                    DX_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_matvec_pers, kPersThreads, s->pers_smem));
+                    DX_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device));
+                    if (per_sm > 0) {
+                        s->use_pers = true;
+                        s->pers_grid = std::min(nt, per_sm * nsm);
+                    }
+                }
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
                 DX_CHECK_CUDA(cudaStreamSynchronize(st));
