@@ -525,7 +525,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
                 LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), s->t_Q.p, bufs, xw, cs));
                 ++launches;
             }
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update2<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, cs));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
             ++launches;
         }
         // convergence check: rr of the last completed iteration against |b|^2

@@ -1313,6 +1313,63 @@ __global__ void k_cg_update2(int V, int it, CGBufs B, const float *__restrict__ 
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
 }
 
+// Vectorized PCG update: 4 vertices per thread read as 3 float4 per field of the packed float3
+// arrays (16-byte accesses); same arithmetic as k_cg_update2.  Vertices [4*nq, V) by k_cg_update2.
+__global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ wv, CGState s) {
+    if (cg_done(s, it + 1)) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nq = V / 4;
+    float acc[2] = {0.f, 0.f};
+    if (t < nq) {
+        const float4 *__restrict__ p = reinterpret_cast<const float4 *>((it & 1) ? B.p1 : B.p0);
+        float4 *__restrict__ u = reinterpret_cast<float4 *>(B.u);
+        float4 *__restrict__ r = reinterpret_cast<float4 *>(B.r);
+        const float4 *__restrict__ q = reinterpret_cast<const float4 *>(B.q);
+        const double pq = s.sc[(it + 1) * 4 + 0];
+        const float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
+        const float4 w4 = reinterpret_cast<const float4 *>(wv)[t];
+        const float w[4] = {w4.x, w4.y, w4.z, w4.w};
+        float uu[12], rr[12], pp[12], qq[12];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float4 a = u[3 * t + c], b = r[3 * t + c], cc = p[3 * t + c], d = q[3 * t + c];
+            uu[4 * c] = a.x; uu[4 * c + 1] = a.y; uu[4 * c + 2] = a.z; uu[4 * c + 3] = a.w;
+            rr[4 * c] = b.x; rr[4 * c + 1] = b.y; rr[4 * c + 2] = b.z; rr[4 * c + 3] = b.w;
+            pp[4 * c] = cc.x; pp[4 * c + 1] = cc.y; pp[4 * c + 2] = cc.z; pp[4 * c + 3] = cc.w;
+            qq[4 * c] = d.x; qq[4 * c + 1] = d.y; qq[4 * c + 2] = d.z; qq[4 * c + 3] = d.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            uu[k] += alpha * pp[k];
+            rr[k] = (w[k / 3] > 0.f) ? rr[k] - alpha * qq[k] : 0.f;
+            const float r2 = rr[k] * rr[k];
+            acc[0] += w[k / 3] * r2;
+            acc[1] += r2;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            u[3 * t + c] = make_float4(uu[4 * c], uu[4 * c + 1], uu[4 * c + 2], uu[4 * c + 3]);
+            r[3 * t + c] = make_float4(rr[4 * c], rr[4 * c + 1], rr[4 * c + 2], rr[4 * c + 3]);
+        }
+    } else if (t == nq) {   // tail vertices
+        for (int v = 4 * nq; v < V; ++v) {
+            const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
+            const double pq = s.sc[(it + 1) * 4 + 0];
+            const float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
+            const float w = wv[v];
+            float3 uv = B.u[v], rv = B.r[v], pv = p[v], qv = B.q[v];
+            uv = uv + alpha * pv;
+            rv = w > 0.f ? rv - alpha * qv : make_float3(0.f, 0.f, 0.f);
+            B.u[v] = uv;
+            B.r[v] = rv;
+            const float r2 = dot3(rv, rv);
+            acc[0] += w * r2;
+            acc[1] += r2;
+        }
+    }
+    block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
+}
+
 // after the solve: y_n = y_{n+1} + u_n ; dphi/df_frame += dt^2 y_n (R8)
 __global__ void k_adjoint_accum(int V, const float *__restrict__ wv, const float3 *__restrict__ u,
                                 float3 *__restrict__ y, float *__restrict__ gforce, float dt) {
