@@ -11,6 +11,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/dxpbd.h"
@@ -100,6 +102,159 @@ void color_sort(const std::vector<int32_t> &col, int nc, std::vector<int32_t> &p
 
 // Morton (Z-order) permutation of the rest positions: internal vertex i = user vertex perm[i]
 // (tiles of kTileV consecutive internal vertices are spatially compact).
+// Reorder idx[0, n) into warp groups (32 consecutive entries) with pairwise distinct shared-memory
+// banks for both endpoints: the (bank_a, bank_b) pairs form a bipartite multigraph on 32 + 32
+// banks; a proper edge coloring (Konig: max-degree colors, alternating-path recoloring) splits it
+// into matchings = conflict-free groups.  Classes are emitted largest first, each in the incoming
+// order; only groups straddling two classes can conflict.  Create-time host work.
+template <class F>
+static void bank_group(int32_t *idx, int n, F banks) {
+    if (n <= 1) return;
+    std::vector<std::pair<int, int>> ed(n);
+    int dl[32] = {0}, dr[32] = {0};
+    for (int k = 0; k < n; ++k) {
+        ed[k] = banks(idx[k]);
+        dl[ed[k].first]++;
+        dr[ed[k].second]++;
+    }
+    int D = 0;
+    for (int b = 0; b < 32; ++b) D = std::max(D, std::max(dl[b], dr[b]));
+    std::vector<int> L(32 * D, -1), R(32 * D, -1), col(n, -1), path;
+    for (int k = 0; k < n; ++k) {
+        const int u = ed[k].first, v = ed[k].second;
+        int a = 0, b = 0;
+        while (L[u * D + a] >= 0) ++a;
+        while (R[v * D + b] >= 0) ++b;
+        if (L[u * D + b] < 0) {
+            a = b;
+        } else if (R[v * D + a] >= 0) {
+            // swap colors a <-> b along the alternating path that starts at v with color a
+            path.clear();
+            bool right = true;
+            int node = v, c = a;
+            for (;;) {
+                const int e = right ? R[node * D + c] : L[node * D + c];
+                if (e < 0) break;
+                path.push_back(e);
+                node = right ? ed[e].first : ed[e].second;
+                right = !right;
+                c = c == a ? b : a;
+            }
+            for (int e : path) { L[ed[e].first * D + col[e]] = -1; R[ed[e].second * D + col[e]] = -1; }
+            for (int e : path) {
+                col[e] = col[e] == a ? b : a;
+                L[ed[e].first * D + col[e]] = e;
+                R[ed[e].second * D + col[e]] = e;
+            }
+        }
+        col[k] = a;
+        L[u * D + a] = k;
+        R[v * D + a] = k;
+    }
+    std::vector<int> csize(D, 0), corder(D);
+    for (int k = 0; k < n; ++k) csize[col[k]]++;
+    for (int c = 0; c < D; ++c) corder[c] = c;
+    std::stable_sort(corder.begin(), corder.end(), [&](int x, int y) { return csize[x] > csize[y]; });
+    std::vector<int32_t> out;
+    out.reserve(n);
+    for (int c : corder)
+        for (int k = 0; k < n; ++k)
+            if (col[k] == c) out.push_back(idx[k]);
+    std::copy(out.begin(), out.end(), idx);
+}
+
+// TMA-kernel layout of one tile (create time, host).  Local indices: own vertex v -> v - t*kTileV,
+// halo vertex -> kTileV + its rank in the tile's sorted halo list.  Each local index gets a
+// shared-memory slot (own: [0, kTileV), halo: [kTileV, kTileV + hcap)) whose bank (slot & 31) is
+// chosen greedily so that, for every (color, side) of the tile's constraint segments, the
+// endpoints spread evenly over the 32 banks (a linear layout folds a color's lower endpoints onto
+// half the banks: Morton index parities).  Each segment is then ordered into conflict-free warp
+// groups (bank_group).  Outputs: vslot / hslot (slots), tpos (sorted position -> layout position),
+// cpair (slot pairs in layout order), the permuted foreign segments with fpair / fposv.
+struct TileLayoutScratch {
+    std::vector<int> deg, moff, memb, cnt, order, slot_of, used;
+    std::vector<int32_t> ids;
+};
+
+static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<int> &halo_t, int hoff_t,
+                            const int64_t *cnt, const int64_t *fc, const int2 *ab, int *fidx, uint16_t *vslot,
+                            uint16_t *hslot, int *tpos, uint32_t *cpair, uint32_t *fpair, int *fposv,
+                            TileLayoutScratch &w) {
+    const int nh = (int)halo_t.size(), NL = kTileV + nh, NK = 4 * nc;
+    auto local = [&](int v) {
+        return v / kTileV == t ? v - t * kTileV
+                               : kTileV + (int)(std::lower_bound(halo_t.begin(), halo_t.end(), v) - halo_t.begin());
+    };
+    // memberships (CSR): key 4c+0 / 4c+1 = lower / upper endpoint of the color-c segment,
+    // 4c+2 / 4c+3 = halo / own endpoint of the color-c foreign segment
+    w.deg.assign(NL + 1, 0);
+    auto each = [&](auto &&f) {
+        for (int c = 0; c < nc; ++c) {
+            const size_t kk = (size_t)c * nt + t;
+            for (int64_t q = cnt[kk]; q < cnt[kk + 1]; ++q) { f(local(ab[q].x), 4 * c); f(local(ab[q].y), 4 * c + 1); }
+            for (int64_t k2 = fc[kk]; k2 < fc[kk + 1]; ++k2) {
+                const int q = fidx[k2];
+                f(local(ab[q].x), 4 * c + 2);
+                f(local(ab[q].y), 4 * c + 3);
+            }
+        }
+    };
+    each([&](int l, int) { w.deg[l + 1]++; });
+    w.moff.assign(NL + 1, 0);
+    for (int l = 0; l < NL; ++l) w.moff[l + 1] = w.moff[l] + w.deg[l + 1];
+    w.memb.resize(w.moff[NL]);
+    for (int l = 0; l < NL; ++l) w.deg[l] = w.moff[l];
+    each([&](int l, int k) { w.memb[w.deg[l]++] = k; });
+    // greedy bank assignment, most-constrained first, per region (own, halo)
+    w.cnt.assign((size_t)NK * 32, 0);
+    w.slot_of.assign(NL, 0);
+    for (int region = 0; region < 2; ++region) {
+        const int lo = region ? kTileV : 0, hi = region ? NL : kTileV, cap = region ? hcap / 32 : kTileV / 32;
+        const int base = region ? kTileV : 0;
+        w.order.resize(hi - lo);
+        for (int l = lo; l < hi; ++l) w.order[l - lo] = l;
+        std::stable_sort(w.order.begin(), w.order.end(),
+                         [&](int x, int y) { return w.moff[x + 1] - w.moff[x] > w.moff[y + 1] - w.moff[y]; });
+        w.used.assign(32, 0);
+        for (int l : w.order) {
+            int best = -1;
+            long bc = 0;
+            for (int b = 0; b < 32; ++b) {
+                if (w.used[b] >= cap) continue;
+                long c = 0;
+                for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) c += w.cnt[(size_t)w.memb[m] * 32 + b];
+                c = c * 1024 + w.used[b];
+                if (best < 0 || c < bc) { best = b; bc = c; }
+            }
+            w.slot_of[l] = base + 32 * w.used[best] + best;
+            w.used[best]++;
+            for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) w.cnt[(size_t)w.memb[m] * 32 + best]++;
+        }
+    }
+    for (int l = 0; l < kTileV; ++l) vslot[(size_t)t * kTileV + l] = (uint16_t)w.slot_of[l];
+    for (int h = 0; h < nh; ++h) hslot[hoff_t + h] = (uint16_t)w.slot_of[kTileV + h];
+    auto sl = [&](int v) { return w.slot_of[local(v)]; };
+    for (int c = 0; c < nc; ++c) {
+        const size_t kk = (size_t)c * nt + t;
+        const int64_t b = cnt[kk], e = cnt[kk + 1];
+        w.ids.resize(e - b);
+        for (int64_t q = b; q < e; ++q) w.ids[q - b] = (int32_t)q;
+        bank_group(w.ids.data(), (int)(e - b), [&](int32_t q) { return std::make_pair(sl(ab[q].x) & 31, sl(ab[q].y) & 31); });
+        for (int64_t i = 0; i < e - b; ++i) {
+            const int q = w.ids[i];
+            tpos[q] = (int)(b + i);
+            cpair[b + i] = (uint32_t)sl(ab[q].x) | ((uint32_t)sl(ab[q].y) << 16);
+        }
+        const int64_t fb = fc[kk], fe = fc[kk + 1];
+        bank_group(fidx + fb, (int)(fe - fb), [&](int32_t q) { return std::make_pair(sl(ab[q].x) & 31, sl(ab[q].y) & 31); });
+        for (int64_t k2 = fb; k2 < fe; ++k2) {
+            const int q = fidx[k2];
+            fposv[q] = (int)k2;
+            fpair[k2] = (uint32_t)sl(ab[q].x) | ((uint32_t)sl(ab[q].y) << 16);
+        }
+    }
+}
+
 static inline uint64_t spread3(uint64_t x) {
     x &= 0x1fffff;
     x = (x | x << 32) & 0x1f00000000ffffull;
@@ -280,13 +435,13 @@ struct dxpbd_scene {
     DBuf<int> d_fseg, d_fidx;             // foreign (b-endpoint) constraint lists per (color, tile)
     DBuf<int4> d_fent;                    // foreign entries {j, a, b, 0}
     // CG-local tile structure (TMA-staged matvec, QF = 1)
-    bool use_tma = false, use_pers = false;
-    int pers_grid = 0;
-    size_t pers_smem = 0;
+    bool use_tma = false;
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hoff, d_hlist, d_fpos;
     DBuf<uint32_t> d_cpair, d_fpair;
+    DBuf<uint16_t> d_vslot, d_hslot;   // tile-local shared-memory slots (own vertices, halo entries)
+    DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
     DBuf<float4> d_fQ;
     // tets (color-sorted, internal vertex ids)
     DBuf<int4> t_idx;
@@ -451,7 +606,8 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             float *eo = want_e ? s->ed.p : nullptr;
             if (first && last && s->qf == 1)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true, 1><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x,
-                                                                                                   s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p));
+                                                                                                   s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p,
+                                                                                                   s->use_tma ? s->d_tpos.p : nullptr));
             else if (first && last)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else if (first)
@@ -504,7 +660,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     CGBufs bufs{s->ax.p, s->r.p, s->p.p, s->p1.p, s->q.p, nullptr};
     TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
     TmaTiles tt{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_hoff.p, s->d_cpair.p, s->d_fpair.p,
-                s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p};
+                s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p, s->d_vslot.p, s->d_hslot.p};
     int it = 0;
     const int chunk = 8;
     iters_out = -1;
@@ -512,9 +668,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         for (; it < end; ++it) {
-            if (s->use_pers)
-                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_pers<<<s->pers_grid, kPersThreads, s->pers_smem, st>>>(it, tt, V, s->hcap, Qc, bufs, xw, cs));
-            else if (s->use_tma)
+            if (s->use_tma)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(it, tt, V, s->hcap, Qc, bufs, xw, cs));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
@@ -684,6 +838,16 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         for (size_t kk = 0; kk < nkeys; ++kk)
             std::sort(s->dist_perm_h.begin() + cnt[kk], s->dist_perm_h.begin() + cnt[kk + 1],
                       [&](int32_t x, int32_t y) { return ab[x].x < ab[y].x; });
+        // halo sets per tile (order-independent): the other endpoints of cross-tile constraints
+        std::vector<std::vector<int>> halo(nt);
+        for (int j = 0; j < E; ++j) {
+            int a = ab[j].x, bb = ab[j].y, ta = a / kTileV, tb = bb / kTileV;
+            if (ta != tb) { halo[ta].push_back(bb); halo[tb].push_back(a); }
+        }
+        for (int t = 0; t < nt; ++t) {
+            std::sort(halo[t].begin(), halo[t].end());
+            halo[t].erase(std::unique(halo[t].begin(), halo[t].end()), halo[t].end());
+        }
         for (int q = 0; q < E; ++q) ab_sorted[q] = ab[s->dist_perm_h[q]];
         s->d_seg.alloc(seg.size());
         upload(s->d_seg.p, seg.data(), sizeof(int) * seg.size(), DXPBD_MEM_HOST, st);
@@ -709,6 +873,60 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                           [&](int x, int y) { return ab_sorted[x].y < ab_sorted[y].y; });
             s->d_fseg.alloc(fseg.size());
             upload(s->d_fseg.p, fseg.data(), sizeof(int) * fseg.size(), DXPBD_MEM_HOST, st);
+            s->n_foreign = fc[nkeys];
+            // CG-local tile structure for the TMA-staged kernels (kernels.cuh "TMA-staged")
+            std::vector<int> hoff(nt + 1, 0);
+            int hmax = 0;
+            for (int t = 0; t < nt; ++t) {
+                hoff[t + 1] = hoff[t] + (int)halo[t].size();
+                hmax = std::max(hmax, (int)halo[t].size());
+            }
+            s->hcap = (hmax + 31) / 32 * 32;
+            s->halo_total = hoff[nt];
+            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors;
+            if (s->use_tma) {
+                std::vector<int> hlist(std::max(hoff[nt], 1));
+                for (int t = 0; t < nt; ++t) std::copy(halo[t].begin(), halo[t].end(), hlist.begin() + hoff[t]);
+                const int64_t NF = fc[nkeys];
+                std::vector<uint32_t> cpair(E + 4, 0), fpair((size_t)std::max<int64_t>(NF, 1) + 4, 0);
+                std::vector<int> fposv(E, -1), tpos(E);
+                std::vector<uint16_t> vslot((size_t)nt * kTileV), hslot(std::max(hoff[nt], 1));
+                // per tile (independent, threaded): bank-balanced shared-memory slots, then
+                // conflict-free warp groups of every (color, tile) segment (tma_tile_layout)
+                auto work = [&](int t0, int t1) {
+                    TileLayoutScratch ws;
+                    for (int t = t0; t < t1; ++t)
+                        tma_tile_layout(t, nc, nt, s->hcap, halo[t], hoff[t], cnt.data(), fc.data(), ab_sorted.data(),
+                                        fidx.data(), vslot.data(), hslot.data(), tpos.data(), cpair.data(), fpair.data(),
+                                        fposv.data(), ws);
+                };
+                const int nth = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+                std::vector<std::thread> pool;
+                for (int k = 0; k < nth; ++k) pool.emplace_back(work, (int)((int64_t)nt * k / nth), (int)((int64_t)nt * (k + 1) / nth));
+                for (auto &th : pool) th.join();
+                s->d_hoff.alloc(hoff.size());
+                upload(s->d_hoff.p, hoff.data(), sizeof(int) * hoff.size(), DXPBD_MEM_HOST, st);
+                s->d_hlist.alloc(hlist.size());
+                upload(s->d_hlist.p, hlist.data(), sizeof(int) * hlist.size(), DXPBD_MEM_HOST, st);
+                s->d_vslot.alloc(vslot.size());
+                upload(s->d_vslot.p, vslot.data(), sizeof(uint16_t) * vslot.size(), DXPBD_MEM_HOST, st);
+                s->d_hslot.alloc(hslot.size());
+                upload(s->d_hslot.p, hslot.data(), sizeof(uint16_t) * hslot.size(), DXPBD_MEM_HOST, st);
+                s->d_cpair.alloc(cpair.size());
+                upload(s->d_cpair.p, cpair.data(), sizeof(uint32_t) * cpair.size(), DXPBD_MEM_HOST, st);
+                s->d_fpair.alloc(fpair.size());
+                upload(s->d_fpair.p, fpair.data(), sizeof(uint32_t) * fpair.size(), DXPBD_MEM_HOST, st);
+                s->d_fpos.alloc(E);
+                upload(s->d_fpos.p, fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
+                s->d_tpos.alloc(E);
+                upload(s->d_tpos.p, tpos.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
+                s->d_fQ.alloc((size_t)std::max<int64_t>(NF, 1));
+                s->tma_smem = tma_smem_bytes(s->hcap);
+                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap);
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
+                DX_CHECK_CUDA(cudaStreamSynchronize(st));
+            }
             s->d_fidx.alloc(fidx.size());
             upload(s->d_fidx.p, fidx.data(), sizeof(int) * fidx.size(), DXPBD_MEM_HOST, st);
             std::vector<int4> fent(fidx.size());
@@ -716,75 +934,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 fent[q] = make_int4(fidx[q], ab_sorted[fidx[q]].x, ab_sorted[fidx[q]].y, 0);
             s->d_fent.alloc(fent.size());
             upload(s->d_fent.p, fent.data(), sizeof(int4) * fent.size(), DXPBD_MEM_HOST, st);
-            s->n_foreign = fc[nkeys];
-            // CG-local tile structure for the TMA-staged kernels (kernels.cuh "TMA-staged")
-            std::vector<std::vector<int>> halo(nt);
-            for (int q = 0; q < E; ++q) {
-                int a = ab_sorted[q].x, bb = ab_sorted[q].y, ta = a / kTileV, tb = bb / kTileV;
-                if (ta != tb) { halo[ta].push_back(bb); halo[tb].push_back(a); }
-            }
-            std::vector<int> hoff(nt + 1, 0);
-            int hmax = 0;
-            for (int t = 0; t < nt; ++t) {
-                std::sort(halo[t].begin(), halo[t].end());
-                halo[t].erase(std::unique(halo[t].begin(), halo[t].end()), halo[t].end());
-                hoff[t + 1] = hoff[t] + (int)halo[t].size();
-                hmax = std::max(hmax, (int)halo[t].size());
-            }
-            auto slot = [&](int t, int v) {
-                return (int)(std::lower_bound(halo[t].begin(), halo[t].end(), v) - halo[t].begin());
-            };
-            s->hcap = (hmax + 31) / 32 * 32;
-            s->halo_total = hoff[nt];
-            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors;
-            if (s->use_tma) {
-                std::vector<int> hlist(std::max(hoff[nt], 1));
-                for (int t = 0; t < nt; ++t) std::copy(halo[t].begin(), halo[t].end(), hlist.begin() + hoff[t]);
-                std::vector<uint32_t> cpair(E + 4, 0), fpair((size_t)std::max<int64_t>(fc[nkeys], 1) + 4, 0);
-                std::vector<int> fposv(E, -1);
-                for (int q = 0; q < E; ++q) {
-                    int a = ab_sorted[q].x, bb = ab_sorted[q].y, ta = a / kTileV, tb = bb / kTileV;
-                    uint32_t la = (uint32_t)(a - ta * kTileV);
-                    uint32_t lb = ta == tb ? (uint32_t)(bb - ta * kTileV) : (uint32_t)(kTileV + slot(ta, bb));
-                    cpair[q] = la | (lb << 16);
-                }
-                for (int64_t k2 = 0; k2 < fc[nkeys]; ++k2) {
-                    int q = fidx[k2];
-                    int a = ab_sorted[q].x, bb = ab_sorted[q].y, tb = bb / kTileV;
-                    fpair[k2] = (uint32_t)(kTileV + slot(tb, a)) | ((uint32_t)(bb - tb * kTileV) << 16);
-                    fposv[q] = (int)k2;
-                }
-                s->d_hoff.alloc(hoff.size());
-                upload(s->d_hoff.p, hoff.data(), sizeof(int) * hoff.size(), DXPBD_MEM_HOST, st);
-                s->d_hlist.alloc(hlist.size());
-                upload(s->d_hlist.p, hlist.data(), sizeof(int) * hlist.size(), DXPBD_MEM_HOST, st);
-                s->d_cpair.alloc(cpair.size());
-                upload(s->d_cpair.p, cpair.data(), sizeof(uint32_t) * cpair.size(), DXPBD_MEM_HOST, st);
-                s->d_fpair.alloc(fpair.size());
-                upload(s->d_fpair.p, fpair.data(), sizeof(uint32_t) * fpair.size(), DXPBD_MEM_HOST, st);
-                s->d_fpos.alloc(E);
-                upload(s->d_fpos.p, fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
-                s->d_fQ.alloc((size_t)std::max<int64_t>(fc[nkeys], 1));
-                s->tma_smem = tma_smem_bytes(s->hcap);
-                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap);
-                // persistent warp-specialized matvec: grid = SMs x resident CTAs
-                s->pers_smem = pers_smem_bytes(s->hcap);
-                // opt-in (DXPBD_MATVEC=pers): measured slower than the per-tile TMA kernel
-                const char *envp = getenv("DXPBD_MATVEC");
-                if (envp && std::string(envp) == "pers" && s->pers_smem <= 113 * 1024) {
-                    DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pers, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pers_smem));
-                    int per_sm = 0, nsm = 0;
-                    DX_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_matvec_pers, kPersThreads, s->pers_smem));
-                    DX_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device));
-                    if (per_sm > 0) {
-                        s->use_pers = true;
-                        s->pers_grid = std::min(nt, per_sm * nsm);
-                    }
-                }
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
-                DX_CHECK_CUDA(cudaStreamSynchronize(st));
-            }
+            DX_CHECK_CUDA(cudaStreamSynchronize(st));
         }
         DBuf<float> alpha_u;
         alpha_u.alloc(E);
@@ -1032,7 +1182,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         {
             TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
             TmaTiles tt{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_hoff.p, s->d_cpair.p, s->d_fpair.p,
-                        s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p};
+                        s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p, s->d_vslot.p, s->d_hslot.p};
             if (s->use_tma)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_rhs_smem, st>>>(
                     tt, V, s->hcap, Qc, s->ax.p, s->uprev.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,

@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, in
                                                         DistScratch sc, int pd, float *__restrict__ Qout,
                                                         float *__restrict__ eout, double4 *__restrict__ x,
                                                         const int *__restrict__ fpos = nullptr,
-                                                        float4 *__restrict__ fQ = nullptr) {
+                                                        float4 *__restrict__ fQ = nullptr,
+                                                        const int *__restrict__ tpos = nullptr) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= count) return;
     int j = begin + t;
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, in
     if (LAST && QF == 1) {
         // K = 1, PD projection on (host guarantees): closed form, no eigen-solve
         float4 q4 = ok ? qpack_iso_rank1(o.n, o.dl, (float)(1.0 / o.len), o.J) : make_float4(0.f, 0.f, 0.f, 0.f);
-        reinterpret_cast<float4 *>(Qout)[j] = q4;
+        reinterpret_cast<float4 *>(Qout)[tpos ? tpos[j] : j] = q4;   // TMA layout position
         if (fpos) {
             const int fp = fpos[j];
             if (fp >= 0) fQ[fp] = q4;   // copy for the tile of b (TMA-staged foreign list)
@@ -612,6 +613,7 @@ struct TmaTiles {
     const uint32_t *cpair, *fpair;
     const int *hlist;
     const float4 *Q4, *fQ;
+    const uint16_t *vslot, *hslot;   // shared-memory slot of own vertex (t, i) / of halo entry (host: tma_tile_layout)
 };
 
 struct TmaStage {
@@ -626,6 +628,7 @@ __host__ __device__ inline size_t tma_smem_bytes(int hcap) {
 }
 
 constexpr int kMaxColors = 64;   // bounds table in shared memory (more colors: generic kernel)
+
 
 DX_INLINE void tma_issue(uint64_t *bar, TmaStage &S, int c, const int *sb, const TmaTiles &T) {
     const int b = sb[4 * c], e = sb[4 * c + 1];
@@ -795,12 +798,13 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
             }
             if (it > 0) pnew[v] = pv;
         }
-        sp[i] = pv.x;
-        sp[spn + i] = pv.y;
-        sp[2 * spn + i] = pv.z;
-        sq[i] = qv.x;
-        sq[kTileV + i] = qv.y;
-        sq[2 * kTileV + i] = qv.z;
+        const int si = T.vslot[(size_t)t * kTileV + i];
+        sp[si] = pv.x;
+        sp[spn + si] = pv.y;
+        sp[2 * spn + si] = pv.z;
+        sq[si] = qv.x;
+        sq[kTileV + si] = qv.y;
+        sq[2 * kTileV + si] = qv.z;
     }
 #pragma unroll
     for (int u = 0; u < NH; ++u) {
@@ -811,230 +815,29 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
                 pv = it > 0 ? make_float3(hw[u] * hr[u].x + beta * hp[u].x, hw[u] * hr[u].y + beta * hp[u].y,
                                           hw[u] * hr[u].z + beta * hp[u].z)
                             : f3(hr[u]);
-            sp[kTileV + h] = pv.x;
-            sp[spn + kTileV + h] = pv.y;
-            sp[2 * spn + kTileV + h] = pv.z;
+            const int sh = T.hslot[h0 + h];
+            sp[sh] = pv.x;
+            sp[spn + sh] = pv.y;
+            sp[2 * spn + sh] = pv.z;
         }
     }
     for (int h = threadIdx.x + NH * kTmaThreads; h < nh; h += blockDim.x) {   // rare: large halos
         const int v = T.hlist[h0 + h];
         const float3 pv = halo_p(it, v, beta, B.r, pold, pnew, wv);
-        sp[kTileV + h] = pv.x;
-        sp[spn + kTileV + h] = pv.y;
-        sp[2 * spn + kTileV + h] = pv.z;
+        const int sh = T.hslot[h0 + h];
+        sp[sh] = pv.x;
+        sp[spn + sh] = pv.y;
+        sp[2 * spn + sh] = pv.z;
     }
     __syncthreads();
     acc[0] += tma_tile_colors<1>(bars, stages, reinterpret_cast<float (*)[1]>(sp), spn, sq, sb, T);
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-        const int v = v0 + i;
-        B.q[v] = wv[v] > 0.f ? make_float3(sq[i], sq[kTileV + i], sq[2 * kTileV + i]) : make_float3(0.f, 0.f, 0.f);
+        const int v = v0 + i, si = T.vslot[(size_t)t * kTileV + i];
+        B.q[v] = wv[v] > 0.f ? make_float3(sq[si], sq[kTileV + si], sq[2 * kTileV + si]) : make_float3(0.f, 0.f, 0.f);
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// ---------------------------------------------------------------------------------------------
-// Persistent warp-specialized PCG matvec (QF = 1, same math as k_cg_matvec_tma).  Each CTA loops
-// over tiles t = blockIdx.x + k * gridDim.x with three roles:
-//   warps 0..7  (compute): per color, wait stage_full, accumulate the tile's distance blocks in
-//                shared memory, named barrier 1 (256 threads), release the stage; flush q per tile.
-//   warp  8     (producer, lane 0): streams the (tile, color) stages with bulk async copies into a
-//                kPersStages ring, continuously across tile boundaries (stage_empty -> stage_full).
-//   warps 9..10 (prefetch): vertex phase of the NEXT tile into the other of two tile slots
-//                (p update, q init with M p + Qc p, halo values, per-color bounds), overlapping the
-//                current tile's colors (slot_empty -> slot_full).
-// Synchronization is mbarrier-only between roles (parity = round & 1), bar.sync 1 inside compute.
-constexpr int kPersStages = 3;
-constexpr int kPersCompute = 256, kPersPrefetch = 64;
-constexpr int kPersThreads = kPersCompute + 32 + kPersPrefetch;
-
-__host__ __device__ inline size_t pers_slot_floats(int hcap) { return 3 * (size_t)(kTileV + hcap) + 3 * (size_t)kTileV; }
-__host__ __device__ inline size_t pers_smem_bytes(int hcap) {
-    return 256 + sizeof(int) * 2 * 4 * kMaxColors + sizeof(TmaStage) * kPersStages + sizeof(float) * 2 * pers_slot_floats(hcap);
-}
-
-DX_INLINE void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-DX_INLINE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__global__ void __launch_bounds__(kPersThreads, 3) k_cg_matvec_pers(int it, TmaTiles T, int V, int hcap,
-                                                                    const float *__restrict__ Qc, CGBufs B,
-                                                                    const float *__restrict__ wv, CGState s) {
-    if (cg_done(s, it + 1)) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t *stage_full = reinterpret_cast<uint64_t *>(smem_raw);
-    uint64_t *stage_empty = stage_full + kPersStages;
-    uint64_t *slot_full = stage_empty + kPersStages;
-    uint64_t *slot_empty = slot_full + 2;
-    int *sbs = reinterpret_cast<int *>(smem_raw + 256);                       // [2][4*kMaxColors]
-    TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 256 + sizeof(int) * 2 * 4 * kMaxColors);
-    float *slots = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(stages) + sizeof(TmaStage) * kPersStages);
-    const size_t slotf = pers_slot_floats(hcap);
-    const int spn = kTileV + hcap;
-    const int ncol = T.ncol, stride = T.ntiles + 1;
-    const int ntl = (T.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;   // my tiles
-    const int warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < kPersStages; ++k) { mbar_init(&stage_full[k], 1); mbar_init(&stage_empty[k], 1); }
-        for (int k = 0; k < 2; ++k) { mbar_init(&slot_full[k], kPersPrefetch); mbar_init(&slot_empty[k], 1); }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const float4 *__restrict__ Q4 = T.Q4;
-    const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
-    float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
-    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
-    float acc[1] = {0.f};
-    if (warp == 8) {
-        // ------------------------------------------------------------------ TMA producer
-        if ((threadIdx.x & 31) == 0) {
-            for (int k = 0; k < ntl; ++k) {
-                const int t = blockIdx.x + k * gridDim.x;
-                for (int c = 0; c < ncol; ++c) {
-                    const int phi = k * ncol + c, st = phi % kPersStages;
-                    mbar_wait(&stage_empty[st], (uint32_t)(((phi / kPersStages) & 1) ^ 1));
-                    int sb4[4] = {T.seg[c * stride + t], T.seg[c * stride + t + 1], T.fseg[c * stride + t],
-                                  T.fseg[c * stride + t + 1]};
-                    fence_proxy_async();
-                    tma_issue(&stage_full[st], stages[st], 0, sb4, T);
-                }
-            }
-        }
-    } else if (warp > 8) {
-        // ------------------------------------------------------------------ vertex-phase prefetch
-        const int lt = threadIdx.x - (kPersCompute + 32);
-        for (int k = 0; k < ntl; ++k) {
-            const int t = blockIdx.x + k * gridDim.x, slot = k & 1;
-            mbar_wait(&slot_empty[slot], (uint32_t)(((k >> 1) & 1) ^ 1));
-            float *sp = slots + slot * slotf;
-            float *sq = sp + 3 * spn;
-            int *sb = sbs + slot * 4 * kMaxColors;
-            for (int c = lt; c < ncol; c += kPersPrefetch) {
-                sb[4 * c] = T.seg[c * stride + t];
-                sb[4 * c + 1] = T.seg[c * stride + t + 1];
-                sb[4 * c + 2] = T.fseg[c * stride + t];
-                sb[4 * c + 3] = T.fseg[c * stride + t + 1];
-            }
-            const int v0 = t * kTileV, nv = min(kTileV, V - v0);
-            constexpr int NO = kTileV / kPersPrefetch;
-            float wo[NO];
-            float3 ro[NO], po[NO];
-#pragma unroll
-            for (int u = 0; u < NO; ++u) {
-                const int v = min(v0 + lt + u * kPersPrefetch, V - 1);
-                wo[u] = wv[v];
-                ro[u] = it > 0 ? B.r[v] : pnew[v];
-                po[u] = it > 0 ? pold[v] : make_float3(0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int u = 0; u < NO; ++u) {
-                const int i = lt + u * kPersPrefetch;
-                float3 pv = make_float3(0.f, 0.f, 0.f), qv = pv;
-                if (i < nv) {
-                    const int v = v0 + i;
-                    const float w = wo[u];
-                    if (w > 0.f) {
-                        pv = it > 0 ? make_float3(w * ro[u].x + beta * po[u].x, w * ro[u].y + beta * po[u].y,
-                                                  w * ro[u].z + beta * po[u].z)
-                                    : ro[u];
-                        qv = (1.f / w) * pv;
-                        if (Qc) {
-                            Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
-                                          Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
-                            qv = qv + sym3_mul(A, pv);
-                        }
-                        acc[0] += dot3(pv, qv);
-                    }
-                    if (it > 0) pnew[v] = pv;
-                }
-                sp[i] = pv.x;
-                sp[spn + i] = pv.y;
-                sp[2 * spn + i] = pv.z;
-                sq[i] = qv.x;
-                sq[kTileV + i] = qv.y;
-                sq[2 * kTileV + i] = qv.z;
-            }
-            const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
-            for (int h0l = 0; h0l < nh; h0l += 4 * kPersPrefetch) {
-                int hv[4];
-                float3 hp[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int h = h0l + lt + u * kPersPrefetch;
-                    hv[u] = h < nh ? T.hlist[h0 + h] : -1;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) hp[u] = hv[u] >= 0 ? halo_p(it, hv[u], beta, B.r, pold, pnew, wv) : make_float3(0.f, 0.f, 0.f);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int h = h0l + lt + u * kPersPrefetch;
-                    if (hv[u] >= 0) {
-                        sp[kTileV + h] = hp[u].x;
-                        sp[spn + kTileV + h] = hp[u].y;
-                        sp[2 * spn + kTileV + h] = hp[u].z;
-                    }
-                }
-            }
-            mbar_arrive(&slot_full[slot]);
-        }
-    } else {
-        // ------------------------------------------------------------------ compute warps
-        for (int k = 0; k < ntl; ++k) {
-            const int t = blockIdx.x + k * gridDim.x, slot = k & 1;
-            mbar_wait(&slot_full[slot], (uint32_t)((k >> 1) & 1));
-            float *sp0 = slots + slot * slotf;
-            float *sp1 = sp0 + spn, *sp2 = sp0 + 2 * spn;
-            float *sq0 = sp0 + 3 * spn, *sq1 = sq0 + kTileV, *sq2 = sq0 + 2 * kTileV;
-            const int *sb = sbs + slot * 4 * kMaxColors;
-            const int v0 = t * kTileV;
-            for (int c = 0; c < ncol; ++c) {
-                const int phi = k * ncol + c, st = phi % kPersStages;
-                TmaStage &S = stages[st];
-                mbar_wait(&stage_full[st], (uint32_t)((phi / kPersStages) & 1));
-                const int b = sb[4 * c], e = sb[4 * c + 1];
-                const int off = (int)((((size_t)b * 4) & 15) >> 2);
-                for (int i = threadIdx.x; i < e - b; i += kPersCompute) {
-                    const uint32_t pr = S.cp[off + i];
-                    const float4 q4 = S.q[i];
-                    const int la = pr & 0xffff, lb = pr >> 16;
-                    const float3 d = make_float3(sp0[la] - sp0[lb], sp1[la] - sp1[lb], sp2[la] - sp2[lb]);
-                    const float3 y = qmul_iso_rank1(q4, d);
-                    acc[0] += dot3(d, y);
-                    sq0[la] += y.x;
-                    sq1[la] += y.y;
-                    sq2[la] += y.z;
-                    if (lb < kTileV) {
-                        sq0[lb] -= y.x;
-                        sq1[lb] -= y.y;
-                        sq2[lb] -= y.z;
-                    }
-                }
-                const int fb = sb[4 * c + 2], fe = sb[4 * c + 3];
-                const int foff = (int)((((size_t)fb * 4) & 15) >> 2);
-                for (int i = threadIdx.x; i < fe - fb; i += kPersCompute) {
-                    const uint32_t pr = i < kFCap ? S.fp[foff + i] : T.fpair[fb + i];
-                    const float4 q4 = i < kFCap ? S.fq[i] : T.fQ[fb + i];
-                    const int la = pr & 0xffff, lb = pr >> 16;
-                    const float3 d = make_float3(sp0[la] - sp0[lb], sp1[la] - sp1[lb], sp2[la] - sp2[lb]);
-                    const float3 y = qmul_iso_rank1(q4, d);
-                    sq0[lb] -= y.x;
-                    sq1[lb] -= y.y;
-                    sq2[lb] -= y.z;
-                }
-                named_bar(1, kPersCompute);
-                if (threadIdx.x == 0) mbar_arrive(&stage_empty[st]);
-            }
-            const int nv = min(kTileV, V - v0);
-            for (int i = threadIdx.x; i < nv; i += kPersCompute) {
-                const int v = v0 + i;
-                B.q[v] = wv[v] > 0.f ? make_float3(sq0[i], sq1[i], sq2[i]) : make_float3(0.f, 0.f, 0.f);
-            }
-            named_bar(1, kPersCompute);
-            if (threadIdx.x == 0) mbar_arrive(&slot_empty[slot]);
-        }
-    }
-    block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
-}
 
 // Increment-system right-hand side with warm start (kernels "adjoint"): for own vertices, with
 // u = u_{n+1}, uprev = u_{n+2} and the extrapolated initial guess u0 = 2u - uprev,
@@ -1105,18 +908,20 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
                 }
             }
         }
-        sy[i] = yv.x; sy[spn + i] = yv.y; sy[2 * spn + i] = yv.z;
-        sz[i] = zv.x; sz[spn + i] = zv.y; sz[2 * spn + i] = zv.z;
-        sqb[i] = bb.x; sqb[kTileV + i] = bb.y; sqb[2 * kTileV + i] = bb.z;
-        sqr[i] = rr.x; sqr[kTileV + i] = rr.y; sqr[2 * kTileV + i] = rr.z;
+        const int si = T.vslot[(size_t)t * kTileV + i];
+        sy[si] = yv.x; sy[spn + si] = yv.y; sy[2 * spn + si] = yv.z;
+        sz[si] = zv.x; sz[spn + si] = zv.y; sz[2 * spn + si] = zv.z;
+        sqb[si] = bb.x; sqb[kTileV + si] = bb.y; sqb[2 * kTileV + si] = bb.z;
+        sqr[si] = rr.x; sqr[kTileV + si] = rr.y; sqr[2 * kTileV + si] = rr.z;
     }
     const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
     for (int h = threadIdx.x; h < nh; h += blockDim.x) {
         const int v = T.hlist[h0 + h];
         const float3 uh = f3(u[v]);
         const float3 yv = f3(y[v]), zv = yv + uh + (uh - f3(uprev[v]));
-        sy[kTileV + h] = yv.x; sy[spn + kTileV + h] = yv.y; sy[2 * spn + kTileV + h] = yv.z;
-        sz[kTileV + h] = zv.x; sz[spn + kTileV + h] = zv.y; sz[2 * spn + kTileV + h] = zv.z;
+        const int sh = T.hslot[h0 + h];
+        sy[sh] = yv.x; sy[spn + sh] = yv.y; sy[2 * spn + sh] = yv.z;
+        sz[sh] = zv.x; sz[spn + sh] = zv.y; sz[2 * spn + sh] = zv.z;
     }
     __syncthreads();
     for (int c = 0; c < T.ncol; ++c) {
@@ -1160,10 +965,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
         }
     }
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-        const int v = v0 + i;
+        const int v = v0 + i, si = T.vslot[(size_t)t * kTileV + i];
         const bool fr = wv[v] > 0.f;
-        bout[v] = fr ? make_float3(sqb[i], sqb[kTileV + i], sqb[2 * kTileV + i]) : make_float3(0.f, 0.f, 0.f);
-        r0out[v] = fr ? make_float3(sqr[i], sqr[kTileV + i], sqr[2 * kTileV + i]) : make_float3(0.f, 0.f, 0.f);
+        bout[v] = fr ? make_float3(sqb[si], sqb[kTileV + si], sqb[2 * kTileV + si]) : make_float3(0.f, 0.f, 0.f);
+        r0out[v] = fr ? make_float3(sqr[si], sqr[kTileV + si], sqr[2 * kTileV + si]) : make_float3(0.f, 0.f, 0.f);
     }
 }
 
