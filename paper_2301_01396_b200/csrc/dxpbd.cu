@@ -102,24 +102,25 @@ void color_sort(const std::vector<int32_t> &col, int nc, std::vector<int32_t> &p
 
 // Morton (Z-order) permutation of the rest positions: internal vertex i = user vertex perm[i]
 // (tiles of kTileV consecutive internal vertices are spatially compact).
-// Reorder idx[0, n) into warp groups (32 consecutive entries) with pairwise distinct shared-memory
-// banks for both endpoints: the (bank_a, bank_b) pairs form a bipartite multigraph on 32 + 32
-// banks; a proper edge coloring (Konig: max-degree colors, alternating-path recoloring) splits it
-// into matchings = conflict-free groups.  Classes are emitted largest first, each in the incoming
-// order; only groups straddling two classes can conflict.  Create-time host work.
+// Reorder idx[0, n) into groups of G consecutive entries (one shared-memory access phase) whose
+// endpoint bank keys (0..NB-1, NB <= 32) are pairwise distinct where the segment allows it: the
+// (bank_a, bank_b) pairs form a bipartite multigraph on NB + NB banks; a proper edge coloring
+// (Konig: max-degree colors, alternating-path recoloring) splits it into matchings; each group
+// starts from the largest remaining matching and is filled with non-conflicting entries of the
+// others (then with any entry, so that every group but the last is full).  Create-time host work.
 template <class F>
-static void bank_group(int32_t *idx, int n, F banks) {
+static void bank_group(int32_t *idx, int n, int NB, int G, F banks) {
     if (n <= 1) return;
     std::vector<std::pair<int, int>> ed(n);
-    int dl[32] = {0}, dr[32] = {0};
+    std::vector<int> dl(NB, 0), dr(NB, 0);
     for (int k = 0; k < n; ++k) {
         ed[k] = banks(idx[k]);
         dl[ed[k].first]++;
         dr[ed[k].second]++;
     }
     int D = 0;
-    for (int b = 0; b < 32; ++b) D = std::max(D, std::max(dl[b], dr[b]));
-    std::vector<int> L(32 * D, -1), R(32 * D, -1), col(n, -1), path;
+    for (int b = 0; b < NB; ++b) D = std::max(D, std::max(dl[b], dr[b]));
+    std::vector<int> L(NB * D, -1), R(NB * D, -1), col(n, -1), path;
     for (int k = 0; k < n; ++k) {
         const int u = ed[k].first, v = ed[k].second;
         int a = 0, b = 0;
@@ -151,25 +152,50 @@ static void bank_group(int32_t *idx, int n, F banks) {
         L[u * D + a] = k;
         R[v * D + a] = k;
     }
-    std::vector<int> csize(D, 0), corder(D);
-    for (int k = 0; k < n; ++k) csize[col[k]]++;
-    for (int c = 0; c < D; ++c) corder[c] = c;
-    std::stable_sort(corder.begin(), corder.end(), [&](int x, int y) { return csize[x] > csize[y]; });
+    std::vector<std::vector<int>> cls(D);
+    for (int k = 0; k < n; ++k) cls[col[k]].push_back(k);
     std::vector<int32_t> out;
     out.reserve(n);
-    for (int c : corder)
-        for (int k = 0; k < n; ++k)
-            if (col[k] == c) out.push_back(idx[k]);
+    std::vector<int> g;
+    for (;;) {
+        cls.erase(std::remove_if(cls.begin(), cls.end(), [](const std::vector<int> &c) { return c.empty(); }), cls.end());
+        if (cls.empty()) break;
+        std::stable_sort(cls.begin(), cls.end(), [](const std::vector<int> &x, const std::vector<int> &y) { return x.size() > y.size(); });
+        g.assign(cls[0].begin(), cls[0].begin() + std::min<size_t>(cls[0].size(), G));
+        cls[0].erase(cls[0].begin(), cls[0].begin() + g.size());
+        uint32_t ma = 0, mb = 0;
+        for (int k : g) { ma |= 1u << ed[k].first; mb |= 1u << ed[k].second; }
+        for (size_t ci = 1; ci < cls.size() && (int)g.size() < G; ++ci) {
+            auto &c = cls[ci];
+            for (size_t q = 0; q < c.size() && (int)g.size() < G;) {
+                const int k = c[q];
+                const uint32_t ba = 1u << ed[k].first, bb = 1u << ed[k].second;
+                if (!(ma & ba) && !(mb & bb)) {
+                    g.push_back(k);
+                    ma |= ba;
+                    mb |= bb;
+                    c.erase(c.begin() + q);
+                } else {
+                    ++q;
+                }
+            }
+        }
+        for (size_t ci = cls.size(); ci-- > 0 && (int)g.size() < G;) {
+            auto &c = cls[ci];
+            while (!c.empty() && (int)g.size() < G) { g.push_back(c.back()); c.pop_back(); }
+        }
+        for (int k : g) out.push_back(idx[k]);
+    }
     std::copy(out.begin(), out.end(), idx);
 }
 
 // TMA-kernel layout of one tile (create time, host).  Local indices: own vertex v -> v - t*kTileV,
 // halo vertex -> kTileV + its rank in the tile's sorted halo list.  Each local index gets a
-// shared-memory slot (own: [0, kTileV), halo: [kTileV, kTileV + hcap)) whose bank (slot & 31) is
-// chosen greedily so that, for every (color, side) of the tile's constraint segments, the
-// endpoints spread evenly over the 32 banks (a linear layout folds a color's lower endpoints onto
-// half the banks: Morton index parities).  Each segment is then ordered into conflict-free warp
-// groups (bank_group).  Outputs: vslot / hslot (slots), tpos (sorted position -> layout position),
+// shared-memory slot (own: [0, kTileV), halo: [kTileV, kTileV + hcap)) holding a float4; its
+// 16-byte bank group (slot & 7) is chosen greedily so that, for every (color, side) of the tile's
+// constraint segments, the endpoints spread evenly over the 8 groups (a linear layout folds a
+// color's lower endpoints onto half of them: Morton index parities).  Each segment is then ordered
+// into groups of 8 (one quarter-warp access phase) with distinct groups per endpoint (bank_group).  Outputs: vslot / hslot (slots), tpos (sorted position -> layout position),
 // cpair (slot pairs in layout order), the permuted foreign segments with fpair / fposv.
 struct TileLayoutScratch {
     std::vector<int> deg, moff, memb, cnt, order, slot_of, used;
@@ -206,29 +232,30 @@ static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<i
     for (int l = 0; l < NL; ++l) w.deg[l] = w.moff[l];
     each([&](int l, int k) { w.memb[w.deg[l]++] = k; });
     // greedy bank assignment, most-constrained first, per region (own, halo)
-    w.cnt.assign((size_t)NK * 32, 0);
+    constexpr int NB = 8;   // 16-byte bank groups of a float4 access phase
+    w.cnt.assign((size_t)NK * NB, 0);
     w.slot_of.assign(NL, 0);
     for (int region = 0; region < 2; ++region) {
-        const int lo = region ? kTileV : 0, hi = region ? NL : kTileV, cap = region ? hcap / 32 : kTileV / 32;
+        const int lo = region ? kTileV : 0, hi = region ? NL : kTileV, cap = region ? hcap / NB : kTileV / NB;
         const int base = region ? kTileV : 0;
         w.order.resize(hi - lo);
         for (int l = lo; l < hi; ++l) w.order[l - lo] = l;
         std::stable_sort(w.order.begin(), w.order.end(),
                          [&](int x, int y) { return w.moff[x + 1] - w.moff[x] > w.moff[y + 1] - w.moff[y]; });
-        w.used.assign(32, 0);
+        w.used.assign(NB, 0);
         for (int l : w.order) {
             int best = -1;
             long bc = 0;
-            for (int b = 0; b < 32; ++b) {
+            for (int b = 0; b < NB; ++b) {
                 if (w.used[b] >= cap) continue;
                 long c = 0;
-                for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) c += w.cnt[(size_t)w.memb[m] * 32 + b];
+                for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) c += w.cnt[(size_t)w.memb[m] * NB + b];
                 c = c * 1024 + w.used[b];
                 if (best < 0 || c < bc) { best = b; bc = c; }
             }
-            w.slot_of[l] = base + 32 * w.used[best] + best;
+            w.slot_of[l] = base + NB * w.used[best] + best;
             w.used[best]++;
-            for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) w.cnt[(size_t)w.memb[m] * 32 + best]++;
+            for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) w.cnt[(size_t)w.memb[m] * NB + best]++;
         }
     }
     for (int l = 0; l < kTileV; ++l) vslot[(size_t)t * kTileV + l] = (uint16_t)w.slot_of[l];
@@ -239,14 +266,14 @@ static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<i
         const int64_t b = cnt[kk], e = cnt[kk + 1];
         w.ids.resize(e - b);
         for (int64_t q = b; q < e; ++q) w.ids[q - b] = (int32_t)q;
-        bank_group(w.ids.data(), (int)(e - b), [&](int32_t q) { return std::make_pair(sl(ab[q].x) & 31, sl(ab[q].y) & 31); });
+        bank_group(w.ids.data(), (int)(e - b), NB, NB, [&](int32_t q) { return std::make_pair(sl(ab[q].x) & (NB - 1), sl(ab[q].y) & (NB - 1)); });
         for (int64_t i = 0; i < e - b; ++i) {
             const int q = w.ids[i];
             tpos[q] = (int)(b + i);
             cpair[b + i] = (uint32_t)sl(ab[q].x) | ((uint32_t)sl(ab[q].y) << 16);
         }
         const int64_t fb = fc[kk], fe = fc[kk + 1];
-        bank_group(fidx + fb, (int)(fe - fb), [&](int32_t q) { return std::make_pair(sl(ab[q].x) & 31, sl(ab[q].y) & 31); });
+        bank_group(fidx + fb, (int)(fe - fb), NB, NB, [&](int32_t q) { return std::make_pair(sl(ab[q].x) & (NB - 1), sl(ab[q].y) & (NB - 1)); });
         for (int64_t k2 = fb; k2 < fe; ++k2) {
             const int q = fidx[k2];
             fposv[q] = (int)k2;
@@ -436,9 +463,11 @@ struct dxpbd_scene {
     DBuf<int4> d_fent;                    // foreign entries {j, a, b, 0}
     // CG-local tile structure (TMA-staged matvec, QF = 1)
     bool use_tma = false;
+    int capm = 0, capf = 0;   // TMA stage capacities (own / staged foreign entries per segment)
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
-    DBuf<int> d_hoff, d_hlist, d_fpos;
+    DBuf<int> d_hpad, d_fpos;
+    DBuf<int4> d_tseg;
     DBuf<uint32_t> d_cpair, d_fpair;
     DBuf<uint16_t> d_vslot, d_hslot;   // tile-local shared-memory slots (own vertices, halo entries)
     DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
@@ -450,6 +479,10 @@ struct dxpbd_scene {
     DBuf<int32_t> t_perm;
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
     TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
+    TmaTiles tma_tiles() const {
+        return TmaTiles{n_dist_colors, ntiles, hcap, capm, capf, d_tseg.p, d_cpair.p, d_fpair.p, d_hpad.p,
+                        reinterpret_cast<const float4 *>(Qd.p), d_fQ.p, d_vslot.p, d_hslot.p};
+    }
     // colliders
     DBuf<float> sph, cap_c, cap_a, cap_r0, cap_L0, cap_Rb, cap_Lb, beta;
     DBuf<Collider> cols;
@@ -659,8 +692,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     const float *Qc = s->NC ? s->Qc.p : nullptr;
     CGBufs bufs{s->ax.p, s->r.p, s->p.p, s->p1.p, s->q.p, nullptr};
     TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
-    TmaTiles tt{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_hoff.p, s->d_cpair.p, s->d_fpair.p,
-                s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p, s->d_vslot.p, s->d_hslot.p};
+    TmaTiles tt = s->tma_tiles();
     int it = 0;
     const int chunk = 8;
     iters_out = -1;
@@ -669,7 +701,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         int end = std::min(maxit, it + chunk);
         for (; it < end; ++it) {
             if (s->use_tma)
-                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(it, tt, V, s->hcap, Qc, bufs, xw, cs));
+                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             else
@@ -883,20 +915,35 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
             }
             s->hcap = (hmax + 31) / 32 * 32;
             s->halo_total = hoff[nt];
-            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors;
+            // stage capacities: the largest own segment, foreign entries staged up to 128 per segment
+            int maxm = 0, maxf = 0;
+            for (size_t kk = 0; kk < nkeys; ++kk) {
+                maxm = std::max<int>(maxm, (int)(cnt[kk + 1] - cnt[kk]));
+                maxf = std::max<int>(maxf, (int)(fc[kk + 1] - fc[kk]));
+            }
+            s->capm = (maxm + 7) & ~7;
+            s->capf = (std::min(maxf, 128) + 7) & ~7;
+            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors &&
+                         tma_rhs_smem_bytes(s->hcap, s->capm, s->capf) <= 200 * 1024;
             if (s->use_tma) {
-                std::vector<int> hlist(std::max(hoff[nt], 1));
-                for (int t = 0; t < nt; ++t) std::copy(halo[t].begin(), halo[t].end(), hlist.begin() + hoff[t]);
+                const int hc = s->hcap;
+                std::vector<int> hpad((size_t)nt * hc, -1);
+                for (int t = 0; t < nt; ++t) std::copy(halo[t].begin(), halo[t].end(), hpad.begin() + (size_t)t * hc);
+                std::vector<int4> tseg((size_t)nt * nc);
+                for (int t = 0; t < nt; ++t)
+                    for (int c = 0; c < nc; ++c)
+                        tseg[(size_t)t * nc + c] = make_int4(seg[(size_t)c * (nt + 1) + t], seg[(size_t)c * (nt + 1) + t + 1],
+                                                             fseg[(size_t)c * (nt + 1) + t], fseg[(size_t)c * (nt + 1) + t + 1]);
                 const int64_t NF = fc[nkeys];
                 std::vector<uint32_t> cpair(E + 4, 0), fpair((size_t)std::max<int64_t>(NF, 1) + 4, 0);
                 std::vector<int> fposv(E, -1), tpos(E);
-                std::vector<uint16_t> vslot((size_t)nt * kTileV), hslot(std::max(hoff[nt], 1));
+                std::vector<uint16_t> vslot((size_t)nt * kTileV), hslot((size_t)nt * hc);
                 // per tile (independent, threaded): bank-balanced shared-memory slots, then
                 // conflict-free warp groups of every (color, tile) segment (tma_tile_layout)
                 auto work = [&](int t0, int t1) {
                     TileLayoutScratch ws;
                     for (int t = t0; t < t1; ++t)
-                        tma_tile_layout(t, nc, nt, s->hcap, halo[t], hoff[t], cnt.data(), fc.data(), ab_sorted.data(),
+                        tma_tile_layout(t, nc, nt, hc, halo[t], t * hc, cnt.data(), fc.data(), ab_sorted.data(),
                                         fidx.data(), vslot.data(), hslot.data(), tpos.data(), cpair.data(), fpair.data(),
                                         fposv.data(), ws);
                 };
@@ -904,10 +951,10 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 std::vector<std::thread> pool;
                 for (int k = 0; k < nth; ++k) pool.emplace_back(work, (int)((int64_t)nt * k / nth), (int)((int64_t)nt * (k + 1) / nth));
                 for (auto &th : pool) th.join();
-                s->d_hoff.alloc(hoff.size());
-                upload(s->d_hoff.p, hoff.data(), sizeof(int) * hoff.size(), DXPBD_MEM_HOST, st);
-                s->d_hlist.alloc(hlist.size());
-                upload(s->d_hlist.p, hlist.data(), sizeof(int) * hlist.size(), DXPBD_MEM_HOST, st);
+                s->d_tseg.alloc(tseg.size());
+                upload(s->d_tseg.p, tseg.data(), sizeof(int4) * tseg.size(), DXPBD_MEM_HOST, st);
+                s->d_hpad.alloc(hpad.size());
+                upload(s->d_hpad.p, hpad.data(), sizeof(int) * hpad.size(), DXPBD_MEM_HOST, st);
                 s->d_vslot.alloc(vslot.size());
                 upload(s->d_vslot.p, vslot.data(), sizeof(uint16_t) * vslot.size(), DXPBD_MEM_HOST, st);
                 s->d_hslot.alloc(hslot.size());
@@ -921,8 +968,8 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 s->d_tpos.alloc(E);
                 upload(s->d_tpos.p, tpos.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
                 s->d_fQ.alloc((size_t)std::max<int64_t>(NF, 1));
-                s->tma_smem = tma_smem_bytes(s->hcap);
-                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap);
+                s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->capf);
+                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->capf);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
                 DX_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -1181,11 +1228,10 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         DX_CHECK_CUDA(cudaMemsetAsync(s->cg_sc.p, 0, sizeof(double) * (size_t)(s->cg_max_iter + 2) * 4, st));
         {
             TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
-            TmaTiles tt{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_hoff.p, s->d_cpair.p, s->d_fpair.p,
-                        s->d_hlist.p, reinterpret_cast<const float4 *>(s->Qd.p), s->d_fQ.p, s->d_vslot.p, s->d_hslot.p};
+            TmaTiles tt = s->tma_tiles();
             if (s->use_tma)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_rhs_smem, st>>>(
-                    tt, V, s->hcap, Qc, s->ax.p, s->uprev.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
+                    tt, V, Qc, s->ax.p, s->uprev.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
                     s->r.p, s->u0.p));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tiled<1><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->uprev.p,

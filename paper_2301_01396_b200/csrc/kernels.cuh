@@ -592,48 +592,62 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
 }
 
 // ---------------------------------------------------------------------------------------------
-// TMA-staged tiled kernels (QF = 1).  CG-local tile structure (built at create):
-//   halo list of tile t: every vertex outside the tile touched by a constraint that updates a
-//   vertex of the tile; its values are loaded once into shared-memory slots kTileV + h.
-//   cpair[j] (own constraint j, a in tile): la | lb' << 16, lb' = b - v0 or kTileV + halo slot.
-//   fpair[k] (foreign entry k, b in tile, a outside): (kTileV + slot(a)) | (b - v0) << 16, with its
-//   own copy fQ[k] of Q_j written by the replay; foreign entries are grouped by (color, tile).
-// Per color c the own range [seg(c,t), seg(c,t+1)) of cpair / Q and the foreign range
-// [fseg(c,t), fseg(c,t+1)) of fpair / fQ are contiguous: thread 0 stages them with bulk async
-// copies (cp.async.bulk -> mbarrier complete_tx) kTmaStages colors ahead; all threads then work
-// purely in shared memory (plain read-modify-write of the accumulator, one barrier per color,
-// vertex-disjoint within a color by R1).
+// TMA-staged tiled kernels (QF = 1).  CG-local tile structure (built at create, host
+// tma_tile_layout):
+//   every vertex a tile's constraints touch has a shared-memory slot: own vertices [0, kTileV),
+//   halo vertices (outside the tile) [kTileV, kTileV + hcap); values are float4 (x, y, z, -) so one
+//   16-byte access reads or writes a vertex.  Slots are assigned so that the endpoints of every
+//   color segment spread evenly over the 8 sixteen-byte bank groups, and each segment is ordered in
+//   groups of 8 entries (one quarter-warp access phase) with distinct bank groups per endpoint.
+//   cpair[j] (own constraint j, a in tile): slot(a) | slot(b) << 16 (b own or halo).
+//   fpair[k] (foreign entry k, b in tile, a outside): slot(a) | slot(b) << 16, with its own copy
+//   fQ[k] of Q_j written by the replay; foreign entries are grouped by (color, tile).
+// Per color c the own range of cpair / Q and the foreign range of fpair / fQ are contiguous:
+// thread 0 stages them with bulk async copies (cp.async.bulk -> mbarrier complete_tx) kTmaStages
+// colors ahead; all threads then work purely in shared memory (plain read-modify-write of the
+// accumulator, one barrier per color, vertex-disjoint within a color by R1).
 constexpr int kTmaStages = 3;
-constexpr int kFCap = 128;
 constexpr int kTmaThreads = 256;
-
-struct TmaTiles {
-    int ncol, ntiles;
-    const int *seg, *fseg, *hoff;
-    const uint32_t *cpair, *fpair;
-    const int *hlist;
-    const float4 *Q4, *fQ;
-    const uint16_t *vslot, *hslot;   // shared-memory slot of own vertex (t, i) / of halo entry (host: tma_tile_layout)
-};
-
-struct TmaStage {
-    uint32_t cp[kTileV + 4];
-    float4 q[kTileV];
-    uint32_t fp[kFCap + 4];
-    float4 fq[kFCap];
-};
-// dynamic smem: [bars][stages][sq 3*kTileV][sp 3*(kTileV + hcap)]
-__host__ __device__ inline size_t tma_smem_bytes(int hcap) {
-    return 64 + sizeof(TmaStage) * kTmaStages + sizeof(float) * 3 * kTileV + sizeof(float) * 3 * (kTileV + hcap);
-}
-
 constexpr int kMaxColors = 64;   // bounds table in shared memory (more colors: generic kernel)
 
+struct TmaTiles {
+    int ncol, ntiles, hcap;
+    int capm, capf;                  // stage capacities: max own entries per segment, staged foreign entries
+    const int4 *tseg;                // [tile][color]: own range (b, e) of cpair / Q4, foreign range (fb, fe)
+    const uint32_t *cpair, *fpair;   // slot pairs (la | lb << 16)
+    const int *hpad;                 // [tile][hcap]: halo vertex ids, -1 padded (fixed stride)
+    const float4 *Q4, *fQ;
+    const uint16_t *vslot;           // [tile][kTileV]: slot of own vertex i
+    const uint16_t *hslot;           // [tile][hcap]: slot of halo entry h
+};
 
-DX_INLINE void tma_issue(uint64_t *bar, TmaStage &S, int c, const int *sb, const TmaTiles &T) {
-    const int b = sb[4 * c], e = sb[4 * c + 1];
-    const int fb = sb[4 * c + 2], fe = sb[4 * c + 3];
-    const int nf = min(fe - fb, kFCap);
+// One stage (bytes, 16-aligned parts): q[capm] | fq[capf] | cp[capm + 4, rounded] | fp[capf + 4, rounded]
+__host__ __device__ inline uint32_t tma_stage_bytes(int capm, int capf) {
+    return (uint32_t)(16 * capm + 16 * capf + ((4 * (capm + 4) + 15) & ~15) + ((4 * (capf + 4) + 15) & ~15));
+}
+struct StageView {
+    const float4 *q, *fq;
+    const uint32_t *cp, *fp;
+};
+DX_INLINE StageView stage_view(unsigned char *base, int capm, int capf) {
+    StageView v;
+    v.q = reinterpret_cast<const float4 *>(base);
+    v.fq = v.q + capm;
+    v.cp = reinterpret_cast<const uint32_t *>(v.fq + capf);
+    v.fp = v.cp + ((capm + 4 + 3) & ~3);
+    return v;
+}
+// dynamic smem of the matvec: [bars 64][stages][sq float4 kTileV][sp float4 kTileV + hcap]
+__host__ __device__ inline size_t tma_smem_bytes(int hcap, int capm, int capf) {
+    return 64 + (size_t)tma_stage_bytes(capm, capf) * kTmaStages + 16 * (size_t)kTileV + 16 * (size_t)(kTileV + hcap);
+}
+// rhs: [bars][stages][sqb, sqr float4 kTileV][sy, sz float4 kTileV + hcap]
+__host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap, int capm, int capf) {
+    return 64 + (size_t)tma_stage_bytes(capm, capf) * kTmaStages + 32 * (size_t)kTileV + 32 * (size_t)(kTileV + hcap);
+}
+
+DX_INLINE void tma_issue(uint64_t *bar, unsigned char *stage, int4 g, const TmaTiles &T) {
+    const int b = g.x, e = g.y, fb = g.z, nf = min(g.w - g.z, T.capf);
     uint32_t tot = 0;
     size_t c0 = 0, c1 = 0, f0 = 0, f1 = 0;
     if (e > b) {
@@ -647,124 +661,119 @@ DX_INLINE void tma_issue(uint64_t *bar, TmaStage &S, int c, const int *sb, const
         tot += (uint32_t)(f1 - f0) + (uint32_t)nf * 16u;
     }
     mbar_expect_tx(bar, tot);
+    const StageView S = stage_view(stage, T.capm, T.capf);
     if (e > b) {
-        bulk_g2s(S.cp, reinterpret_cast<const char *>(T.cpair) + c0, (uint32_t)(c1 - c0), bar);
-        bulk_g2s(S.q, T.Q4 + b, (uint32_t)(e - b) * 16u, bar);
+        bulk_g2s((void *)S.cp, reinterpret_cast<const char *>(T.cpair) + c0, (uint32_t)(c1 - c0), bar);
+        bulk_g2s((void *)S.q, T.Q4 + b, (uint32_t)(e - b) * 16u, bar);
     }
     if (nf > 0) {
-        bulk_g2s(S.fp, reinterpret_cast<const char *>(T.fpair) + f0, (uint32_t)(f1 - f0), bar);
-        bulk_g2s(S.fq, T.fQ + fb, (uint32_t)nf * 16u, bar);
+        bulk_g2s((void *)S.fp, reinterpret_cast<const char *>(T.fpair) + f0, (uint32_t)(f1 - f0), bar);
+        bulk_g2s((void *)S.fq, T.fQ + fb, (uint32_t)nf * 16u, bar);
     }
 }
 
-// Walk all colors of tile t.  sp: values (own then halo slots), sq: own accumulator.
-// SIGN +1: sq += A_dist sp (CG, also accumulates sp.(A sp) over own constraints); SIGN -1: sq -= ...
-template <int SIGN>
-DX_INLINE float tma_tile_colors(uint64_t *bars, TmaStage *stages, float (*sp)[1], int spn, float *sq0, const int *sb,
+// Entry i of a color's combined list: own constraints [0, nm), padding up to nmp (a multiple of 8,
+// so foreign entries start on a quarter-warp boundary as the host grouped them), then foreign
+// entries (staged up to capf; the rest read from global memory by a cold path).
+struct TItem {
+    uint32_t pr;
+    float4 q;
+};
+__device__ __noinline__ TItem titem_global(const TmaTiles &T, int k) { return TItem{T.fpair[k], T.fQ[k]}; }
+DX_INLINE float3 xyz(float4 v) { return make_float3(v.x, v.y, v.z); }
+DX_INLINE float4 f4of(float3 v) { return make_float4(v.x, v.y, v.z, 0.f); }
+
+// Walk all colors of tile t: sq += A_dist sp; returns sp.(A_dist sp) over own constraints.
+DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const float4 *sp, float4 *sq, const int4 *sb,
                                 const TmaTiles &T) {
     float dotacc = 0.f;
-    float *sp0 = &sp[0][0];
-    float *sp1 = sp0 + spn, *sp2 = sp0 + 2 * spn;
-    float *sq1 = sq0 + kTileV, *sq2 = sq0 + 2 * kTileV;
+    const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
     for (int c = 0; c < T.ncol; ++c) {
         const int st = c % kTmaStages;
-        TmaStage &S = stages[st];
+        unsigned char *stage = stages + (size_t)st * sbytes;
+        const StageView S = stage_view(stage, T.capm, T.capf);
         mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
-        const int b = sb[4 * c], e = sb[4 * c + 1];
-        const int off = (int)((((size_t)b * 4) & 15) >> 2);
-        for (int i = threadIdx.x; i < e - b; i += blockDim.x) {
-            const uint32_t pr = S.cp[off + i];
-            const float4 q4 = S.q[i];
-            const int la = pr & 0xffff, lb = pr >> 16;
-            const float3 d = make_float3(sp0[la] - sp0[lb], sp1[la] - sp1[lb], sp2[la] - sp2[lb]);
-            float3 y = qmul_iso_rank1(q4, d);
-            if (SIGN > 0) dotacc += dot3(d, y);
-            else y = -y;
-            sq0[la] += y.x;
-            sq1[la] += y.y;
-            sq2[la] += y.z;
-            if (lb < kTileV) {
-                sq0[lb] -= y.x;
-                sq1[lb] -= y.y;
-                sq2[lb] -= y.z;
+        const int4 g = sb[c];
+        const int nm = g.y - g.x, nmp = (nm + 7) & ~7, n = nmp + (g.w - g.z);
+        const int off = g.x & 3, foff = g.z & 3;
+        for (int i = threadIdx.x; i < n; i += kTmaThreads) {
+            TItem e;
+            if (i < nm) e = TItem{S.cp[off + i], S.q[i]};
+            else if (i < nmp) continue;
+            else if (i - nmp < T.capf) e = TItem{S.fp[foff + i - nmp], S.fq[i - nmp]};
+            else e = titem_global(T, g.z + i - nmp);
+            const int la = e.pr & 0xffff, lb = e.pr >> 16;
+            const float3 d = xyz(sp[la]) - xyz(sp[lb]);
+            const float3 y = qmul_iso_rank1(e.q, d);
+            if (i < nm) {   // own constraint: a is an own vertex
+                dotacc += dot3(d, y);
+                sq[la] = f4of(xyz(sq[la]) + y);
             }
-        }
-        const int fb = sb[4 * c + 2], fe = sb[4 * c + 3];
-        const int foff = (int)((((size_t)fb * 4) & 15) >> 2);
-        for (int i = threadIdx.x; i < fe - fb; i += blockDim.x) {
-            const uint32_t pr = i < kFCap ? S.fp[foff + i] : T.fpair[fb + i];
-            const float4 q4 = i < kFCap ? S.fq[i] : T.fQ[fb + i];
-            const int la = pr & 0xffff, lb = pr >> 16;   // la: halo slot of a, lb: own b
-            const float3 d = make_float3(sp0[la] - sp0[lb], sp1[la] - sp1[lb], sp2[la] - sp2[lb]);
-            float3 y = qmul_iso_rank1(q4, d);
-            if (SIGN < 0) y = -y;
-            sq0[lb] -= y.x;
-            sq1[lb] -= y.y;
-            sq2[lb] -= y.z;
+            if (lb < kTileV) sq[lb] = f4of(xyz(sq[lb]) - y);
         }
         __syncthreads();
         if (threadIdx.x == 0 && c + kTmaStages < T.ncol) {
             fence_proxy_async();
-            tma_issue(&bars[st], S, c + kTmaStages, sb, T);
+            tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
         }
     }
     return dotacc;
 }
 
 // Fused PCG matvec (see k_cg_matvec): p_it update for own and halo vertices, q = A p, p.q.
-__global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTiles T, int V, int hcap,
+// Round trip 1 loads everything that has no dependency (convergence flag, per-color ranges,
+// halo ids, slots, inverse masses); round trip 2 the vector values and the first bulk copies.
+__global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTiles T, int V,
                                                                   const float *__restrict__ Qc, CGBufs B,
                                                                   const float *__restrict__ wv, CGState s) {
-    if (cg_done(s, it + 1)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
-    TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 64);
-    float *sq = reinterpret_cast<float *>(smem_raw + 64 + sizeof(TmaStage) * kTmaStages);
-    float *sp = sq + 3 * kTileV;
-    const int spn = kTileV + hcap;
+    unsigned char *stages = smem_raw + 64;
+    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.capm, T.capf) * kTmaStages);
+    float4 *sp = sq + kTileV;
+    const int hcap = T.hcap;
     const int t = blockIdx.x;
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
-    __shared__ int sb[4 * kMaxColors];   // per-color (b, e, fb, fe) of this tile
-    {
-        const int stride = T.ntiles + 1;
-        for (int c = threadIdx.x; c < T.ncol; c += blockDim.x) {
-            sb[4 * c] = T.seg[c * stride + t];
-            sb[4 * c + 1] = T.seg[c * stride + t + 1];
-            sb[4 * c + 2] = T.fseg[c * stride + t];
-            sb[4 * c + 3] = T.fseg[c * stride + t + 1];
-        }
+    __shared__ int4 sb[kMaxColors];
+    constexpr int NO = kTileV / kTmaThreads, NH = 2;
+    // ---- round trip 1
+    const bool done = cg_done(s, it + 1);
+    if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
+    float wo[NO];
+    int so[NO];
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int i = threadIdx.x + u * kTmaThreads;
+        wo[u] = wv[min(v0 + i, V - 1)];
+        so[u] = T.vslot[(size_t)t * kTileV + i];
     }
+    int hv[NH], hs[NH];
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        const int h = threadIdx.x + u * kTmaThreads;
+        hv[u] = h < hcap ? T.hpad[(size_t)t * hcap + h] : -1;
+        hs[u] = h < hcap ? T.hslot[(size_t)t * hcap + h] : 0;
+    }
+    if (done) return;
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
-        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages[c], c, sb, T);
+        const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
+        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
+    // ---- round trip 2
     const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
     float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
     const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
-    // vertex phase: all loads of a thread (own vertices and halo slots) are issued as one batch,
-    // unconditionally, before any use (no load behind a w > 0 branch)
-    constexpr int NO = kTileV / kTmaThreads;
-    float wo[NO];
     float3 ro[NO], po[NO];
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
-        const int i = threadIdx.x + u * kTmaThreads;
-        const int v = min(v0 + i, V - 1);
-        wo[u] = wv[v];
+        const int v = min(v0 + (int)threadIdx.x + u * kTmaThreads, V - 1);
         ro[u] = it > 0 ? B.r[v] : pnew[v];
         po[u] = it > 0 ? pold[v] : make_float3(0.f, 0.f, 0.f);
-    }
-    const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
-    constexpr int NH = 2;
-    int hv[NH];
-#pragma unroll
-    for (int u = 0; u < NH; ++u) {
-        const int h = threadIdx.x + u * kTmaThreads;
-        hv[u] = h < nh ? T.hlist[h0 + h] : -1;
     }
     float hw[NH];
     float3 hr[NH], hp[NH];
@@ -787,64 +796,47 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
                 pv = it > 0 ? make_float3(w * ro[u].x + beta * po[u].x, w * ro[u].y + beta * po[u].y,
                                           w * ro[u].z + beta * po[u].z)
                             : ro[u];
-                float3 pp = f3(pv);
-                qv = (1.f / w) * pp;
+                qv = (1.f / w) * pv;
                 if (Qc) {
                     Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
                                   Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
-                    qv = qv + sym3_mul(A, pp);
+                    qv = qv + sym3_mul(A, pv);
                 }
-                acc[0] += dot3(pp, qv);
+                acc[0] += dot3(pv, qv);
             }
             if (it > 0) pnew[v] = pv;
         }
-        const int si = T.vslot[(size_t)t * kTileV + i];
-        sp[si] = pv.x;
-        sp[spn + si] = pv.y;
-        sp[2 * spn + si] = pv.z;
-        sq[si] = qv.x;
-        sq[kTileV + si] = qv.y;
-        sq[2 * kTileV + si] = qv.z;
+        sp[so[u]] = f4of(pv);
+        sq[so[u]] = f4of(qv);
     }
 #pragma unroll
     for (int u = 0; u < NH; ++u) {
-        const int h = threadIdx.x + u * kTmaThreads;
         if (hv[u] >= 0) {
             float3 pv = make_float3(0.f, 0.f, 0.f);
             if (hw[u] > 0.f)
                 pv = it > 0 ? make_float3(hw[u] * hr[u].x + beta * hp[u].x, hw[u] * hr[u].y + beta * hp[u].y,
                                           hw[u] * hr[u].z + beta * hp[u].z)
                             : f3(hr[u]);
-            const int sh = T.hslot[h0 + h];
-            sp[sh] = pv.x;
-            sp[spn + sh] = pv.y;
-            sp[2 * spn + sh] = pv.z;
+            sp[hs[u]] = f4of(pv);
         }
     }
-    for (int h = threadIdx.x + NH * kTmaThreads; h < nh; h += blockDim.x) {   // rare: large halos
-        const int v = T.hlist[h0 + h];
-        const float3 pv = halo_p(it, v, beta, B.r, pold, pnew, wv);
-        const int sh = T.hslot[h0 + h];
-        sp[sh] = pv.x;
-        sp[spn + sh] = pv.y;
-        sp[2 * spn + sh] = pv.z;
+    for (int h = threadIdx.x + NH * kTmaThreads; h < hcap; h += blockDim.x) {   // rare: large halos
+        const int v = T.hpad[(size_t)t * hcap + h];
+        if (v >= 0) sp[T.hslot[(size_t)t * hcap + h]] = f4of(halo_p(it, v, beta, B.r, pold, pnew, wv));
     }
     __syncthreads();
-    acc[0] += tma_tile_colors<1>(bars, stages, reinterpret_cast<float (*)[1]>(sp), spn, sq, sb, T);
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-        const int v = v0 + i, si = T.vslot[(size_t)t * kTileV + i];
-        B.q[v] = wv[v] > 0.f ? make_float3(sq[si], sq[kTileV + si], sq[2 * kTileV + si]) : make_float3(0.f, 0.f, 0.f);
+    acc[0] += tma_tile_colors(bars, stages, sp, sq, sb, T);
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int i = threadIdx.x + u * kTmaThreads;
+        if (i < nv) B.q[v0 + i] = wo[u] > 0.f ? xyz(sq[so[u]]) : make_float3(0.f, 0.f, 0.f);
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-
-// Increment-system right-hand side with warm start (kernels "adjoint"): for own vertices, with
-// u = u_{n+1}, uprev = u_{n+2} and the extrapolated initial guess u0 = 2u - uprev,
-//   b  = M u + dphi - (Qc + A) y              (the system right-hand side, for its norm)
-//   r0 = b - (M + Qc + A) u0 = dphi - M (u - uprev) - (Qc + A)(y + u0)
-// A_dist is applied to y and to z = y + u0 in the same pass (Q read once).  Writes b, r0, u0.
-__global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, int hcap, const float *__restrict__ Qc,
+// rhs (warm start): b = M u - Q_n y + dphi, r0 = b - A_n (u + du); A_dist applied tile-locally
+// with the same staging / slot layout as the matvec.
+__global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, const float *__restrict__ Qc,
                                                             const float3 *__restrict__ u, const float3 *__restrict__ uprev,
                                                             const float3 *__restrict__ y,
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
@@ -853,30 +845,23 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
                                                             float3 *__restrict__ u0out) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
-    TmaStage *stages = reinterpret_cast<TmaStage *>(smem_raw + 64);
-    float *sqb = reinterpret_cast<float *>(smem_raw + 64 + sizeof(TmaStage) * kTmaStages);
-    float *sqr = sqb + 3 * kTileV;
-    const int spn = kTileV + hcap;
-    float *sy = sqr + 3 * kTileV;
-    float *sz = sy + 3 * spn;
+    unsigned char *stages = smem_raw + 64;
+    const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
+    float4 *sqb = reinterpret_cast<float4 *>(stages + (size_t)sbytes * kTmaStages);
+    float4 *sqr = sqb + kTileV;
+    const int hcap = T.hcap;
+    float4 *sy = sqr + kTileV;
+    float4 *sz = sy + kTileV + hcap;
     const int t = blockIdx.x;
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
-    __shared__ int sb[4 * kMaxColors];
-    {
-        const int stride = T.ntiles + 1;
-        for (int c = threadIdx.x; c < T.ncol; c += blockDim.x) {
-            sb[4 * c] = T.seg[c * stride + t];
-            sb[4 * c + 1] = T.seg[c * stride + t + 1];
-            sb[4 * c + 2] = T.fseg[c * stride + t];
-            sb[4 * c + 3] = T.fseg[c * stride + t + 1];
-        }
-    }
+    __shared__ int4 sb[kMaxColors];
+    if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
-        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages[c], c, sb, T);
+        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
     for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
         float3 yv = make_float3(0.f, 0.f, 0.f), zv = yv, bb = yv, rr = yv;
@@ -909,71 +894,60 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, i
             }
         }
         const int si = T.vslot[(size_t)t * kTileV + i];
-        sy[si] = yv.x; sy[spn + si] = yv.y; sy[2 * spn + si] = yv.z;
-        sz[si] = zv.x; sz[spn + si] = zv.y; sz[2 * spn + si] = zv.z;
-        sqb[si] = bb.x; sqb[kTileV + si] = bb.y; sqb[2 * kTileV + si] = bb.z;
-        sqr[si] = rr.x; sqr[kTileV + si] = rr.y; sqr[2 * kTileV + si] = rr.z;
+        sy[si] = f4of(yv);
+        sz[si] = f4of(zv);
+        sqb[si] = f4of(bb);
+        sqr[si] = f4of(rr);
     }
-    const int h0 = T.hoff[t], nh = T.hoff[t + 1] - h0;
-    for (int h = threadIdx.x; h < nh; h += blockDim.x) {
-        const int v = T.hlist[h0 + h];
+    for (int h = threadIdx.x; h < hcap; h += blockDim.x) {
+        const int v = T.hpad[(size_t)t * hcap + h];
+        if (v < 0) continue;
         const float3 uh = f3(u[v]);
         const float3 yv = f3(y[v]), zv = yv + uh + (uh - f3(uprev[v]));
-        const int sh = T.hslot[h0 + h];
-        sy[sh] = yv.x; sy[spn + sh] = yv.y; sy[2 * spn + sh] = yv.z;
-        sz[sh] = zv.x; sz[spn + sh] = zv.y; sz[2 * spn + sh] = zv.z;
+        const int sh = T.hslot[(size_t)t * hcap + h];
+        sy[sh] = f4of(yv);
+        sz[sh] = f4of(zv);
     }
     __syncthreads();
+    // b -= A_dist y, r0 -= A_dist z (same per-color scheme as tma_tile_colors)
     for (int c = 0; c < T.ncol; ++c) {
         const int st = c % kTmaStages;
-        TmaStage &S = stages[st];
+        unsigned char *stage = stages + (size_t)st * sbytes;
+        const StageView S = stage_view(stage, T.capm, T.capf);
         mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
-        const int b = sb[4 * c], e = sb[4 * c + 1];
-        const int off = (int)((((size_t)b * 4) & 15) >> 2);
-        for (int i = threadIdx.x; i < e - b; i += blockDim.x) {
-            const uint32_t pr = S.cp[off + i];
-            const float4 q4 = S.q[i];
-            const int la = pr & 0xffff, lb = pr >> 16;
-            const float3 qy = qmul_iso_rank1(q4, make_float3(sy[la] - sy[lb], sy[spn + la] - sy[spn + lb],
-                                                             sy[2 * spn + la] - sy[2 * spn + lb]));
-            const float3 qz = qmul_iso_rank1(q4, make_float3(sz[la] - sz[lb], sz[spn + la] - sz[spn + lb],
-                                                             sz[2 * spn + la] - sz[2 * spn + lb]));
-            sqb[la] -= qy.x; sqb[kTileV + la] -= qy.y; sqb[2 * kTileV + la] -= qy.z;
-            sqr[la] -= qz.x; sqr[kTileV + la] -= qz.y; sqr[2 * kTileV + la] -= qz.z;
-            if (lb < kTileV) {
-                sqb[lb] += qy.x; sqb[kTileV + lb] += qy.y; sqb[2 * kTileV + lb] += qy.z;
-                sqr[lb] += qz.x; sqr[kTileV + lb] += qz.y; sqr[2 * kTileV + lb] += qz.z;
+        const int4 g = sb[c];
+        const int nm = g.y - g.x, nmp = (nm + 7) & ~7, n = nmp + (g.w - g.z);
+        const int off = g.x & 3, foff = g.z & 3;
+        for (int i = threadIdx.x; i < n; i += kTmaThreads) {
+            TItem e;
+            if (i < nm) e = TItem{S.cp[off + i], S.q[i]};
+            else if (i < nmp) continue;
+            else if (i - nmp < T.capf) e = TItem{S.fp[foff + i - nmp], S.fq[i - nmp]};
+            else e = titem_global(T, g.z + i - nmp);
+            const int la = e.pr & 0xffff, lb = e.pr >> 16;
+            const float3 qy = qmul_iso_rank1(e.q, xyz(sy[la]) - xyz(sy[lb]));
+            const float3 qz = qmul_iso_rank1(e.q, xyz(sz[la]) - xyz(sz[lb]));
+            if (i < nm) {
+                sqb[la] = f4of(xyz(sqb[la]) - qy);
+                sqr[la] = f4of(xyz(sqr[la]) - qz);
             }
-        }
-        const int fb = sb[4 * c + 2], fe = sb[4 * c + 3];
-        const int foff = (int)((((size_t)fb * 4) & 15) >> 2);
-        for (int i = threadIdx.x; i < fe - fb; i += blockDim.x) {
-            const uint32_t pr = i < kFCap ? S.fp[foff + i] : T.fpair[fb + i];
-            const float4 q4 = i < kFCap ? S.fq[i] : T.fQ[fb + i];
-            const int la = pr & 0xffff, lb = pr >> 16;   // la: halo slot of a, lb: own b
-            const float3 qy = qmul_iso_rank1(q4, make_float3(sy[la] - sy[lb], sy[spn + la] - sy[spn + lb],
-                                                             sy[2 * spn + la] - sy[2 * spn + lb]));
-            const float3 qz = qmul_iso_rank1(q4, make_float3(sz[la] - sz[lb], sz[spn + la] - sz[spn + lb],
-                                                             sz[2 * spn + la] - sz[2 * spn + lb]));
-            sqb[lb] += qy.x; sqb[kTileV + lb] += qy.y; sqb[2 * kTileV + lb] += qy.z;
-            sqr[lb] += qz.x; sqr[kTileV + lb] += qz.y; sqr[2 * kTileV + lb] += qz.z;
+            if (lb < kTileV) {
+                sqb[lb] = f4of(xyz(sqb[lb]) + qy);
+                sqr[lb] = f4of(xyz(sqr[lb]) + qz);
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0 && c + kTmaStages < T.ncol) {
             fence_proxy_async();
-            tma_issue(&bars[st], S, c + kTmaStages, sb, T);
+            tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
         }
     }
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i, si = T.vslot[(size_t)t * kTileV + i];
         const bool fr = wv[v] > 0.f;
-        bout[v] = fr ? make_float3(sqb[si], sqb[kTileV + si], sqb[2 * kTileV + si]) : make_float3(0.f, 0.f, 0.f);
-        r0out[v] = fr ? make_float3(sqr[si], sqr[kTileV + si], sqr[2 * kTileV + si]) : make_float3(0.f, 0.f, 0.f);
+        bout[v] = fr ? xyz(sqb[si]) : make_float3(0.f, 0.f, 0.f);
+        r0out[v] = fr ? xyz(sqr[si]) : make_float3(0.f, 0.f, 0.f);
     }
-}
-
-__host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap) {
-    return 64 + sizeof(TmaStage) * kTmaStages + sizeof(float) * 6 * kTileV + sizeof(float) * 6 * (kTileV + hcap);
 }
 
 // PCG start from the warm start: r = r0 (filtered), p_0 = M^-1 r; slot 0 gets r.z and r.r;
