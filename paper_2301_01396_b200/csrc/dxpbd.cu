@@ -464,6 +464,7 @@ struct dxpbd_scene {
     // CG-local tile structure (TMA-staged matvec, QF = 1)
     bool use_tma = false;
     int capm = 0, capf = 0;   // TMA stage capacities (own / staged foreign entries per segment)
+    int mv_variant = 0;       // TMA matvec variant: 0 = 256 x 4/SM one entry per pass, 1 = two-entry ILP, 2 = 320 x 3/SM
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hpad, d_fpos;
@@ -700,8 +701,12 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         for (; it < end; ++it) {
-            if (s->use_tma)
-                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec_tma<<<s->ntiles, kTmaThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs));
+            if (s->use_tma && s->mv_variant == 1)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4, 1><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
+            else if (s->use_tma && s->mv_variant == 2)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<320, 3, 0><<<s->ntiles, 320, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
+            else if (s->use_tma)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4, 0><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             else
@@ -970,7 +975,10 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 s->d_fQ.alloc((size_t)std::max<int64_t>(NF, 1));
                 s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->capf);
                 s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->capf);
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<320, 3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                if (const char *ev = getenv("DXPBD_MV")) s->mv_variant = atoi(ev);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
                 DX_CHECK_CUDA(cudaStreamSynchronize(st));
             }

@@ -680,10 +680,46 @@ struct TItem {
     float4 q;
 };
 __device__ __noinline__ TItem titem_global(const TmaTiles &T, int k) { return TItem{T.fpair[k], T.fQ[k]}; }
+DX_INLINE TItem titem(const StageView &S, int i, int nm, int nmp, int off, int foff, int fb, const TmaTiles &T) {
+    if (i < nm) return TItem{S.cp[off + i], S.q[i]};
+    if (i - nmp < T.capf) return TItem{S.fp[foff + i - nmp], S.fq[i - nmp]};
+    return titem_global(T, fb + i - nmp);
+}
 DX_INLINE float3 xyz(float4 v) { return make_float3(v.x, v.y, v.z); }
 DX_INLINE float4 f4of(float3 v) { return make_float4(v.x, v.y, v.z, 0.f); }
 
+// Up to NE (1, 2) entries i0, i1 of one color per thread (i0 valid; i1 checked), all shared loads
+// before any store: entries of one color are vertex-disjoint (R1), so no aliasing.
+template <int NE>
+DX_INLINE float mv_entries(const StageView &S, int i0, int i1, int n, int nm, int nmp, int off, int foff, int fb,
+                           const TmaTiles &T, const float4 *sp, float4 *sq) {
+    const bool h1 = NE == 2 && i1 < n && !(i1 >= nm && i1 < nmp);
+    const TItem e0 = titem(S, i0, nm, nmp, off, foff, fb, T);
+    TItem e1{0u, make_float4(0.f, 0.f, 0.f, 0.f)};
+    if (h1) e1 = titem(S, i1, nm, nmp, off, foff, fb, T);
+    const int la0 = e0.pr & 0xffff, lb0 = e0.pr >> 16, la1 = e1.pr & 0xffff, lb1 = e1.pr >> 16;
+    const float3 d0 = xyz(sp[la0]) - xyz(sp[lb0]);
+    float3 d1 = make_float3(0.f, 0.f, 0.f);
+    if (h1) d1 = xyz(sp[la1]) - xyz(sp[lb1]);
+    const float3 y0 = qmul_iso_rank1(e0.q, d0), y1 = qmul_iso_rank1(e1.q, d1);
+    const bool a0 = i0 < nm, a1 = h1 && i1 < nm;            // own constraint: a is an own vertex
+    const bool b0 = lb0 < kTileV, b1 = h1 && lb1 < kTileV;
+    float dot = a0 ? dot3(d0, y0) : 0.f;
+    if (a1) dot += dot3(d1, y1);
+    float4 qa0, qb0, qa1, qb1;
+    if (a0) qa0 = sq[la0];
+    if (b0) qb0 = sq[lb0];
+    if (a1) qa1 = sq[la1];
+    if (b1) qb1 = sq[lb1];
+    if (a0) sq[la0] = f4of(xyz(qa0) + y0);
+    if (b0) sq[lb0] = f4of(xyz(qb0) - y0);
+    if (a1) sq[la1] = f4of(xyz(qa1) + y1);
+    if (b1) sq[lb1] = f4of(xyz(qb1) - y1);
+    return dot;
+}
+
 // Walk all colors of tile t: sq += A_dist sp; returns sp.(A_dist sp) over own constraints.
+template <int NT, int LOOP>
 DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const float4 *sp, float4 *sq, const int4 *sb,
                                 const TmaTiles &T) {
     float dotacc = 0.f;
@@ -696,26 +732,27 @@ DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const flo
         const int4 g = sb[c];
         const int nm = g.y - g.x, nmp = (nm + 7) & ~7, n = nmp + (g.w - g.z);
         const int off = g.x & 3, foff = g.z & 3;
-        for (int i = threadIdx.x; i < n; i += kTmaThreads) {
-            TItem e;
-            if (i < nm) e = TItem{S.cp[off + i], S.q[i]};
-            else if (i < nmp) continue;
-            else if (i - nmp < T.capf) e = TItem{S.fp[foff + i - nmp], S.fq[i - nmp]};
-            else e = titem_global(T, g.z + i - nmp);
-            const int la = e.pr & 0xffff, lb = e.pr >> 16;
-            const float3 d = xyz(sp[la]) - xyz(sp[lb]);
-            const float3 y = qmul_iso_rank1(e.q, d);
-            if (i < nm) {   // own constraint: a is an own vertex
-                dotacc += dot3(d, y);
-                sq[la] = f4of(xyz(sq[la]) + y);
+        if (LOOP == 0) {
+            for (int i = threadIdx.x; i < n; i += NT) {
+                if (i >= nm && i < nmp) continue;
+                dotacc += mv_entries<1>(S, i, 0, n, nm, nmp, off, foff, g.z, T, sp, sq);
             }
-            if (lb < kTileV) sq[lb] = f4of(xyz(sq[lb]) - y);
+        } else {
+            // entries i and i + NT per thread; warps that own a second entry process both with all
+            // shared loads first (entries of one color are vertex-disjoint, R1: no aliasing)
+            for (int base = 0; base < n; base += 2 * NT) {
+                const int i0 = base + threadIdx.x, i1 = i0 + NT;
+                const bool two = __any_sync(0xffffffffu, i1 < n);   // uniform loop: every lane votes
+                if (i0 >= n || (i0 >= nm && i0 < nmp)) continue;
+                dotacc += two ? mv_entries<2>(S, i0, i1, n, nm, nmp, off, foff, g.z, T, sp, sq)
+                              : mv_entries<1>(S, i0, i1, n, nm, nmp, off, foff, g.z, T, sp, sq);
+            }
         }
         __syncthreads();
-        if (threadIdx.x == 0 && c + kTmaStages < T.ncol) {
-            fence_proxy_async();
-            tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
-        }
+        // re-arm this stage for color c + kTmaStages: all reads of it completed before the barrier
+        // (write-after-read across proxies is ordered by the barrier, as in a TMA consumer release);
+        // issued from the last warp, which never holds a second entry
+        if (threadIdx.x == NT - 32 && c + kTmaStages < T.ncol) tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
     }
     return dotacc;
 }
@@ -723,7 +760,10 @@ DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const flo
 // Fused PCG matvec (see k_cg_matvec): p_it update for own and halo vertices, q = A p, p.q.
 // Round trip 1 loads everything that has no dependency (convergence flag, per-color ranges,
 // halo ids, slots, inverse masses); round trip 2 the vector values and the first bulk copies.
-__global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTiles T, int V,
+// NT threads per CTA (a color's combined list is ~1.1 x kTileV / 2 entries: NT = 320 processes it
+// in one pass), MINB resident CTAs per SM.
+template <int NT, int MINB, int LOOP>
+__global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, int V,
                                                                   const float *__restrict__ Qc, CGBufs B,
                                                                   const float *__restrict__ wv, CGState s) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -736,7 +776,7 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
     __shared__ int4 sb[kMaxColors];
-    constexpr int NO = kTileV / kTmaThreads, NH = 2;
+    constexpr int NO = (kTileV + NT - 1) / NT, NH = (512 + NT - 1) / NT;
     // ---- round trip 1
     const bool done = cg_done(s, it + 1);
     if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
@@ -744,20 +784,20 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
     int so[NO];
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
-        const int i = threadIdx.x + u * kTmaThreads;
+        const int i = threadIdx.x + u * NT;
         wo[u] = wv[min(v0 + i, V - 1)];
-        so[u] = T.vslot[(size_t)t * kTileV + i];
+        so[u] = i < kTileV ? T.vslot[(size_t)t * kTileV + i] : 0;
     }
     int hv[NH], hs[NH];
 #pragma unroll
     for (int u = 0; u < NH; ++u) {
-        const int h = threadIdx.x + u * kTmaThreads;
+        const int h = threadIdx.x + u * NT;
         hv[u] = h < hcap ? T.hpad[(size_t)t * hcap + h] : -1;
         hs[u] = h < hcap ? T.hslot[(size_t)t * hcap + h] : 0;
     }
     if (done) return;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == NT - 32) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
         const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
@@ -771,7 +811,7 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
     float3 ro[NO], po[NO];
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
-        const int v = min(v0 + (int)threadIdx.x + u * kTmaThreads, V - 1);
+        const int v = min(v0 + (int)threadIdx.x + u * NT, V - 1);
         ro[u] = it > 0 ? B.r[v] : pnew[v];
         po[u] = it > 0 ? pold[v] : make_float3(0.f, 0.f, 0.f);
     }
@@ -786,7 +826,7 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
     }
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
-        const int i = threadIdx.x + u * kTmaThreads;
+        const int i = threadIdx.x + u * NT;
         float3 pv = make_float3(0.f, 0.f, 0.f);
         float3 qv = make_float3(0.f, 0.f, 0.f);
         if (i < nv) {
@@ -806,8 +846,10 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
             }
             if (it > 0) pnew[v] = pv;
         }
-        sp[so[u]] = f4of(pv);
-        sq[so[u]] = f4of(qv);
+        if (i < kTileV) {
+            sp[so[u]] = f4of(pv);
+            sq[so[u]] = f4of(qv);
+        }
     }
 #pragma unroll
     for (int u = 0; u < NH; ++u) {
@@ -820,15 +862,15 @@ __global__ void __launch_bounds__(kTmaThreads, 4) k_cg_matvec_tma(int it, TmaTil
             sp[hs[u]] = f4of(pv);
         }
     }
-    for (int h = threadIdx.x + NH * kTmaThreads; h < hcap; h += blockDim.x) {   // rare: large halos
+    for (int h = threadIdx.x + NH * NT; h < hcap; h += blockDim.x) {   // rare: large halos
         const int v = T.hpad[(size_t)t * hcap + h];
         if (v >= 0) sp[T.hslot[(size_t)t * hcap + h]] = f4of(halo_p(it, v, beta, B.r, pold, pnew, wv));
     }
     __syncthreads();
-    acc[0] += tma_tile_colors(bars, stages, sp, sq, sb, T);
+    acc[0] += tma_tile_colors<NT, LOOP>(bars, stages, sp, sq, sb, T);
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
-        const int i = threadIdx.x + u * kTmaThreads;
+        const int i = threadIdx.x + u * NT;
         if (i < nv) B.q[v0 + i] = wo[u] > 0.f ? xyz(sq[so[u]]) : make_float3(0.f, 0.f, 0.f);
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
@@ -858,7 +900,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
     __shared__ int4 sb[kMaxColors];
     if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == kTmaThreads - 32) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
@@ -937,10 +979,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0 && c + kTmaStages < T.ncol) {
-            fence_proxy_async();
-            tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
-        }
+        // re-arm the stage (write-after-read ordered by the barrier; see tma_tile_colors)
+        if (threadIdx.x == kTmaThreads - 32 && c + kTmaStages < T.ncol) tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
     }
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i, si = T.vslot[(size_t)t * kTileV + i];
