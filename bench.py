@@ -225,7 +225,7 @@ def run_ours(a):
         api.dxpbd_profile(sc, True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    launches, cg_iters = 0, 0
+    launches, cg_iters, cg_mv = 0, 0, 0
     torch.cuda.synchronize()
     par.barrier()
     for i in range(a.steps):
@@ -235,6 +235,7 @@ def run_ours(a):
         st = api.dxpbd_stats(sc)
         launches += int(st["fwd_launches"] + st["bwd_launches"]) + 1
         cg_iters += int(st["cg_iters_total"])
+        cg_mv += int(st["cg_matvecs"])
     torch.cuda.synchronize()
     par.barrier()
     clk = clocks.stop()
@@ -286,7 +287,7 @@ def run_ours(a):
         # PCG kernels: the host polls convergence every 8 iterations, so launches after convergence
         # exit at once; only working launches (= PCG iterations) count, their time stays in ms
         # (conservative)
-        work = cg_iters if dom in ("cg_dist", "cg_update") and cg_iters > 0 else cnt
+        work = {"cg_dist": cg_mv, "cg_update": cg_iters}.get(dom, 0) or cnt
         avg_ms = ms / work
         ach = (b / (avg_ms / 1e3)) / 1e9 if b else None
         share = ms / sum(v[0] for v in ktimes.values())

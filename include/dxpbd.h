@@ -148,7 +148,9 @@ int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out
  *  0: total PCG iterations of the last backward, 1: max PCG iterations of one solve,
  *  2: kernel launches of the last forward, 3: of the last backward, 4: substeps solved,
  *  5: worst final relative residual, 6: last loss, 7: foreign constraint entries (tiled PCG),
- *  8: halo slots summed over tiles, 9: E, 10: V, 11: T, 12: vertex tiles, 13: TMA path on. */
+ *  8: halo slots summed over tiles, 9: E, 10: V, 11: T, 12: vertex tiles, 13: TMA path on,
+ *  14: PCG matvec launches of the last backward that did work (iterations, plus one start
+ *      matvec per solve for the single-reduction PCG). */
 int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
 
 /* Kernel classes timed by the opt-in event profiler (dxpbd_profile / dxpbd_kernel_times). */

@@ -199,6 +199,7 @@ static void bank_group(int32_t *idx, int n, int NB, int G, F banks) {
 // cpair (slot pairs in layout order), the permuted foreign segments with fpair / fposv.
 struct TileLayoutScratch {
     std::vector<int> deg, moff, memb, cnt, order, slot_of, used;
+    std::vector<uint32_t> gmask;
     std::vector<int32_t> ids;
 };
 
@@ -243,11 +244,15 @@ static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<i
         std::stable_sort(w.order.begin(), w.order.end(),
                          [&](int x, int y) { return w.moff[x + 1] - w.moff[x] > w.moff[y + 1] - w.moff[y]; });
         w.used.assign(NB, 0);
+        // each aligned group of 8 consecutive local indices (one quarter-warp of the vertex / halo
+        // phases, which access slot(i) for i = thread + k * blockDim) takes 8 distinct bank groups
+        w.gmask.assign((hi - lo + 7) / 8 + 1, 0);
         for (int l : w.order) {
             int best = -1;
             long bc = 0;
+            const int gi = (l - lo) / 8;
             for (int b = 0; b < NB; ++b) {
-                if (w.used[b] >= cap) continue;
+                if (w.used[b] >= cap || ((w.gmask[gi] >> b) & 1)) continue;
                 long c = 0;
                 for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) c += w.cnt[(size_t)w.memb[m] * NB + b];
                 c = c * 1024 + w.used[b];
@@ -255,6 +260,7 @@ static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<i
             }
             w.slot_of[l] = base + NB * w.used[best] + best;
             w.used[best]++;
+            w.gmask[gi] |= 1u << best;
             for (int m = w.moff[l]; m < w.moff[l + 1]; ++m) w.cnt[(size_t)w.memb[m] * NB + best]++;
         }
     }
@@ -464,7 +470,6 @@ struct dxpbd_scene {
     // CG-local tile structure (TMA-staged matvec, QF = 1)
     bool use_tma = false;
     int capm = 0, capf = 0;   // TMA stage capacities (own / staged foreign entries per segment)
-    int mv_variant = 0;       // TMA matvec variant: 0 = 256 x 4/SM one entry per pass, 1 = two-entry ILP, 2 = 320 x 3/SM
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hpad, d_fpos;
@@ -502,6 +507,12 @@ struct dxpbd_scene {
     // backward
     DBuf<double4> xr;
     DBuf<float3> ax, rhs, y, r, p, q, p1, uprev, u0;   // packed 12 B vector fields
+    DBuf<float3> uprev2;                               // u_{n+3} (quadratic warm start, warm_order 2)
+    int warm_order = 2;                                // PCG warm start: extrapolation order (1 or 2; TMA path)
+    DBuf<float3> r1, s1, w1;                           // single-reduction PCG ping-pong partners
+    bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
+                                                       // measured 10 % slower than matvec + update)
+    int cgcg_minb = 4;                                 // its resident CTAs per SM (launch bounds)
     int qf = 0;   // Q format: 0 = sym6 SoA, 1 = iso+rank1 float4 (K = 1 with PD projection)
     DBuf<float> Qd, ed, Qc, ec;
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
@@ -688,12 +699,24 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     const int maxit = s->cg_max_iter;
     CGState cs{s->cg_sc.p, s->cg_sc.p + (size_t)(maxit + 1) * 4, s->cg_tol * s->cg_tol};
     const float *xw = s->inv_mass.p;
-    LAUNCH(DXPBD_K_CG_INIT, k_cg_start<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->r.p, s->p.p, xw, cs));
-    int launches = 1;
     const float *Qc = s->NC ? s->Qc.p : nullptr;
     CGBufs bufs{s->ax.p, s->r.p, s->p.p, s->p1.p, s->q.p, nullptr};
     TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
     TmaTiles tt = s->tma_tiles();
+    // single-reduction PCG (kernels.cuh k_cgcg_tma): cloth-only TMA path
+    const bool cgcg = s->use_tma && !s->T && s->cgcg;
+    CGCGBufs cb{s->ax.p, s->p.p, {s->r.p, s->r1.p}, {s->p1.p, s->s1.p}, {s->q.p, s->w1.p}, s->rhs.p};
+    auto cgcg_launch = [&](int i) {
+        if (s->cgcg_minb == 3)
+            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<256, 3><<<s->ntiles, 256, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
+        else
+            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<256, 4><<<s->ntiles, 256, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
+    };
+    if (cgcg)
+        cgcg_launch(-1);
+    else
+        LAUNCH(DXPBD_K_CG_INIT, k_cg_start<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->r.p, s->p.p, xw, cs));
+    int launches = 1;
     int it = 0;
     const int chunk = 8;
     iters_out = -1;
@@ -701,12 +724,13 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         for (; it < end; ++it) {
-            if (s->use_tma && s->mv_variant == 1)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4, 1><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
-            else if (s->use_tma && s->mv_variant == 2)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<320, 3, 0><<<s->ntiles, 320, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
-            else if (s->use_tma)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4, 0><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
+            if (cgcg) {
+                cgcg_launch(it);
+                ++launches;
+                continue;
+            }
+            if (s->use_tma)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             else
@@ -975,10 +999,11 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 s->d_fQ.alloc((size_t)std::max<int64_t>(NF, 1));
                 s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->capf);
                 s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->capf);
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<320, 3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                if (const char *ev = getenv("DXPBD_MV")) s->mv_variant = atoi(ev);
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                if (const char *ev = getenv("DXPBD_CGCG_MINB")) s->cgcg_minb = atoi(ev);
+                if (const char *ev = getenv("DXPBD_CG")) s->cgcg = std::string(ev) == "cgcg";
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
                 DX_CHECK_CUDA(cudaStreamSynchronize(st));
             }
@@ -1155,7 +1180,11 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     if (s->xr.n < (size_t)V) s->xr.alloc(V);
     auto ensure4 = [&](DBuf<float3> &b) { if (b.n < (size_t)V) b.alloc(V); };
     ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
+    if (s->use_tma && !s->T && s->cgcg) { ensure4(s->r1); ensure4(s->s1); ensure4(s->w1); }
     ensure4(s->uprev); ensure4(s->u0);
+    if (const char *ev = getenv("DXPBD_WARM")) s->warm_order = atoi(ev) == 2 ? 2 : 1;
+    if (s->warm_order == 2 && s->use_tma) ensure4(s->uprev2);
+    const bool warm2 = s->warm_order == 2 && s->use_tma;
     if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);
     const bool g_comp = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
     const bool g_forces = (s->grad_flags >> DXPBD_GRAD_FORCES) & 1;
@@ -1221,6 +1250,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     DX_CHECK_CUDA(cudaMemsetAsync(s->y.p, 0, sizeof(float3) * V, st));
     DX_CHECK_CUDA(cudaMemsetAsync(s->ax.p, 0, sizeof(float3) * V, st));   // ax holds u
     DX_CHECK_CUDA(cudaMemsetAsync(s->uprev.p, 0, sizeof(float3) * V, st));
+    if (warm2) DX_CHECK_CUDA(cudaMemsetAsync(s->uprev2.p, 0, sizeof(float3) * V, st));
     int last_key_state = -1;
     for (int n = 0; n <= N; ++n) if (key_of[n] >= 0) last_key_state = n;
     int launches = num_keys + 2, total_it = 0, max_it = 0;
@@ -1239,7 +1269,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             TmaTiles tt = s->tma_tiles();
             if (s->use_tma)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_rhs_smem, st>>>(
-                    tt, V, Qc, s->ax.p, s->uprev.p, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
+                    tt, V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
                     s->r.p, s->u0.p));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tiled<1><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->uprev.p,
@@ -1261,7 +1291,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         // rotate: the PCG iterates on the warm start u0; afterwards ax = u_n, uprev = u_{n+1}
         std::swap(s->ax.p, s->u0.p);      // ax <- u0 (solution buffer), u0 <- u_{n+1}
         launches += pcg_solve(s, st, iters, rel);   // u_n into s->ax
-        std::swap(s->uprev.p, s->u0.p);   // uprev <- u_{n+1}, u0 <- u_{n+2} (free)
+        if (warm2) std::swap(s->uprev2.p, s->uprev.p);   // uprev2 <- u_{n+2}
+        std::swap(s->uprev.p, s->u0.p);   // uprev <- u_{n+1}, u0 <- u_{n+2} or u_{n+3} (free)
         total_it += iters;
         max_it = std::max(max_it, iters);
         worst = std::max(worst, rel);
@@ -1293,6 +1324,9 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     phi = s->h_scal[0];
     if (loss_out) *loss_out = (float)phi;
     s->stats[0] = total_it;
+    // PCG matvec launches that did work: one per iteration (+ the start matvec per solve for the
+    // single-reduction form)
+    s->stats[14] = total_it + ((s->use_tma && !s->T && s->cgcg) ? solves : 0);
     s->stats[1] = max_it;
     s->stats[3] = launches;
     s->stats[4] = solves;

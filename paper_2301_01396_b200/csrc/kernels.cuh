@@ -719,7 +719,7 @@ DX_INLINE float mv_entries(const StageView &S, int i0, int i1, int n, int nm, in
 }
 
 // Walk all colors of tile t: sq += A_dist sp; returns sp.(A_dist sp) over own constraints.
-template <int NT, int LOOP>
+template <int NT>
 DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const float4 *sp, float4 *sq, const int4 *sb,
                                 const TmaTiles &T) {
     float dotacc = 0.f;
@@ -732,21 +732,9 @@ DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const flo
         const int4 g = sb[c];
         const int nm = g.y - g.x, nmp = (nm + 7) & ~7, n = nmp + (g.w - g.z);
         const int off = g.x & 3, foff = g.z & 3;
-        if (LOOP == 0) {
-            for (int i = threadIdx.x; i < n; i += NT) {
-                if (i >= nm && i < nmp) continue;
-                dotacc += mv_entries<1>(S, i, 0, n, nm, nmp, off, foff, g.z, T, sp, sq);
-            }
-        } else {
-            // entries i and i + NT per thread; warps that own a second entry process both with all
-            // shared loads first (entries of one color are vertex-disjoint, R1: no aliasing)
-            for (int base = 0; base < n; base += 2 * NT) {
-                const int i0 = base + threadIdx.x, i1 = i0 + NT;
-                const bool two = __any_sync(0xffffffffu, i1 < n);   // uniform loop: every lane votes
-                if (i0 >= n || (i0 >= nm && i0 < nmp)) continue;
-                dotacc += two ? mv_entries<2>(S, i0, i1, n, nm, nmp, off, foff, g.z, T, sp, sq)
-                              : mv_entries<1>(S, i0, i1, n, nm, nmp, off, foff, g.z, T, sp, sq);
-            }
+        for (int i = threadIdx.x; i < n; i += NT) {
+            if (i >= nm && i < nmp) continue;
+            dotacc += mv_entries<1>(S, i, 0, n, nm, nmp, off, foff, g.z, T, sp, sq);
         }
         __syncthreads();
         // re-arm this stage for color c + kTmaStages: all reads of it completed before the barrier
@@ -762,7 +750,7 @@ DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const flo
 // halo ids, slots, inverse masses); round trip 2 the vector values and the first bulk copies.
 // NT threads per CTA (a color's combined list is ~1.1 x kTileV / 2 entries: NT = 320 processes it
 // in one pass), MINB resident CTAs per SM.
-template <int NT, int MINB, int LOOP>
+template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, int V,
                                                                   const float *__restrict__ Qc, CGBufs B,
                                                                   const float *__restrict__ wv, CGState s) {
@@ -867,7 +855,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
         if (v >= 0) sp[T.hslot[(size_t)t * hcap + h]] = f4of(halo_p(it, v, beta, B.r, pold, pnew, wv));
     }
     __syncthreads();
-    acc[0] += tma_tile_colors<NT, LOOP>(bars, stages, sp, sq, sb, T);
+    acc[0] += tma_tile_colors<NT>(bars, stages, sp, sq, sb, T);
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
         const int i = threadIdx.x + u * NT;
@@ -876,10 +864,189 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Single-reduction PCG (Chronopoulos-Gear form of preconditioned CG; same iterates as
+// k_cg_matvec_tma + k_cg_update4 in exact arithmetic), one fused kernel per iteration.  With
+// M the mass matrix, W = M^-1 the Jacobi preconditioner and A = M + Q_c + A_dist:
+//   kernel -1:  u_0 = W r_0, w_0 = A u_0;  slot 0 = (delta_0 = u_0.w_0, gamma_0 = r_0.u_0, r_0.r_0), |b|^2
+//   kernel i:   beta_i = gamma_i / gamma_{i-1} (0 for i = 0),
+//               alpha_i = gamma_i / (delta_i - beta_i gamma_i / alpha_{i-1})  (gamma_0 / delta_0),
+//               p_i = u_i + beta_i p_{i-1},  s_i = w_i + beta_i s_{i-1}   (s_i = A p_i),
+//               x += alpha_i p_i,  r_{i+1} = r_i - alpha_i s_i,  u_{i+1} = W r_{i+1},
+//               w_{i+1} = A u_{i+1} (tile matvec),  slot i+1 = (delta, gamma, rr);  alpha_i -> slot i.
+// M u_{i+1} = r_{i+1} on free vertices, so the vertex term of w needs no extra read.  Halo values
+// u_{i+1} are recomputed from the neighbours' r_i, w_i, s_{i-1} (ping-pong buffers: the owners
+// write r_{i+1}, w_{i+1}, s_i in the same launch).  Pinned vertices: u = p = s = r = w = 0.
+struct CGCGBufs {
+    float3 *x, *p;
+    float3 *r[2], *s[2], *w[2];
+    const float3 *b;
+};
+
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V, const float *__restrict__ Qc,
+                                                       CGCGBufs B, const float *__restrict__ wv, CGState s) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    unsigned char *stages = smem_raw + 64;
+    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.capm, T.capf) * kTmaStages);
+    float4 *sp = sq + kTileV;
+    const int hcap = T.hcap;
+    const int t = blockIdx.x;
+    const int v0 = t * kTileV;
+    const int nv = min(kTileV, V - v0);
+    __shared__ int4 sb[kMaxColors];
+    constexpr int NO = (kTileV + NT - 1) / NT, NH = (512 + NT - 1) / NT;
+    // ---- round trip 1
+    const bool done = i >= 0 && cg_done(s, i + 1);
+    if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
+    float wo[NO];
+    int so[NO];
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int l = threadIdx.x + u * NT;
+        wo[u] = wv[min(v0 + l, V - 1)];
+        so[u] = l < kTileV ? T.vslot[(size_t)t * kTileV + l] : 0;
+    }
+    int hv[NH], hs[NH];
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        const int h = threadIdx.x + u * NT;
+        hv[u] = h < hcap ? T.hpad[(size_t)t * hcap + h] : -1;
+        hs[u] = h < hcap ? T.hslot[(size_t)t * hcap + h] : 0;
+    }
+    if (done) return;
+    __syncthreads();
+    if (threadIdx.x == NT - 32) {
+        for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
+        fence_mbar_init();
+        const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
+        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
+    }
+    // ---- scalars of this iteration (double, from the previous launches' reductions)
+    double al = 0.0, be = 0.0;
+    if (i >= 0) {
+        const double gi = s.sc[i * 4 + 1], di = s.sc[i * 4 + 0];
+        if (i == 0) {
+            al = di > 0.0 ? gi / di : 0.0;
+        } else {
+            const double gp = s.sc[(i - 1) * 4 + 1], ap = s.sc[(i - 1) * 4 + 3];
+            be = gp > 0.0 ? gi / gp : 0.0;
+            const double den = ap != 0.0 ? di - be * gi / ap : di;
+            al = den > 0.0 ? gi / den : 0.0;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) s.sc[i * 4 + 3] = al;
+    }
+    const float alpha = (float)al, beta = (float)be;
+    const float3 z3 = make_float3(0.f, 0.f, 0.f);
+    const float3 *__restrict__ rin = B.r[i >= 0 ? (i & 1) : 0];
+    float3 *__restrict__ rout = B.r[(i + 1) & 1];
+    const float3 *__restrict__ win = B.w[i >= 0 ? (i & 1) : 1];
+    float3 *__restrict__ wout = B.w[(i + 1) & 1];
+    const float3 *__restrict__ sin_ = B.s[(i + 1) & 1];   // s_{i-1}
+    float3 *__restrict__ sout = B.s[i >= 0 ? (i & 1) : 0];
+    // ---- round trip 2: own r_i, w_i, s_{i-1}, p_{i-1}, x (and b for kernel -1); halo r_i, w_i, s_{i-1}
+    float acc[3] = {0.f, 0.f, 0.f};   // delta, gamma, rr of slot i + 1
+    float bacc = 0.f;
+    float3 ro[NO], wq[NO], so_[NO], po[NO], xo[NO];
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int v = min(v0 + (int)threadIdx.x + u * NT, V - 1);
+        ro[u] = rin[v];
+        if (i >= 0) {
+            wq[u] = win[v];
+            so_[u] = i > 0 ? sin_[v] : z3;
+            po[u] = i > 0 ? B.p[v] : z3;
+            xo[u] = B.x[v];
+        } else {
+            wq[u] = B.b[v];   // kernel -1: |b|^2
+        }
+    }
+    float hw[NH];
+    float3 hr[NH], hwq[NH], hsv[NH];
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        const int v = max(hv[u], 0);
+        hw[u] = wv[v];
+        hr[u] = rin[v];
+        hwq[u] = i >= 0 ? win[v] : z3;
+        hsv[u] = i > 0 ? sin_[v] : z3;
+    }
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int l = threadIdx.x + u * NT;
+        float3 un = z3, wn = z3;
+        if (l < nv) {
+            const int v = v0 + l;
+            const float w = wo[u];
+            float3 rn = z3;
+            if (i >= 0) {
+                float3 pv = z3, sv = wq[u] + beta * so_[u];
+                if (w > 0.f) pv = w * ro[u] + beta * po[u];
+                B.p[v] = pv;
+                sout[v] = sv;
+                B.x[v] = xo[u] + alpha * pv;
+                if (w > 0.f) rn = ro[u] - alpha * sv;
+                rout[v] = rn;
+            } else {
+                if (w > 0.f) {
+                    rn = ro[u];
+                    bacc += dot3(wq[u], wq[u]);
+                }
+            }
+            if (w > 0.f) {
+                un = w * rn;
+                wn = rn;
+                if (Qc) {
+                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                                  Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                    wn = wn + sym3_mul(A, un);
+                }
+                acc[0] += dot3(un, wn);
+                acc[1] += dot3(rn, un);
+                acc[2] += dot3(rn, rn);
+            }
+        }
+        if (l < kTileV) {
+            sp[so[u]] = f4of(un);
+            sq[so[u]] = f4of(wn);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < NH; ++u) {
+        if (hv[u] >= 0) {
+            float3 un = z3;
+            if (hw[u] > 0.f) un = hw[u] * (i >= 0 ? hr[u] - alpha * (hwq[u] + beta * hsv[u]) : hr[u]);
+            sp[hs[u]] = f4of(un);
+        }
+    }
+    for (int h = threadIdx.x + NH * NT; h < hcap; h += blockDim.x) {   // rare: large halos
+        const int v = T.hpad[(size_t)t * hcap + h];
+        if (v < 0) continue;
+        const float w = wv[v];
+        float3 un = z3;
+        if (w > 0.f) un = w * (i >= 0 ? rin[v] - alpha * (win[v] + beta * (i > 0 ? sin_[v] : z3)) : rin[v]);
+        sp[T.hslot[(size_t)t * hcap + h]] = f4of(un);
+    }
+    __syncthreads();
+    acc[0] += tma_tile_colors<NT>(bars, stages, sp, sq, sb, T);
+#pragma unroll
+    for (int u = 0; u < NO; ++u) {
+        const int l = threadIdx.x + u * NT;
+        if (l < nv) wout[v0 + l] = wo[u] > 0.f ? xyz(sq[so[u]]) : z3;
+    }
+    block_reduce_add<3>(acc, s.sc + (i + 1) * 4);
+    if (i < 0) {
+        float bb[1] = {bacc};
+        block_reduce_add<1>(bb, s.bnorm2);
+    }
+}
+
 // rhs (warm start): b = M u - Q_n y + dphi, r0 = b - A_n (u + du); A_dist applied tile-locally
 // with the same staging / slot layout as the matvec.
 __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, const float *__restrict__ Qc,
                                                             const float3 *__restrict__ u, const float3 *__restrict__ uprev,
+                                                            const float3 *__restrict__ uprev2,
                                                             const float3 *__restrict__ y,
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                             const float *__restrict__ weights, const float *__restrict__ wv,
@@ -912,7 +1079,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
             const float w = wv[v];
             yv = f3(y[v]);
             const float3 uv = f3(u[v]);
-            const float3 dv = uv - f3(uprev[v]);          // warm start u0 = u + (u - uprev)
+            // warm start u0 = u + dv: linear 2u_{n+1} - u_{n+2}, or quadratic 3u_{n+1} - 3u_{n+2} + u_{n+3}
+            const float3 dv = uprev2 ? 2.f * uv - 3.f * f3(uprev[v]) + f3(uprev2[v]) : uv - f3(uprev[v]);
             const float3 u0 = uv + dv;
             zv = yv + u0;
             u0out[v] = w > 0.f ? u0 : make_float3(0.f, 0.f, 0.f);
@@ -945,7 +1113,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
         const int v = T.hpad[(size_t)t * hcap + h];
         if (v < 0) continue;
         const float3 uh = f3(u[v]);
-        const float3 yv = f3(y[v]), zv = yv + uh + (uh - f3(uprev[v]));
+        const float3 dh = uprev2 ? 2.f * uh - 3.f * f3(uprev[v]) + f3(uprev2[v]) : uh - f3(uprev[v]);
+        const float3 yv = f3(y[v]), zv = yv + uh + dh;
         const int sh = T.hslot[(size_t)t * hcap + h];
         sy[sh] = f4of(yv);
         sz[sh] = f4of(zv);
