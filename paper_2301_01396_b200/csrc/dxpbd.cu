@@ -509,6 +509,8 @@ struct dxpbd_scene {
     DBuf<float3> ax, rhs, y, r, p, q, p1, uprev, u0;   // packed 12 B vector fields
     DBuf<float3> uprev2;                               // u_{n+3} (quadratic warm start, warm_order 2)
     int warm_order = 2;                                // PCG warm start: extrapolation order (1 or 2; TMA path)
+    int nb = 1;                                        // K = 1 forward projection: constraints per thread
+    int nb_rep = 2;                                    // K = 1 replay: constraints per thread
     DBuf<float3> r1, s1, w1;                           // single-reduction PCG ping-pong partners
     bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
                                                        // measured 10 % slower than matvec + update)
@@ -595,8 +597,10 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         for (int c = 0; c < s->n_dist_colors; ++c) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
-            if (!rd && !wr)
-                LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo));
+            if (!rd && !wr && s->nb == 2)
+                LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project1<2><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, xo));
+            else if (!rd && !wr)
+                LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project1<1><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, xo));
             else if (!rd && wr)
                 LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project<false, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->lam_d.p, xo));
             else if (rd && wr)
@@ -649,10 +653,14 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
             float *eo = want_e ? s->ed.p : nullptr;
-            if (first && last && s->qf == 1)
-                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true, 1><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x,
-                                                                                                   s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p,
-                                                                                                   s->use_tma ? s->d_tpos.p : nullptr));
+            if (first && last && s->qf == 1 && s->nb_rep == 2)
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay1<2><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p));
+            else if (first && last && s->qf == 1)
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay1<1><<<nblk(cnt), kBlock, 0, st>>>(
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p));
             else if (first && last)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else if (first)
@@ -838,6 +846,10 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     s->cg_tol = d->cg_tol > 0 ? d->cg_tol : 1e-6f;
     s->cg_max_iter = d->cg_max_iter > 0 ? d->cg_max_iter : 500;
     s->qf = (s->iterations == 1 && s->pd) ? 1 : 0;
+    // A/B switches for measurements (defaults are the measured-best settings)
+    if (const char *ev = getenv("DXPBD_WARM")) s->warm_order = atoi(ev) == 2 ? 2 : 1;
+    if (const char *ev = getenv("DXPBD_NB")) s->nb = atoi(ev) == 2 ? 2 : 1;
+    if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
 
     cudaStream_t st = 0;
 
@@ -1182,7 +1194,6 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
     if (s->use_tma && !s->T && s->cgcg) { ensure4(s->r1); ensure4(s->s1); ensure4(s->w1); }
     ensure4(s->uprev); ensure4(s->u0);
-    if (const char *ev = getenv("DXPBD_WARM")) s->warm_order = atoi(ev) == 2 ? 2 : 1;
     if (s->warm_order == 2 && s->use_tma) ensure4(s->uprev2);
     const bool warm2 = s->warm_order == 2 && s->use_tma;
     if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);

@@ -139,6 +139,98 @@ DX_INLINE float3 qmul_iso_rank1(float4 Q, float3 d) {
     return make_float3(c * d.x + ud * u.x, c * d.y + ud * u.y, c * d.z + ud * u.z);
 }
 
+// K = 1 forward projection, NB constraints per thread: all index / endpoint loads are issued before
+// any arithmetic (memory-level parallelism; the constraints of one color are vertex-disjoint, so
+// a thread's loads never alias its stores).  Same arithmetic as k_dist_project<false, false>.
+template <int NB>
+__global__ void __launch_bounds__(kBlock) k_dist_project1(int begin, int count, const int2 *__restrict__ idx,
+                                                          const float *__restrict__ rest,
+                                                          const float *__restrict__ alpha, float inv_dt2,
+                                                          double4 *__restrict__ x) {
+    const int t0 = blockIdx.x * blockDim.x * NB + threadIdx.x;
+    int2 e[NB];
+    float rs[NB], al[NB];
+    double4 pa[NB], pb[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int t = t0 + k * blockDim.x;
+        const int j = begin + min(t, count - 1);
+        e[k] = idx[j];
+        rs[k] = rest[j];
+        al[k] = alpha[j];
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        pa[k] = x[e[k].x];
+        pb[k] = x[e[k].y];
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        if (t0 + k * (int)blockDim.x >= count) continue;
+        DistCore o;
+        if (!dist_core(pa[k], pb[k], rs[k], rmul(al[k], inv_dt2), 0.f, o)) continue;
+        dist_apply(pa[k], pb[k], o);
+        x[e[k].x] = pa[k];
+        x[e[k].y] = pb[k];
+    }
+}
+
+// K = 1 replay with the PD projection (QF = 1), NB constraints per thread as above: regenerates the
+// iterate, stores the closed-form block Q_j at its TMA-layout position tpos[j] (and the foreign copy),
+// and the compliance control vector e_j = t n, t = -dl / (dt^2 J) (the general replay with
+// lambda_0 = T = 0).  Same arithmetic as k_dist_replay<true, true, 1>.
+template <int NB>
+__global__ void __launch_bounds__(kBlock) k_dist_replay1(int begin, int count, int E, const int2 *__restrict__ idx,
+                                                         const float *__restrict__ rest,
+                                                         const float *__restrict__ alpha, float inv_dt2,
+                                                         float4 *__restrict__ Q4, float *__restrict__ eout,
+                                                         double4 *__restrict__ x, const int *__restrict__ tpos,
+                                                         const int *__restrict__ fpos, float4 *__restrict__ fQ) {
+    const int t0 = blockIdx.x * blockDim.x * NB + threadIdx.x;
+    int2 e[NB];
+    float rs[NB], al[NB];
+    int tp[NB], fp[NB];
+    double4 pa[NB], pb[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int t = t0 + k * blockDim.x;
+        const int j = begin + min(t, count - 1);
+        e[k] = idx[j];
+        rs[k] = rest[j];
+        al[k] = alpha[j];
+        tp[k] = tpos ? tpos[j] : j;
+        fp[k] = fpos ? fpos[j] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        pa[k] = x[e[k].x];
+        pb[k] = x[e[k].y];
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int t = t0 + k * blockDim.x;
+        if (t >= count) continue;
+        const int j = begin + t;
+        const float at = rmul(al[k], inv_dt2);
+        DistCore o;
+        const bool ok = dist_core(pa[k], pb[k], rs[k], at, 0.f, o);
+        float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 ec = make_float3(0.f, 0.f, 0.f);
+        if (ok) {
+            q4 = qpack_iso_rank1(o.n, o.dl, (float)(1.0 / o.len), o.J);
+            const float iJ = 1.f / o.J;
+            const float tt = (-(0.f + o.dl) * inv_dt2 - at * 0.f) * iJ;
+            ec = ec + tt * o.n;
+            dist_apply(pa[k], pb[k], o);
+            x[e[k].x] = pa[k];
+            x[e[k].y] = pb[k];
+        }
+        Q4[tp[k]] = q4;
+        if (fp[k] >= 0) fQ[fp[k]] = q4;
+        if (eout) { eout[j] = ec.x; eout[E + j] = ec.y; eout[2 * E + j] = ec.z; }
+    }
+}
+
 template <bool FIRST, bool LAST, int QF = 0>
 __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, int E, const int2 *__restrict__ idx,
                                                         const float *__restrict__ rest,
