@@ -196,7 +196,8 @@ static void bank_group(int32_t *idx, int n, int NB, int G, F banks) {
 // constraint segments, the endpoints spread evenly over the 8 groups (a linear layout folds a
 // color's lower endpoints onto half of them: Morton index parities).  Each segment is then ordered
 // into groups of 8 (one quarter-warp access phase) with distinct groups per endpoint (bank_group).  Outputs: vslot / hslot (slots), tpos (sorted position -> layout position),
-// cpair (slot pairs in layout order), the permuted foreign segments with fpair / fposv.
+// cpair (slot pairs of the combined segments), tpos / fposv (layout positions of each constraint's
+// block: in its own tile's segment and, if b lies in another tile, in that tile's segment).
 struct TileLayoutScratch {
     std::vector<int> deg, moff, memb, cnt, order, slot_of, used;
     std::vector<uint32_t> gmask;
@@ -204,9 +205,9 @@ struct TileLayoutScratch {
 };
 
 static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<int> &halo_t, int hoff_t,
-                            const int64_t *cnt, const int64_t *fc, const int2 *ab, int *fidx, uint16_t *vslot,
-                            uint16_t *hslot, int *tpos, uint32_t *cpair, uint32_t *fpair, int *fposv,
-                            TileLayoutScratch &w) {
+                            const int64_t *cnt, const int64_t *fc, const int2 *ab, const int *fidx,
+                            const int64_t *cbase, uint16_t *vslot, uint16_t *hslot, int *tpos, int *fposv,
+                            uint32_t *cpair, TileLayoutScratch &w) {
     const int nh = (int)halo_t.size(), NL = kTileV + nh, NK = 4 * nc;
     auto local = [&](int v) {
         return v / kTileV == t ? v - t * kTileV
@@ -267,23 +268,26 @@ static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<i
     for (int l = 0; l < kTileV; ++l) vslot[(size_t)t * kTileV + l] = (uint16_t)w.slot_of[l];
     for (int h = 0; h < nh; ++h) hslot[hoff_t + h] = (uint16_t)w.slot_of[kTileV + h];
     auto sl = [&](int v) { return w.slot_of[local(v)]; };
+    // combined segment of (t, c) at cbase[t * nc + c]: own constraints (ids q >= 0) and foreign
+    // entries (ids -(k2 + 1)), grouped jointly; "own" is recovered in the kernels as slot(a) < kTileV
+    auto con = [&](int32_t id) { return id >= 0 ? id : fidx[-id - 1]; };
     for (int c = 0; c < nc; ++c) {
         const size_t kk = (size_t)c * nt + t;
-        const int64_t b = cnt[kk], e = cnt[kk + 1];
-        w.ids.resize(e - b);
-        for (int64_t q = b; q < e; ++q) w.ids[q - b] = (int32_t)q;
-        bank_group(w.ids.data(), (int)(e - b), NB, NB, [&](int32_t q) { return std::make_pair(sl(ab[q].x) & (NB - 1), sl(ab[q].y) & (NB - 1)); });
-        for (int64_t i = 0; i < e - b; ++i) {
-            const int q = w.ids[i];
-            tpos[q] = (int)(b + i);
-            cpair[b + i] = (uint32_t)sl(ab[q].x) | ((uint32_t)sl(ab[q].y) << 16);
-        }
-        const int64_t fb = fc[kk], fe = fc[kk + 1];
-        bank_group(fidx + fb, (int)(fe - fb), NB, NB, [&](int32_t q) { return std::make_pair(sl(ab[q].x) & (NB - 1), sl(ab[q].y) & (NB - 1)); });
-        for (int64_t k2 = fb; k2 < fe; ++k2) {
-            const int q = fidx[k2];
-            fposv[q] = (int)k2;
-            fpair[k2] = (uint32_t)sl(ab[q].x) | ((uint32_t)sl(ab[q].y) << 16);
+        const int64_t b = cnt[kk], e = cnt[kk + 1], fb = fc[kk], fe = fc[kk + 1];
+        w.ids.clear();
+        for (int64_t q = b; q < e; ++q) w.ids.push_back((int32_t)q);
+        for (int64_t k2 = fb; k2 < fe; ++k2) w.ids.push_back((int32_t)(-(k2 + 1)));
+        bank_group(w.ids.data(), (int)w.ids.size(), NB, NB, [&](int32_t id) {
+            const int q = con(id);
+            return std::make_pair(sl(ab[q].x) & (NB - 1), sl(ab[q].y) & (NB - 1));
+        });
+        const int64_t base = cbase[(size_t)t * nc + c];
+        for (size_t i = 0; i < w.ids.size(); ++i) {
+            const int32_t id = w.ids[i];
+            const int q = con(id);
+            cpair[base + i] = (uint32_t)sl(ab[q].x) | ((uint32_t)sl(ab[q].y) << 16);
+            if (id >= 0) tpos[q] = (int)(base + i);
+            else fposv[q] = (int)(base + i);
         }
     }
 }
@@ -469,15 +473,15 @@ struct dxpbd_scene {
     DBuf<int4> d_fent;                    // foreign entries {j, a, b, 0}
     // CG-local tile structure (TMA-staged matvec, QF = 1)
     bool use_tma = false;
-    int capm = 0, capf = 0;   // TMA stage capacities (own / staged foreign entries per segment)
+    int capm = 0;             // TMA stage capacity: largest combined (own + foreign) segment
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hpad, d_fpos;
     DBuf<int4> d_tseg;
-    DBuf<uint32_t> d_cpair, d_fpair;
+    DBuf<uint32_t> d_cpair;
+    DBuf<float4> d_Qt;                  // Q blocks in the TMA layout (own at tpos[j], foreign copy at fpos[j])
     DBuf<uint16_t> d_vslot, d_hslot;   // tile-local shared-memory slots (own vertices, halo entries)
     DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
-    DBuf<float4> d_fQ;
     // tets (color-sorted, internal vertex ids)
     DBuf<int4> t_idx;
     DBuf<double> t_Dm, t_vol;
@@ -486,8 +490,7 @@ struct dxpbd_scene {
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
     TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
     TmaTiles tma_tiles() const {
-        return TmaTiles{n_dist_colors, ntiles, hcap, capm, capf, d_tseg.p, d_cpair.p, d_fpair.p, d_hpad.p,
-                        reinterpret_cast<const float4 *>(Qd.p), d_fQ.p, d_vslot.p, d_hslot.p};
+        return TmaTiles{n_dist_colors, ntiles, hcap, capm, d_tseg.p, d_cpair.p, d_hpad.p, d_Qt.p, d_vslot.p, d_hslot.p};
     }
     // colliders
     DBuf<float> sph, cap_c, cap_a, cap_r0, cap_L0, cap_Rb, cap_Lb, beta;
@@ -655,12 +658,14 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             float *eo = want_e ? s->ed.p : nullptr;
             if (first && last && s->qf == 1 && s->nb_rep == 2)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay1<2><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
-                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, reinterpret_cast<float4 *>(s->Qd.p), eo, x,
-                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p));
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
+                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p));
             else if (first && last && s->qf == 1)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay1<1><<<nblk(cnt), kBlock, 0, st>>>(
-                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, reinterpret_cast<float4 *>(s->Qd.p), eo, x,
-                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_fQ.p));
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
+                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p));
             else if (first && last)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else if (first)
@@ -956,37 +961,37 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
             }
             s->hcap = (hmax + 31) / 32 * 32;
             s->halo_total = hoff[nt];
-            // stage capacities: the largest own segment, foreign entries staged up to 128 per segment
-            int maxm = 0, maxf = 0;
-            for (size_t kk = 0; kk < nkeys; ++kk) {
-                maxm = std::max<int>(maxm, (int)(cnt[kk + 1] - cnt[kk]));
-                maxf = std::max<int>(maxf, (int)(fc[kk + 1] - fc[kk]));
-            }
-            s->capm = (maxm + 7) & ~7;
-            s->capf = (std::min(maxf, 128) + 7) & ~7;
-            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors &&
-                         tma_rhs_smem_bytes(s->hcap, s->capm, s->capf) <= 200 * 1024;
+            // combined (own + foreign) segments, tile-major: tile t's colors are contiguous
+            std::vector<int64_t> cbase((size_t)nt * nc + 1, 0);
+            int maxn = 0;
+            for (int t = 0; t < nt; ++t)
+                for (int c = 0; c < nc; ++c) {
+                    const size_t kk = (size_t)c * nt + t;
+                    const int64_t n = (cnt[kk + 1] - cnt[kk]) + (fc[kk + 1] - fc[kk]);
+                    cbase[(size_t)t * nc + c + 1] = cbase[(size_t)t * nc + c] + n;
+                    maxn = std::max<int>(maxn, (int)n);
+                }
+            s->capm = (maxn + 7) & ~7;
+            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors && cbase.back() < (int64_t)INT32_MAX &&
+                         tma_rhs_smem_bytes(s->hcap, s->capm) <= 200 * 1024;
             if (s->use_tma) {
                 const int hc = s->hcap;
                 std::vector<int> hpad((size_t)nt * hc, -1);
                 for (int t = 0; t < nt; ++t) std::copy(halo[t].begin(), halo[t].end(), hpad.begin() + (size_t)t * hc);
                 std::vector<int4> tseg((size_t)nt * nc);
-                for (int t = 0; t < nt; ++t)
-                    for (int c = 0; c < nc; ++c)
-                        tseg[(size_t)t * nc + c] = make_int4(seg[(size_t)c * (nt + 1) + t], seg[(size_t)c * (nt + 1) + t + 1],
-                                                             fseg[(size_t)c * (nt + 1) + t], fseg[(size_t)c * (nt + 1) + t + 1]);
-                const int64_t NF = fc[nkeys];
-                std::vector<uint32_t> cpair(E + 4, 0), fpair((size_t)std::max<int64_t>(NF, 1) + 4, 0);
+                for (size_t k = 0; k < (size_t)nt * nc; ++k) tseg[k] = make_int4((int)cbase[k], (int)cbase[k + 1], 0, 0);
+                const int64_t NTOT = cbase.back();
+                std::vector<uint32_t> cpair((size_t)NTOT + 4, 0);
                 std::vector<int> fposv(E, -1), tpos(E);
                 std::vector<uint16_t> vslot((size_t)nt * kTileV), hslot((size_t)nt * hc);
                 // per tile (independent, threaded): bank-balanced shared-memory slots, then
-                // conflict-free warp groups of every (color, tile) segment (tma_tile_layout)
+                // conflict-free groups of every combined (tile, color) segment (tma_tile_layout)
                 auto work = [&](int t0, int t1) {
                     TileLayoutScratch ws;
                     for (int t = t0; t < t1; ++t)
                         tma_tile_layout(t, nc, nt, hc, halo[t], t * hc, cnt.data(), fc.data(), ab_sorted.data(),
-                                        fidx.data(), vslot.data(), hslot.data(), tpos.data(), cpair.data(), fpair.data(),
-                                        fposv.data(), ws);
+                                        fidx.data(), cbase.data(), vslot.data(), hslot.data(), tpos.data(),
+                                        fposv.data(), cpair.data(), ws);
                 };
                 const int nth = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
                 std::vector<std::thread> pool;
@@ -1002,15 +1007,13 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 upload(s->d_hslot.p, hslot.data(), sizeof(uint16_t) * hslot.size(), DXPBD_MEM_HOST, st);
                 s->d_cpair.alloc(cpair.size());
                 upload(s->d_cpair.p, cpair.data(), sizeof(uint32_t) * cpair.size(), DXPBD_MEM_HOST, st);
-                s->d_fpair.alloc(fpair.size());
-                upload(s->d_fpair.p, fpair.data(), sizeof(uint32_t) * fpair.size(), DXPBD_MEM_HOST, st);
                 s->d_fpos.alloc(E);
                 upload(s->d_fpos.p, fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
                 s->d_tpos.alloc(E);
                 upload(s->d_tpos.p, tpos.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
-                s->d_fQ.alloc((size_t)std::max<int64_t>(NF, 1));
-                s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->capf);
-                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->capf);
+                s->d_Qt.alloc((size_t)NTOT + 1);
+                s->tma_smem = tma_smem_bytes(s->hcap, s->capm);
+                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));

@@ -691,147 +691,98 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
 //   16-byte access reads or writes a vertex.  Slots are assigned so that the endpoints of every
 //   color segment spread evenly over the 8 sixteen-byte bank groups, and each segment is ordered in
 //   groups of 8 entries (one quarter-warp access phase) with distinct bank groups per endpoint.
-//   cpair[j] (own constraint j, a in tile): slot(a) | slot(b) << 16 (b own or halo).
-//   fpair[k] (foreign entry k, b in tile, a outside): slot(a) | slot(b) << 16, with its own copy
-//   fQ[k] of Q_j written by the replay; foreign entries are grouped by (color, tile).
-// Per color c the own range of cpair / Q and the foreign range of fpair / fQ are contiguous:
-// thread 0 stages them with bulk async copies (cp.async.bulk -> mbarrier complete_tx) kTmaStages
-// colors ahead; all threads then work purely in shared memory (plain read-modify-write of the
-// accumulator, one barrier per color, vertex-disjoint within a color by R1).
+//   Per (tile, color) one combined segment (tile-major) holds the tile's own constraints (a in the
+//   tile; b own or halo) and its foreign entries (b in the tile, a in another tile): cpair =
+//   slot(a) | slot(b) << 16 and the block Q4 in the same order; the replay writes each block at
+//   its own-tile position and, for cross-tile constraints, a copy at the b-tile position.
+// Per color the combined segment is contiguous: one thread stages it with two bulk async copies
+// (cp.async.bulk -> mbarrier complete_tx) kTmaStages colors ahead; all threads then work purely
+// in shared memory (plain read-modify-write of the accumulator, one barrier per color,
+// vertex-disjoint within a color by R1).
 constexpr int kTmaStages = 3;
 constexpr int kTmaThreads = 256;
 constexpr int kMaxColors = 64;   // bounds table in shared memory (more colors: generic kernel)
 
 struct TmaTiles {
     int ncol, ntiles, hcap;
-    int capm, capf;                  // stage capacities: max own entries per segment, staged foreign entries
-    const int4 *tseg;                // [tile][color]: own range (b, e) of cpair / Q4, foreign range (fb, fe)
-    const uint32_t *cpair, *fpair;   // slot pairs (la | lb << 16)
+    int cap;                         // stage capacity: largest combined segment
+    const int4 *tseg;                // [tile][color]: combined segment [x, y) of cpair / Q4 (tile-major)
+    const uint32_t *cpair;           // slot pairs (la | lb << 16); la >= kTileV marks a foreign entry
     const int *hpad;                 // [tile][hcap]: halo vertex ids, -1 padded (fixed stride)
-    const float4 *Q4, *fQ;
+    const float4 *Q4;                // blocks in the same layout (the replay writes both copies)
     const uint16_t *vslot;           // [tile][kTileV]: slot of own vertex i
     const uint16_t *hslot;           // [tile][hcap]: slot of halo entry h
 };
 
-// One stage (bytes, 16-aligned parts): q[capm] | fq[capf] | cp[capm + 4, rounded] | fp[capf + 4, rounded]
-__host__ __device__ inline uint32_t tma_stage_bytes(int capm, int capf) {
-    return (uint32_t)(16 * capm + 16 * capf + ((4 * (capm + 4) + 15) & ~15) + ((4 * (capf + 4) + 15) & ~15));
+// One stage (bytes, 16-aligned parts): q[cap] | cp[cap + 4, rounded to 16 bytes]
+__host__ __device__ inline uint32_t tma_stage_bytes(int cap) {
+    return (uint32_t)(16 * cap + ((4 * (cap + 4) + 15) & ~15));
 }
 struct StageView {
-    const float4 *q, *fq;
-    const uint32_t *cp, *fp;
+    const float4 *q;
+    const uint32_t *cp;
 };
-DX_INLINE StageView stage_view(unsigned char *base, int capm, int capf) {
+DX_INLINE StageView stage_view(unsigned char *base, int cap) {
     StageView v;
     v.q = reinterpret_cast<const float4 *>(base);
-    v.fq = v.q + capm;
-    v.cp = reinterpret_cast<const uint32_t *>(v.fq + capf);
-    v.fp = v.cp + ((capm + 4 + 3) & ~3);
+    v.cp = reinterpret_cast<const uint32_t *>(v.q + cap);
     return v;
 }
 // dynamic smem of the matvec: [bars 64][stages][sq float4 kTileV][sp float4 kTileV + hcap]
-__host__ __device__ inline size_t tma_smem_bytes(int hcap, int capm, int capf) {
-    return 64 + (size_t)tma_stage_bytes(capm, capf) * kTmaStages + 16 * (size_t)kTileV + 16 * (size_t)(kTileV + hcap);
+__host__ __device__ inline size_t tma_smem_bytes(int hcap, int cap) {
+    return 64 + (size_t)tma_stage_bytes(cap) * kTmaStages + 16 * (size_t)kTileV + 16 * (size_t)(kTileV + hcap);
 }
 // rhs: [bars][stages][sqb, sqr float4 kTileV][sy, sz float4 kTileV + hcap]
-__host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap, int capm, int capf) {
-    return 64 + (size_t)tma_stage_bytes(capm, capf) * kTmaStages + 32 * (size_t)kTileV + 32 * (size_t)(kTileV + hcap);
+__host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap, int cap) {
+    return 64 + (size_t)tma_stage_bytes(cap) * kTmaStages + 32 * (size_t)kTileV + 32 * (size_t)(kTileV + hcap);
 }
 
 DX_INLINE void tma_issue(uint64_t *bar, unsigned char *stage, int4 g, const TmaTiles &T) {
-    const int b = g.x, e = g.y, fb = g.z, nf = min(g.w - g.z, T.capf);
-    uint32_t tot = 0;
-    size_t c0 = 0, c1 = 0, f0 = 0, f1 = 0;
-    if (e > b) {
-        c0 = ((size_t)b * 4) & ~(size_t)15;
-        c1 = ((size_t)e * 4 + 15) & ~(size_t)15;
-        tot += (uint32_t)(c1 - c0) + (uint32_t)(e - b) * 16u;
+    const int b = g.x, e = g.y;
+    if (e <= b) {   // empty segment: complete the phase without a transfer
+        mbar_expect_tx(bar, 0);
+        return;
     }
-    if (nf > 0) {
-        f0 = ((size_t)fb * 4) & ~(size_t)15;
-        f1 = ((size_t)(fb + nf) * 4 + 15) & ~(size_t)15;
-        tot += (uint32_t)(f1 - f0) + (uint32_t)nf * 16u;
-    }
-    mbar_expect_tx(bar, tot);
-    const StageView S = stage_view(stage, T.capm, T.capf);
-    if (e > b) {
-        bulk_g2s((void *)S.cp, reinterpret_cast<const char *>(T.cpair) + c0, (uint32_t)(c1 - c0), bar);
-        bulk_g2s((void *)S.q, T.Q4 + b, (uint32_t)(e - b) * 16u, bar);
-    }
-    if (nf > 0) {
-        bulk_g2s((void *)S.fp, reinterpret_cast<const char *>(T.fpair) + f0, (uint32_t)(f1 - f0), bar);
-        bulk_g2s((void *)S.fq, T.fQ + fb, (uint32_t)nf * 16u, bar);
-    }
+    const size_t c0 = ((size_t)b * 4) & ~(size_t)15, c1 = ((size_t)e * 4 + 15) & ~(size_t)15;
+    mbar_expect_tx(bar, (uint32_t)(c1 - c0) + (uint32_t)(e - b) * 16u);
+    const StageView S = stage_view(stage, T.cap);
+    bulk_g2s((void *)S.cp, reinterpret_cast<const char *>(T.cpair) + c0, (uint32_t)(c1 - c0), bar);
+    bulk_g2s((void *)S.q, T.Q4 + b, (uint32_t)(e - b) * 16u, bar);
 }
 
-// Entry i of a color's combined list: own constraints [0, nm), padding up to nmp (a multiple of 8,
-// so foreign entries start on a quarter-warp boundary as the host grouped them), then foreign
-// entries (staged up to capf; the rest read from global memory by a cold path).
-struct TItem {
-    uint32_t pr;
-    float4 q;
-};
-__device__ __noinline__ TItem titem_global(const TmaTiles &T, int k) { return TItem{T.fpair[k], T.fQ[k]}; }
-DX_INLINE TItem titem(const StageView &S, int i, int nm, int nmp, int off, int foff, int fb, const TmaTiles &T) {
-    if (i < nm) return TItem{S.cp[off + i], S.q[i]};
-    if (i - nmp < T.capf) return TItem{S.fp[foff + i - nmp], S.fq[i - nmp]};
-    return titem_global(T, fb + i - nmp);
-}
 DX_INLINE float3 xyz(float4 v) { return make_float3(v.x, v.y, v.z); }
 DX_INLINE float4 f4of(float3 v) { return make_float4(v.x, v.y, v.z, 0.f); }
 
-// Up to NE (1, 2) entries i0, i1 of one color per thread (i0 valid; i1 checked), all shared loads
-// before any store: entries of one color are vertex-disjoint (R1), so no aliasing.
-template <int NE>
-DX_INLINE float mv_entries(const StageView &S, int i0, int i1, int n, int nm, int nmp, int off, int foff, int fb,
-                           const TmaTiles &T, const float4 *sp, float4 *sq) {
-    const bool h1 = NE == 2 && i1 < n && !(i1 >= nm && i1 < nmp);
-    const TItem e0 = titem(S, i0, nm, nmp, off, foff, fb, T);
-    TItem e1{0u, make_float4(0.f, 0.f, 0.f, 0.f)};
-    if (h1) e1 = titem(S, i1, nm, nmp, off, foff, fb, T);
-    const int la0 = e0.pr & 0xffff, lb0 = e0.pr >> 16, la1 = e1.pr & 0xffff, lb1 = e1.pr >> 16;
-    const float3 d0 = xyz(sp[la0]) - xyz(sp[lb0]);
-    float3 d1 = make_float3(0.f, 0.f, 0.f);
-    if (h1) d1 = xyz(sp[la1]) - xyz(sp[lb1]);
-    const float3 y0 = qmul_iso_rank1(e0.q, d0), y1 = qmul_iso_rank1(e1.q, d1);
-    const bool a0 = i0 < nm, a1 = h1 && i1 < nm;            // own constraint: a is an own vertex
-    const bool b0 = lb0 < kTileV, b1 = h1 && lb1 < kTileV;
-    float dot = a0 ? dot3(d0, y0) : 0.f;
-    if (a1) dot += dot3(d1, y1);
-    float4 qa0, qb0, qa1, qb1;
-    if (a0) qa0 = sq[la0];
-    if (b0) qb0 = sq[lb0];
-    if (a1) qa1 = sq[la1];
-    if (b1) qb1 = sq[lb1];
-    if (a0) sq[la0] = f4of(xyz(qa0) + y0);
-    if (b0) sq[lb0] = f4of(xyz(qb0) - y0);
-    if (a1) sq[la1] = f4of(xyz(qa1) + y1);
-    if (b1) sq[lb1] = f4of(xyz(qb1) - y1);
-    return dot;
-}
-
-// Walk all colors of tile t: sq += A_dist sp; returns sp.(A_dist sp) over own constraints.
+// Walk all colors of tile t: sq += A_dist sp; returns sp.(A_dist sp) over own constraints.  Entry
+// (la, lb): own constraint if la < kTileV (a own; b own or halo), else a foreign entry (a halo,
+// b own); only own slots are accumulated.
 template <int NT>
 DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const float4 *sp, float4 *sq, const int4 *sb,
                                 const TmaTiles &T) {
     float dotacc = 0.f;
-    const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
+    const uint32_t sbytes = tma_stage_bytes(T.cap);
     for (int c = 0; c < T.ncol; ++c) {
         const int st = c % kTmaStages;
         unsigned char *stage = stages + (size_t)st * sbytes;
-        const StageView S = stage_view(stage, T.capm, T.capf);
+        const StageView S = stage_view(stage, T.cap);
         mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
         const int4 g = sb[c];
-        const int nm = g.y - g.x, nmp = (nm + 7) & ~7, n = nmp + (g.w - g.z);
-        const int off = g.x & 3, foff = g.z & 3;
+        const int n = g.y - g.x, off = g.x & 3;
         for (int i = threadIdx.x; i < n; i += NT) {
-            if (i >= nm && i < nmp) continue;
-            dotacc += mv_entries<1>(S, i, 0, n, nm, nmp, off, foff, g.z, T, sp, sq);
+            const uint32_t pr = S.cp[off + i];
+            const int la = pr & 0xffff, lb = pr >> 16;
+            const float3 d = xyz(sp[la]) - xyz(sp[lb]);
+            const float3 y = qmul_iso_rank1(S.q[i], d);
+            if (la < kTileV) {
+                dotacc += dot3(d, y);
+                sq[la] = f4of(xyz(sq[la]) + y);
+            }
+            if (lb < kTileV) sq[lb] = f4of(xyz(sq[lb]) - y);
         }
         __syncthreads();
         // re-arm this stage for color c + kTmaStages: all reads of it completed before the barrier
         // (write-after-read across proxies is ordered by the barrier, as in a TMA consumer release);
-        // issued from the last warp, which never holds a second entry
+        // issued from the last warp
         if (threadIdx.x == NT - 32 && c + kTmaStages < T.ncol) tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
     }
     return dotacc;
@@ -849,7 +800,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
-    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.capm, T.capf) * kTmaStages);
+    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap) * kTmaStages);
     float4 *sp = sq + kTileV;
     const int hcap = T.hcap;
     const int t = blockIdx.x;
@@ -880,7 +831,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     if (threadIdx.x == NT - 32) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
-        const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
+        const uint32_t sbytes = tma_stage_bytes(T.cap);
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
     // ---- round trip 2
@@ -981,7 +932,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V,
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
-    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.capm, T.capf) * kTmaStages);
+    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap) * kTmaStages);
     float4 *sp = sq + kTileV;
     const int hcap = T.hcap;
     const int t = blockIdx.x;
@@ -1012,7 +963,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V,
     if (threadIdx.x == NT - 32) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
-        const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
+        const uint32_t sbytes = tma_stage_bytes(T.cap);
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
     // ---- scalars of this iteration (double, from the previous launches' reductions)
@@ -1147,7 +1098,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
-    const uint32_t sbytes = tma_stage_bytes(T.capm, T.capf);
+    const uint32_t sbytes = tma_stage_bytes(T.cap);
     float4 *sqb = reinterpret_cast<float4 *>(stages + (size_t)sbytes * kTmaStages);
     float4 *sqr = sqb + kTileV;
     const int hcap = T.hcap;
@@ -1216,21 +1167,17 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
     for (int c = 0; c < T.ncol; ++c) {
         const int st = c % kTmaStages;
         unsigned char *stage = stages + (size_t)st * sbytes;
-        const StageView S = stage_view(stage, T.capm, T.capf);
+        const StageView S = stage_view(stage, T.cap);
         mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
         const int4 g = sb[c];
-        const int nm = g.y - g.x, nmp = (nm + 7) & ~7, n = nmp + (g.w - g.z);
-        const int off = g.x & 3, foff = g.z & 3;
+        const int n = g.y - g.x, off = g.x & 3;
         for (int i = threadIdx.x; i < n; i += kTmaThreads) {
-            TItem e;
-            if (i < nm) e = TItem{S.cp[off + i], S.q[i]};
-            else if (i < nmp) continue;
-            else if (i - nmp < T.capf) e = TItem{S.fp[foff + i - nmp], S.fq[i - nmp]};
-            else e = titem_global(T, g.z + i - nmp);
-            const int la = e.pr & 0xffff, lb = e.pr >> 16;
-            const float3 qy = qmul_iso_rank1(e.q, xyz(sy[la]) - xyz(sy[lb]));
-            const float3 qz = qmul_iso_rank1(e.q, xyz(sz[la]) - xyz(sz[lb]));
-            if (i < nm) {
+            const uint32_t pr = S.cp[off + i];
+            const float4 q4 = S.q[i];
+            const int la = pr & 0xffff, lb = pr >> 16;
+            const float3 qy = qmul_iso_rank1(q4, xyz(sy[la]) - xyz(sy[lb]));
+            const float3 qz = qmul_iso_rank1(q4, xyz(sz[la]) - xyz(sz[lb]));
+            if (la < kTileV) {
                 sqb[la] = f4of(xyz(sqb[la]) - qy);
                 sqr[la] = f4of(xyz(sqr[la]) - qz);
             }
