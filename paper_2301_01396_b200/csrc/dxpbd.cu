@@ -474,6 +474,7 @@ struct dxpbd_scene {
     // CG-local tile structure (TMA-staged matvec, QF = 1)
     bool use_tma = false;
     int capm = 0;             // TMA stage capacity: largest combined (own + foreign) segment
+    int mv_minb = 4;          // TMA matvec: resident CTAs per SM (launch bounds)
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hpad, d_fpos;
@@ -742,7 +743,9 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
                 ++launches;
                 continue;
             }
-            if (s->use_tma)
+            if (s->use_tma && s->mv_minb == 5)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 5><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
+            else if (s->use_tma)
                 LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
@@ -1015,6 +1018,8 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 s->tma_smem = tma_smem_bytes(s->hcap, s->capm);
                 s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                if (const char *ev = getenv("DXPBD_MV_MINB")) s->mv_minb = atoi(ev);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 if (const char *ev = getenv("DXPBD_CGCG_MINB")) s->cgcg_minb = atoi(ev);
