@@ -297,6 +297,21 @@ def run_ours(a):
                 "avg_launch_ms": avg_ms, "launches": cnt, "working_launches": work, "share_of_kernel_time": share,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"}
 
+    # ---- whole-step roofline: compulsory bytes of every kernel class of one step (forward + adjoint)
+    # over the step time; rhs ~ one matvec + 36 B/vertex, adjoint ~ 40 B/vertex
+    step_roof = None
+    sst = api.dxpbd_stats(sc)
+    if sst["tma"]:
+        S = substeps_total
+        mv = algo_bytes("cg_dist", sst)
+        per_step = (S * (algo_bytes("predict", sst) + algo_bytes("dist_project", sst, E * a.iterations)
+                         + algo_bytes("dist_replay", sst, E * a.iterations)
+                         + mv + 36.0 * V + 40.0 * V)
+                    + (cg_mv / a.steps) * mv + (cg_iters / a.steps) * algo_bytes("cg_update", sst))
+        ach = per_step / (ms_per_step / 1e3) / 1e9
+        step_roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "algorithmic_bytes_per_step": per_step}
+
     # ---- CPU baseline (oracle on a bounded crop, rank 0 at N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -319,7 +334,7 @@ def run_ours(a):
             "ms_per_substep_fwd": (sum(t_fwds) / a.steps) / substeps_total,
             "ms_per_substep_fwd_adjoint": ms_per_step / substeps_total,
             "cg_iters_per_substep": cg_iters / max(1, a.steps * substeps_total),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "create_s": t_create, "loss": loss,
             "kernel_ms_per_step": {k: v[0] / a.steps for k, v in ktimes.items()},
         }
