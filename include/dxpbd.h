@@ -153,6 +153,33 @@ int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out
  *      matvec per solve for the single-reduction PCG). */
 int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
 
+/* ---- Vertex-partitioned domain decomposition -------------------------
+ * A group splits one scene into num_parts partitions, each owning a contiguous range of
+ * Morton vertex tiles and the distance constraints whose lower endpoint lies there; every
+ * partition keeps its own copy of the vertex state and the partitions exchange the vertices
+ * they write after every color sweep (forward and replay), the cross-partition derivative
+ * blocks after every replay, halo r / p after every PCG iteration (with all-reduced PCG
+ * scalars) and the adjoint halo after every substep.  This in-process group runs all
+ * partitions on desc->device with device-to-device exchanges; results equal the single scene
+ * (positions bit for bit; gradients up to the order of the PCG reductions).
+ * Supported: iterations == 1, pd_projection, no tets, grad_flags within FORCES | X0 | V0;
+ * the scene must take the TMA path (dxpbd_stats field 13).  Same argument conventions as
+ * the scene calls above. */
+typedef struct dxpbd_group dxpbd_group;
+int dxpbd_group_create(const dxpbd_scene_desc *desc, int32_t num_parts, dxpbd_group **out);
+int dxpbd_group_destroy(dxpbd_group *group);
+int dxpbd_group_forward(dxpbd_group *group, const float *x0, const float *v0, const float *forces,
+                        int32_t num_frames, int32_t mem, void *stream);
+int dxpbd_group_positions(dxpbd_group *group, int32_t frame, float *out, int32_t mem, void *stream);
+int dxpbd_group_backward(dxpbd_group *group, int32_t num_keys, const int32_t *key_frames,
+                         const float *targets, const float *weights, int32_t mem, float *loss_out,
+                         void *stream);
+/* kind: DXPBD_GRAD_FORCES, DXPBD_GRAD_X0 or DXPBD_GRAD_V0 */
+int dxpbd_group_grads(dxpbd_group *group, int32_t kind, float *out, int64_t out_len, int32_t mem,
+                      void *stream);
+/* out[0..n), n <= 16: 0 total PCG iterations, 1 max per solve, 4 solves, 5 worst residual, 6 loss */
+int dxpbd_group_stats(dxpbd_group *group, double *out, int32_t n);
+
 /* Kernel classes timed by the opt-in event profiler (dxpbd_profile / dxpbd_kernel_times). */
 #define DXPBD_K_PREDICT 0
 #define DXPBD_K_DIST_PROJECT 1

@@ -72,6 +72,13 @@ def lib():
             "dxpbd_stats": ([vp, vp, i32], ctypes.c_int),
             "dxpbd_profile": ([vp, i32], ctypes.c_int),
             "dxpbd_kernel_times": ([vp, vp, vp, i32], ctypes.c_int),
+            "dxpbd_group_create": ([ctypes.POINTER(SceneDesc), i32, ctypes.POINTER(vp)], ctypes.c_int),
+            "dxpbd_group_destroy": ([vp], ctypes.c_int),
+            "dxpbd_group_forward": ([vp, vp, vp, vp, i32, i32, vp], ctypes.c_int),
+            "dxpbd_group_positions": ([vp, i32, vp, i32, vp], ctypes.c_int),
+            "dxpbd_group_backward": ([vp, i32, vp, vp, vp, i32, vp, vp], ctypes.c_int),
+            "dxpbd_group_grads": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
+            "dxpbd_group_stats": ([vp, vp, i32], ctypes.c_int),
             "dxpbd_last_error": ([], ctypes.c_char_p),
             "dxpbd_version": ([], ctypes.c_int),
         }
@@ -85,7 +92,9 @@ def lib():
 
 EXPORTED = ["dxpbd_create", "dxpbd_destroy", "dxpbd_forward", "dxpbd_positions", "dxpbd_backward",
             "dxpbd_grads", "dxpbd_set_params", "dxpbd_coloring", "dxpbd_stats", "dxpbd_last_error",
-            "dxpbd_version", "dxpbd_profile", "dxpbd_kernel_times"]
+            "dxpbd_version", "dxpbd_profile", "dxpbd_kernel_times", "dxpbd_group_create", "dxpbd_group_destroy",
+            "dxpbd_group_forward", "dxpbd_group_positions", "dxpbd_group_backward", "dxpbd_group_grads",
+            "dxpbd_group_stats"]
 
 KCLASSES = ["predict", "dist_project", "contact_project", "tet_project", "dist_replay", "contact_replay",
             "tet_replay", "cg_vertex", "cg_dist", "cg_tet", "cg_update", "cg_init", "rhs", "adjoint", "grads",
@@ -156,11 +165,12 @@ class DxScene:
 
 
 # ------------------------------------------------------------------ C entry points
-def dxpbd_create(x_rest, inv_mass, dist_idx=None, dist_compliance=None, tet_idx=None, tet_a=None, tet_b=None,
-                 spheres=None, cap_center=None, cap_axis=None, cap_r0=None, cap_L0=None, cap_rbasis=None,
-                 cap_lbasis=None, shape_beta=None, gravity=(0.0, -9.81, 0.0), frame_dt=1 / 60, substeps=1,
-                 iterations=1, thickness=0.0, collision_compliance=0.0, max_frames=1, grad_flags=0,
-                 pd_projection=1, cg_tol=1e-6, cg_max_iter=500, device=0) -> DxScene:
+def _desc(x_rest, inv_mass, dist_idx=None, dist_compliance=None, tet_idx=None, tet_a=None, tet_b=None,
+          spheres=None, cap_center=None, cap_axis=None, cap_r0=None, cap_L0=None, cap_rbasis=None,
+          cap_lbasis=None, shape_beta=None, gravity=(0.0, -9.81, 0.0), frame_dt=1 / 60, substeps=1,
+          iterations=1, thickness=0.0, collision_compliance=0.0, max_frames=1, grad_flags=0,
+          pd_projection=1, cg_tol=1e-6, cg_max_iter=500, device=0):
+    """dxpbd_scene_desc from host arrays; returns (desc, kept arrays, handle dimensions)."""
     keep = []
 
     def h(a, dt=np.float32):
@@ -207,9 +217,14 @@ def dxpbd_create(x_rest, inv_mass, dist_idx=None, dist_compliance=None, tet_idx=
     d.cg_tol = float(cg_tol)
     d.cg_max_iter = int(cg_max_iter)
     d.device = int(device)
+    return d, keep, (V, E, T, S, K, NS if K else 0, int(max_frames), int(substeps))
+
+
+def dxpbd_create(x_rest, inv_mass, **kw) -> DxScene:
+    d, keep, dims = _desc(x_rest, inv_mass, **kw)
     out = ctypes.c_void_p()
     _check(lib().dxpbd_create(ctypes.byref(d), ctypes.byref(out)), "dxpbd_create")
-    return DxScene(out.value, V, E, T, S, K, NS if K else 0, int(max_frames), int(substeps))
+    return DxScene(out.value, *dims)
 
 
 def dxpbd_destroy(scene: DxScene):
@@ -312,6 +327,79 @@ def dxpbd_version() -> int:
 
 
 # ------------------------------------------------------------------ convenience
+# ------------------------------------------------------------------ partition groups (domain decomposition)
+class DxGroup(DxScene):
+    """Owning handle of a dxpbd_group (one scene split into num_parts vertex partitions)."""
+
+    def __init__(self, handle, parts, *dims):
+        super().__init__(handle, *dims)
+        self.parts = parts
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().dxpbd_group_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def dxpbd_group_create(x_rest, inv_mass, num_parts: int = 2, **kw) -> DxGroup:
+    d, keep, dims = _desc(x_rest, inv_mass, **kw)
+    out = ctypes.c_void_p()
+    _check(lib().dxpbd_group_create(ctypes.byref(d), int(num_parts), ctypes.byref(out)), "dxpbd_group_create")
+    return DxGroup(out.value, int(num_parts), *dims)
+
+
+def dxpbd_group_destroy(group: DxGroup):
+    if group.handle:
+        _check(lib().dxpbd_group_destroy(group.handle), "dxpbd_group_destroy")
+        group.handle = None
+
+
+def dxpbd_group_forward(group: DxGroup, x0, v0, forces=None, num_frames: int = 1):
+    ax, av, af = _Arg(x0, np.float32), _Arg(v0, np.float32), _Arg(forces, np.float32)
+    mem = _mem_of(ax, av, af)
+    _check(lib().dxpbd_group_forward(group.handle, ax.ptr, av.ptr, af.ptr, int(num_frames), mem,
+                                     _stream(x0, v0, forces)), "dxpbd_group_forward")
+    group.frames = int(num_frames)
+
+
+def dxpbd_group_positions(group: DxGroup, frame: int, out=None):
+    if out is None:
+        out = np.zeros((group.V, 3), np.float32)
+    a = _Arg(out, np.float32)
+    _check(lib().dxpbd_group_positions(group.handle, int(frame), a.ptr, a.mem, _stream(out)), "dxpbd_group_positions")
+    return out
+
+
+def dxpbd_group_backward(group: DxGroup, key_frames, targets, weights=None) -> float:
+    kf = np.ascontiguousarray(np.asarray(key_frames, np.int32).reshape(-1))
+    at, aw = _Arg(targets, np.float32), _Arg(weights, np.float32)
+    mem = _mem_of(at, aw)
+    loss = ctypes.c_float(0.0)
+    _check(lib().dxpbd_group_backward(group.handle, len(kf), kf.ctypes.data, at.ptr, aw.ptr, mem,
+                                      ctypes.byref(loss), _stream(targets, weights)), "dxpbd_group_backward")
+    return float(loss.value)
+
+
+def dxpbd_group_grads(group: DxGroup, kind, out=None):
+    kind = GRAD_NAMES.get(kind, kind)
+    shape = _grad_size(group, kind)
+    if out is None:
+        out = np.zeros(shape, np.float32)
+    a = _Arg(out, np.float32)
+    _check(lib().dxpbd_group_grads(group.handle, int(kind), a.ptr, int(np.prod(shape)), a.mem, _stream(out)),
+           "dxpbd_group_grads")
+    return out
+
+
+def dxpbd_group_stats(group: DxGroup) -> dict:
+    out = np.zeros(16, np.float64)
+    _check(lib().dxpbd_group_stats(group.handle, out.ctypes.data, 16), "dxpbd_group_stats")
+    return dict(cg_iters_total=out[0], cg_iters_max=out[1], solves=out[4], worst_relres=out[5], loss=out[6])
+
+
 def scene_kwargs(scene) -> dict:
     """Map a synth.Scene (duck-typed) onto dxpbd_create keyword arguments."""
     s = scene

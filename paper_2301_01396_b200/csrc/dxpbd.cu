@@ -24,6 +24,7 @@ using namespace dx;
 namespace {
 
 thread_local std::string g_err;
+thread_local bool g_keep_host = false;   // dxpbd_create keeps the host layout (partition groups)
 
 struct Err {
     int code;
@@ -482,6 +483,11 @@ struct dxpbd_scene {
     DBuf<uint32_t> d_cpair;
     DBuf<float4> d_Qt;                  // Q blocks in the TMA layout (own at tpos[j], foreign copy at fpos[j])
     DBuf<uint16_t> d_vslot, d_hslot;   // tile-local shared-memory slots (own vertices, halo entries)
+    // host layout kept for partition groups (g_keep_host at create)
+    std::vector<int> seg_h;                 // [nc][nt + 1] sorted-constraint offsets per (color, tile)
+    std::vector<int2> ab_h;                 // sorted constraints: internal endpoints (a < b)
+    std::vector<std::vector<int>> halo_h;   // per tile: halo vertex ids (sorted)
+    std::vector<int> fpos_h;                // per sorted constraint: position of the b-tile copy in Qt, or -1
     DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
     // tets (color-sorted, internal vertex ids)
     DBuf<int4> t_idx;
@@ -703,6 +709,118 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     }
     DX_CHECK_CUDA(cudaGetLastError());
     return launches;
+}
+
+// x0, v0, forces (user order, host or device) -> internal order: state 0, v0, per-frame forces
+void forward_inputs(dxpbd_scene *s, const float *x0, const float *v0, const float *forces, int num_frames, int mem,
+                    cudaStream_t st) {
+    const int V = s->V;
+    // user vertex order -> internal (Morton) order at the boundary
+    const float *src = x0;
+    if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, x0, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
+    k_pack4d<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->inv_mass.p, state(s, 0));
+    src = v0;
+    if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, v0, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
+    k_pack4g<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->v0.p);
+    s->have_forces = forces != nullptr;
+    if (forces) {
+        if (s->forces.n < (size_t)s->max_frames * V * 3) s->forces.alloc((size_t)s->max_frames * V * 3);
+        if (mem == DXPBD_MEM_HOST) {
+            for (int f = 0; f < num_frames; ++f) {
+                upload(s->tmp3.p, forces + (size_t)f * V * 3, sizeof(float) * V * 3, mem, st);
+                k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->tmp3.p, s->vperm.p, s->forces.p + (size_t)f * V * 3);
+            }
+        } else {
+            k_gather3<<<nblk((int64_t)V * num_frames), kBlock, 0, st>>>(V, num_frames, forces, s->vperm.p, s->forces.p);
+        }
+    }
+}
+
+struct BwdSetup {
+    const float *wts = nullptr;
+    std::vector<int> key_of;   // state index -> keyframe slot
+    bool g_comp = false, g_forces = false, g_coll = false, warm2 = false;
+    int last_key_state = -1;
+};
+
+// Buffers, targets / weights (internal order), zeroed accumulators and adjoint state of a backward.
+BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frames, const float *targets,
+                          const float *weights, int mem, cudaStream_t st) {
+    const int V = s->V, E = s->E, sub = s->substeps;
+    const int N = s->frames_done * sub;
+    BwdSetup su;
+    // buffers
+    if (s->xr.n < (size_t)V) s->xr.alloc(V);
+    auto ensure4 = [&](DBuf<float3> &b) { if (b.n < (size_t)V) b.alloc(V); };
+    ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
+    if (s->use_tma && !s->T && s->cgcg) { ensure4(s->r1); ensure4(s->s1); ensure4(s->w1); }
+    ensure4(s->uprev); ensure4(s->u0);
+    if (s->warm_order == 2 && s->use_tma) ensure4(s->uprev2);
+    const bool warm2 = su.warm2 = s->warm_order == 2 && s->use_tma;
+    if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);
+    const bool g_comp = su.g_comp = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
+    const bool g_forces = su.g_forces = (s->grad_flags >> DXPBD_GRAD_FORCES) & 1;
+    const bool g_coll = su.g_coll = (s->grad_flags & ((1u << DXPBD_GRAD_SHAPE) | (1u << DXPBD_GRAD_SPHERE))) != 0;
+    if (E && g_comp && s->ed.n < (size_t)3 * E) s->ed.alloc((size_t)3 * E);
+    if (E && s->iterations > 1 && s->sc_lam.n < (size_t)E) {
+        s->sc_lam.alloc(E); s->sc_sig.alloc((size_t)3 * E); s->sc_B.alloc((size_t)6 * E); s->sc_T.alloc(E); s->sc_e.alloc((size_t)3 * E);
+    }
+    if (s->NC) {
+        const size_t NV = (size_t)s->NC * V;
+        if (s->Qc.n < (size_t)6 * V) s->Qc.alloc((size_t)6 * V);
+        if (g_coll && s->ec.n < 12 * NV) s->ec.alloc(12 * NV);
+        if (s->iterations > 1 && s->cc_lam.n < NV) {
+            s->cc_lam.alloc(NV); s->cc_T.alloc(4 * NV); s->cc_sig.alloc(3 * NV); s->cc_B.alloc(6 * NV); s->cc_e.alloc(12 * NV);
+        }
+    }
+    if (s->cg_sc.n < (size_t)(s->cg_max_iter + 2) * 4) s->cg_sc.alloc((size_t)(s->cg_max_iter + 2) * 4);
+    const size_t nacc = 1 + 4 * (size_t)std::max(s->NC, 1);
+    if (s->acc.n < nacc) s->acc.alloc(nacc);
+    if (s->T) {
+        const size_t T = s->T;
+        if (s->t_Q.n < 45 * T) s->t_Q.alloc(45 * T);
+        if (((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) && s->t_e.n < 18 * T) s->t_e.alloc(18 * T);
+        if (s->t_g.n < 2 * T) s->t_g.alloc(2 * T);
+        if (s->iterations > 1 && s->ts_lam.n < 2 * T) {
+            s->ts_lam.alloc(2 * T); s->ts_S.alloc(18 * T); s->ts_Dt.alloc(45 * T); s->ts_Tu.alloc(4 * T); s->ts_e.alloc(18 * T);
+        }
+    }
+    // targets
+    if (num_keys) {
+        if (s->targets.n < (size_t)num_keys * V * 3) s->targets.alloc((size_t)num_keys * V * 3);
+        for (int k = 0; k < num_keys; ++k) {
+            const float *src = targets + (size_t)k * V * 3;
+            if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, src, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
+            k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, src, s->vperm.p, s->targets.p + (size_t)k * V * 3);
+        }
+    }
+    if (weights) {
+        if (s->weights.n < (size_t)V) s->weights.alloc(V);
+        const float *src = weights;
+        if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, weights, sizeof(float) * V, mem, st); src = s->tmp3.p; }
+        k_gather1<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->weights.p);
+        su.wts = s->weights.p;
+    }
+    // gradient accumulators
+    if (g_comp && E) { if (s->g_comp.n < (size_t)E) s->g_comp.alloc(E); DX_CHECK_CUDA(cudaMemsetAsync(s->g_comp.p, 0, sizeof(float) * E, st)); }
+    if (g_forces) {
+        size_t nf = (size_t)std::max(s->frames_done, 1) * V * 3;
+        if (s->g_force.n < nf) s->g_force.alloc(nf);
+        DX_CHECK_CUDA(cudaMemsetAsync(s->g_force.p, 0, sizeof(float) * nf, st));
+    }
+    DX_CHECK_CUDA(cudaMemsetAsync(s->acc.p, 0, sizeof(double) * nacc, st));
+    if (s->T) DX_CHECK_CUDA(cudaMemsetAsync(s->t_g.p, 0, sizeof(float) * 2 * s->T, st));
+    // state index -> keyframe slot
+    su.key_of.assign(N + 1, -1);
+    for (int k = 0; k < num_keys; ++k) su.key_of[key_frames[k] * sub] = k;   // duplicates: last wins
+    // increment-form adjoint (kernels.cuh "adjoint"): y = u = 0 beyond the horizon
+    DX_CHECK_CUDA(cudaMemsetAsync(s->y.p, 0, sizeof(float3) * V, st));
+    DX_CHECK_CUDA(cudaMemsetAsync(s->ax.p, 0, sizeof(float3) * V, st));   // ax holds u
+    DX_CHECK_CUDA(cudaMemsetAsync(s->uprev.p, 0, sizeof(float3) * V, st));
+    if (warm2) DX_CHECK_CUDA(cudaMemsetAsync(s->uprev2.p, 0, sizeof(float3) * V, st));
+    for (int n = 0; n <= N; ++n) if (su.key_of[n] >= 0) su.last_key_state = n;
+    (void)g_comp; (void)g_forces; (void)g_coll;
+    return su;
 }
 
 // ------------------------------------------------------------------ filtered PCG
@@ -1012,6 +1130,12 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 upload(s->d_cpair.p, cpair.data(), sizeof(uint32_t) * cpair.size(), DXPBD_MEM_HOST, st);
                 s->d_fpos.alloc(E);
                 upload(s->d_fpos.p, fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
+                if (g_keep_host) {
+                    s->seg_h = seg;
+                    s->ab_h = ab_sorted;
+                    s->halo_h = halo;
+                    s->fpos_h = fposv;
+                }
                 s->d_tpos.alloc(E);
                 upload(s->d_tpos.p, tpos.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
                 s->d_Qt.alloc((size_t)NTOT + 1);
@@ -1139,26 +1263,7 @@ int dxpbd_forward(dxpbd_scene *s, const float *x0, const float *v0, const float 
     DX_REQUIRE(num_frames >= 0 && num_frames <= s->max_frames, DXPBD_ERR_LIMIT, "num_frames exceeds max_frames");
     DX_CHECK_CUDA(cudaSetDevice(s->device));
     cudaStream_t st = (cudaStream_t)stream;
-    const int V = s->V;
-    // user vertex order -> internal (Morton) order at the boundary
-    const float *src = x0;
-    if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, x0, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
-    k_pack4d<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->inv_mass.p, state(s, 0));
-    src = v0;
-    if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, v0, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
-    k_pack4g<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->v0.p);
-    s->have_forces = forces != nullptr;
-    if (forces) {
-        if (s->forces.n < (size_t)s->max_frames * V * 3) s->forces.alloc((size_t)s->max_frames * V * 3);
-        if (mem == DXPBD_MEM_HOST) {
-            for (int f = 0; f < num_frames; ++f) {
-                upload(s->tmp3.p, forces + (size_t)f * V * 3, sizeof(float) * V * 3, mem, st);
-                k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->tmp3.p, s->vperm.p, s->forces.p + (size_t)f * V * 3);
-            }
-        } else {
-            k_gather3<<<nblk((int64_t)V * num_frames), kBlock, 0, st>>>(V, num_frames, forces, s->vperm.p, s->forces.p);
-        }
-    }
+    forward_inputs(s, x0, v0, forces, num_frames, mem, st);
     int launches = 4;
     const int N = num_frames * s->substeps;
     for (int n = 0; n < N; ++n) launches += forward_substep(s, n, st);
@@ -1196,82 +1301,15 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     const int N = s->frames_done * sub;
     for (int k = 0; k < num_keys; ++k)
         DX_REQUIRE(key_frames[k] >= 0 && key_frames[k] <= s->frames_done, DXPBD_ERR_ARG, "key frame out of range");
-    // buffers
-    if (s->xr.n < (size_t)V) s->xr.alloc(V);
-    auto ensure4 = [&](DBuf<float3> &b) { if (b.n < (size_t)V) b.alloc(V); };
-    ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
-    if (s->use_tma && !s->T && s->cgcg) { ensure4(s->r1); ensure4(s->s1); ensure4(s->w1); }
-    ensure4(s->uprev); ensure4(s->u0);
-    if (s->warm_order == 2 && s->use_tma) ensure4(s->uprev2);
-    const bool warm2 = s->warm_order == 2 && s->use_tma;
-    if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);
-    const bool g_comp = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
-    const bool g_forces = (s->grad_flags >> DXPBD_GRAD_FORCES) & 1;
-    const bool g_coll = (s->grad_flags & ((1u << DXPBD_GRAD_SHAPE) | (1u << DXPBD_GRAD_SPHERE))) != 0;
-    if (E && g_comp && s->ed.n < (size_t)3 * E) s->ed.alloc((size_t)3 * E);
-    if (E && s->iterations > 1 && s->sc_lam.n < (size_t)E) {
-        s->sc_lam.alloc(E); s->sc_sig.alloc((size_t)3 * E); s->sc_B.alloc((size_t)6 * E); s->sc_T.alloc(E); s->sc_e.alloc((size_t)3 * E);
-    }
-    if (s->NC) {
-        const size_t NV = (size_t)s->NC * V;
-        if (s->Qc.n < (size_t)6 * V) s->Qc.alloc((size_t)6 * V);
-        if (g_coll && s->ec.n < 12 * NV) s->ec.alloc(12 * NV);
-        if (s->iterations > 1 && s->cc_lam.n < NV) {
-            s->cc_lam.alloc(NV); s->cc_T.alloc(4 * NV); s->cc_sig.alloc(3 * NV); s->cc_B.alloc(6 * NV); s->cc_e.alloc(12 * NV);
-        }
-    }
-    if (s->cg_sc.n < (size_t)(s->cg_max_iter + 2) * 4) s->cg_sc.alloc((size_t)(s->cg_max_iter + 2) * 4);
-    const size_t nacc = 1 + 4 * (size_t)std::max(s->NC, 1);
-    if (s->acc.n < nacc) s->acc.alloc(nacc);
-    if (s->T) {
-        const size_t T = s->T;
-        if (s->t_Q.n < 45 * T) s->t_Q.alloc(45 * T);
-        if (((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) && s->t_e.n < 18 * T) s->t_e.alloc(18 * T);
-        if (s->t_g.n < 2 * T) s->t_g.alloc(2 * T);
-        if (s->iterations > 1 && s->ts_lam.n < 2 * T) {
-            s->ts_lam.alloc(2 * T); s->ts_S.alloc(18 * T); s->ts_Dt.alloc(45 * T); s->ts_Tu.alloc(4 * T); s->ts_e.alloc(18 * T);
-        }
-    }
-    // targets
-    if (num_keys) {
-        if (s->targets.n < (size_t)num_keys * V * 3) s->targets.alloc((size_t)num_keys * V * 3);
-        for (int k = 0; k < num_keys; ++k) {
-            const float *src = targets + (size_t)k * V * 3;
-            if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, src, sizeof(float) * V * 3, mem, st); src = s->tmp3.p; }
-            k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, src, s->vperm.p, s->targets.p + (size_t)k * V * 3);
-        }
-    }
-    const float *wts = nullptr;
-    if (weights) {
-        if (s->weights.n < (size_t)V) s->weights.alloc(V);
-        const float *src = weights;
-        if (mem == DXPBD_MEM_HOST) { upload(s->tmp3.p, weights, sizeof(float) * V, mem, st); src = s->tmp3.p; }
-        k_gather1<<<nblk(V), kBlock, 0, st>>>(V, src, s->vperm.p, s->weights.p);
-        wts = s->weights.p;
-    }
-    // gradient accumulators
-    if (g_comp && E) { if (s->g_comp.n < (size_t)E) s->g_comp.alloc(E); DX_CHECK_CUDA(cudaMemsetAsync(s->g_comp.p, 0, sizeof(float) * E, st)); }
-    if (g_forces) {
-        size_t nf = (size_t)std::max(s->frames_done, 1) * V * 3;
-        if (s->g_force.n < nf) s->g_force.alloc(nf);
-        DX_CHECK_CUDA(cudaMemsetAsync(s->g_force.p, 0, sizeof(float) * nf, st));
-    }
-    DX_CHECK_CUDA(cudaMemsetAsync(s->acc.p, 0, sizeof(double) * nacc, st));
-    if (s->T) DX_CHECK_CUDA(cudaMemsetAsync(s->t_g.p, 0, sizeof(float) * 2 * s->T, st));
-    // state index -> keyframe slot
-    std::vector<int> key_of(N + 1, -1);
-    for (int k = 0; k < num_keys; ++k) key_of[key_frames[k] * sub] = k;   // duplicates: last wins
+    BwdSetup su = backward_prepare(s, num_keys, key_frames, targets, weights, mem, st);
+    const float *wts = su.wts;
+    const bool g_comp = su.g_comp, g_forces = su.g_forces, g_coll = su.g_coll, warm2 = su.warm2;
+    const int last_key_state = su.last_key_state;
+    std::vector<int> &key_of = su.key_of;
     // loss
     for (int k = 0; k < num_keys; ++k)
         LAUNCH(DXPBD_K_OTHER, k_loss<<<nblk(V), kBlock, 0, st>>>(V, state(s, key_frames[k] * sub), s->targets.p + (size_t)k * V * 3, wts, s->acc.p));
-    // increment-form adjoint (kernels.cuh "adjoint"): y = u = 0 beyond the horizon
     auto tgt = [&](int n) -> const float * { return key_of[n] >= 0 ? s->targets.p + (size_t)key_of[n] * V * 3 : nullptr; };
-    DX_CHECK_CUDA(cudaMemsetAsync(s->y.p, 0, sizeof(float3) * V, st));
-    DX_CHECK_CUDA(cudaMemsetAsync(s->ax.p, 0, sizeof(float3) * V, st));   // ax holds u
-    DX_CHECK_CUDA(cudaMemsetAsync(s->uprev.p, 0, sizeof(float3) * V, st));
-    if (warm2) DX_CHECK_CUDA(cudaMemsetAsync(s->uprev2.p, 0, sizeof(float3) * V, st));
-    int last_key_state = -1;
-    for (int n = 0; n <= N; ++n) if (key_of[n] >= 0) last_key_state = n;
     int launches = num_keys + 2, total_it = 0, max_it = 0;
     double worst = 0.0;
     int solves = 0;
@@ -1522,3 +1560,5 @@ int dxpbd_stats(dxpbd_scene *s, double *out, int32_t n) {
 }
 
 }  // extern "C"
+
+#include "group.inc"

@@ -796,14 +796,14 @@ DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const flo
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, int V,
                                                                   const float *__restrict__ Qc, CGBufs B,
-                                                                  const float *__restrict__ wv, CGState s) {
+                                                                  const float *__restrict__ wv, CGState s, int t0 = 0) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
     float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap) * kTmaStages);
     float4 *sp = sq + kTileV;
     const int hcap = T.hcap;
-    const int t = blockIdx.x;
+    const int t = blockIdx.x + t0;   // t0: first tile of a partition (domain decomposition)
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
     __shared__ int4 sb[kMaxColors];
@@ -1094,7 +1094,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                             const float *__restrict__ weights, const float *__restrict__ wv,
                                                             float3 *__restrict__ bout, float3 *__restrict__ r0out,
-                                                            float3 *__restrict__ u0out) {
+                                                            float3 *__restrict__ u0out, int t0 = 0) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
     const int hcap = T.hcap;
     float4 *sy = sqr + kTileV;
     float4 *sz = sy + kTileV + hcap;
-    const int t = blockIdx.x;
+    const int t = blockIdx.x + t0;
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
     __shared__ int4 sb[kMaxColors];
@@ -1481,5 +1481,26 @@ __global__ void k_grad_colliders(int V, int NC, const float *__restrict__ e, con
         __syncthreads();
     }
 }
+
+// ---------------------------------------------------------------------------------------------
+// Domain decomposition (in-process partition group, dxpbd_group_*): halo exchange between the
+// partitions' copies of a vertex or block array (dst[ids[i]] = src[ids[i]]) and the all-reduce
+// of the PCG scalar slots (sum over partitions, written back to every partition).
+template <class T>
+__global__ void k_xchg(int n, const int *__restrict__ ids, const T *__restrict__ src, T *__restrict__ dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const int k = ids[i];
+        dst[k] = src[k];
+    }
+}
+__global__ void k_slot_allreduce(int P, double *const *__restrict__ slots, int off, int count) {
+    const int i = threadIdx.x;
+    if (i >= count) return;
+    double sum = 0.0;
+    for (int p = 0; p < P; ++p) sum += slots[p][off + i];
+    for (int p = 0; p < P; ++p) slots[p][off + i] = sum;
+}
+
 
 }  // namespace dx
