@@ -48,6 +48,9 @@ def args_():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--ref-n", type=int, default=80, help="grid side of the oracle crop")
+    p.add_argument("--partitions", type=int, default=0,
+                   help="run the vertex-partitioned domain decomposition with P partitions on this GPU "
+                        "(in-process group, serialized partitions: measures the exchange overhead)")
     return p.parse_args()
 
 
@@ -172,6 +175,66 @@ def algo_bytes(cls, st, units_per_launch=None):
     if cls == "predict":        # x_n 32, x_{n-1} 32, f 12, out 32
         return 108.0 * V
     return None
+
+
+def run_partitioned(a):
+    """Domain decomposition (dxpbd_group_*) with a.partitions partitions on one GPU.  The partitions
+    run one after another on the same device with device-to-device halo exchanges, so the line
+    measures the decomposition's overhead (exchanges, redundant per-vertex work), not multi-GPU
+    scaling."""
+    import numpy as np
+    import torch
+    from paper_2301_01396_b200 import api
+    from synth import large_cloth
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    side = 10.0 * (a.n - 1) / 2943.0
+    s = large_cloth(n=a.n, frames=a.frames, substeps=a.substeps, iterations=a.iterations, seed=4, side=side,
+                    with_forces=False, key_frames=tuple(k for k in (10, 20, 30) if k <= a.frames) or (a.frames,))
+    V, E = s.num_vertices, len(s.dist_idx)
+    g = torch.Generator(device="cpu").manual_seed(1234)
+    dev = torch.device("cuda", 0)
+    forces = (torch.randn((a.frames, V, 3), generator=g, dtype=torch.float32) * 0.1).to(dev)
+    x0, v0 = (torch.as_tensor(t, dtype=torch.float32, device=dev) for t in (s.x0, s.v0))
+    tg = torch.as_tensor(s.targets, dtype=torch.float32, device=dev)
+    kf = np.asarray(s.key_frames, np.int32)
+    t_create = time.perf_counter()
+    grp = api.dxpbd_group_create(**api.scene_kwargs(s), num_parts=a.partitions, max_frames=a.frames,
+                                 grad_flags=api.flags("forces"), cg_tol=a.cg_tol, cg_max_iter=1000)
+    t_create = time.perf_counter() - t_create
+    del s
+    gf = torch.empty((a.frames, V, 3), dtype=torch.float32, device=dev)
+
+    def step():
+        api.dxpbd_group_forward(grp, x0, v0, forces, a.frames)
+        loss = api.dxpbd_group_backward(grp, kf, tg)
+        api.dxpbd_group_grads(grp, "forces", gf)
+        return loss
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    st = api.dxpbd_group_stats(grp)
+    solves = E * a.iterations * a.frames * a.substeps
+    line = {"metric": METRIC, "value": solves / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"large_cloth {a.n}x{a.n} (BASELINE configs[4] shape), {a.frames} frames",
+                       "vertices": V, "constraints": E, "frames": a.frames, "substeps": a.substeps,
+                       "parallelism": f"domain decomposition, {a.partitions} partitions on 1 GPU (serialized, "
+                                      "device-to-device halo exchange)"},
+            "exchange": {"vertices_per_sweep": st["xchg_sweep"], "halo_vertices": st["xchg_halo"],
+                         "cross_blocks": st["xchg_blocks"],
+                         "bytes_per_substep_forward": 32.0 * st["xchg_sweep"]},
+            "cg_iters_per_substep": st["cg_iters_total"] / max(st["solves"], 1), "create_s": t_create}
+    print(json.dumps(line), flush=True)
 
 
 def run_ours(a):
@@ -346,6 +409,8 @@ def main():
     a = args_()
     if a.impl == "reference":
         run_reference(a)
+    elif a.partitions > 0:
+        run_partitioned(a)
     else:
         run_ours(a)
 

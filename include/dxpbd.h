@@ -177,7 +177,9 @@ int dxpbd_group_backward(dxpbd_group *group, int32_t num_keys, const int32_t *ke
 /* kind: DXPBD_GRAD_FORCES, DXPBD_GRAD_X0 or DXPBD_GRAD_V0 */
 int dxpbd_group_grads(dxpbd_group *group, int32_t kind, float *out, int64_t out_len, int32_t mem,
                       void *stream);
-/* out[0..n), n <= 16: 0 total PCG iterations, 1 max per solve, 4 solves, 5 worst residual, 6 loss */
+/* out[0..n), n <= 16: 0 total PCG iterations, 1 max per solve, 4 solves, 5 worst residual, 6 loss,
+ * 8 vertices exchanged per substep sweep (all colors, forward or replay), 9 halo vertices
+ * exchanged per PCG vector exchange, 10 cross-partition blocks per replay, 11 partitions. */
 int dxpbd_group_stats(dxpbd_group *group, double *out, int32_t n);
 
 /* Kernel classes timed by the opt-in event profiler (dxpbd_profile / dxpbd_kernel_times). */
