@@ -521,6 +521,7 @@ struct dxpbd_scene {
     int warm_order = 2;                                // PCG warm start: extrapolation order (1 or 2; TMA path)
     int nb = 1;                                        // K = 1 forward projection: constraints per thread
     int nb_rep = 2;                                    // K = 1 replay: constraints per thread
+    int rep_minb = 3;                                  // K = 1 replay: launch-bounds CTAs per SM (measured best)
     DBuf<float3> r1, s1, w1;                           // single-reduction PCG ping-pong partners
     bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
                                                        // measured 10 % slower than matvec + update)
@@ -663,7 +664,17 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
             float *eo = want_e ? s->ed.p : nullptr;
-            if (first && last && s->qf == 1 && s->nb_rep == 2)
+            if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3)
+                LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 3><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
+                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p)));
+            else if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 4)
+                LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 4><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
+                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p)));
+            else if (first && last && s->qf == 1 && s->nb_rep == 2)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay1<2><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
                     s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
@@ -976,6 +987,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_WARM")) s->warm_order = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_NB")) s->nb = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
+    if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
 
     cudaStream_t st = 0;
 

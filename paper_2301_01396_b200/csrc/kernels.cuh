@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(kBlock) k_dist_project1(int begin, int count, 
 // iterate, stores the closed-form block Q_j at its TMA-layout position tpos[j] (and the foreign copy),
 // and the compliance control vector e_j = t n, t = -dl / (dt^2 J) (the general replay with
 // lambda_0 = T = 0).  Same arithmetic as k_dist_replay<true, true, 1>.
-template <int NB>
-__global__ void __launch_bounds__(kBlock) k_dist_replay1(int begin, int count, int E, const int2 *__restrict__ idx,
+template <int NB, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB) k_dist_replay1(int begin, int count, int E, const int2 *__restrict__ idx,
                                                          const float *__restrict__ rest,
                                                          const float *__restrict__ alpha, float inv_dt2,
                                                          float4 *__restrict__ Q4, float *__restrict__ eout,
