@@ -835,7 +835,7 @@ BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frame
 }
 
 // ------------------------------------------------------------------ filtered PCG
-int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_out) {
+int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_out, bool started) {
     // warm-started PCG: s->ax holds u_{n+1} (initial guess), s->r the residual r0 and s->rhs the
     // system right-hand side b (both from the rhs kernel); cg_sc was zeroed before the rhs kernel.
     const int V = s->V, E = s->E;
@@ -857,7 +857,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     };
     if (cgcg)
         cgcg_launch(-1);
-    else
+    else if (!started)   // else fused into the rhs kernel
         LAUNCH(DXPBD_K_CG_INIT, k_cg_start<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->r.p, s->p.p, xw, cs));
     int launches = 1;
     int it = 0;
@@ -1326,6 +1326,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     double worst = 0.0;
     int solves = 0;
     const float *Qc = s->NC ? s->Qc.p : nullptr;
+    // PCG start fused into the TMA rhs kernel (no tet rhs pass after it, standard PCG)
+    const bool fuse_start = s->use_tma && !s->T && !(s->cgcg);
     for (int n = std::min(N, last_key_state) - 1; n >= 0; --n) {
         const int frame = n / sub;
         float *gf = g_forces ? s->g_force.p + (size_t)frame * V * 3 : nullptr;
@@ -1339,7 +1341,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             if (s->use_tma)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_rhs_smem, st>>>(
                     tt, V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
-                    s->r.p, s->u0.p));
+                    s->r.p, s->u0.p, 0, fuse_start ? s->p.p : nullptr,
+                    CGState{s->cg_sc.p, s->cg_sc.p + (size_t)(s->cg_max_iter + 1) * 4, s->cg_tol * s->cg_tol}));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tiled<1><<<s->ntiles, kBlock, 0, st>>>(tl, V, s->d_idx.p, s->Qd.p, E, Qc, s->ax.p, s->uprev.p,
                                                                                  s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p,
@@ -1359,7 +1362,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         double rel = 0.0;
         // rotate: the PCG iterates on the warm start u0; afterwards ax = u_n, uprev = u_{n+1}
         std::swap(s->ax.p, s->u0.p);      // ax <- u0 (solution buffer), u0 <- u_{n+1}
-        launches += pcg_solve(s, st, iters, rel);   // u_n into s->ax
+        launches += pcg_solve(s, st, iters, rel, fuse_start);   // u_n into s->ax
         if (warm2) std::swap(s->uprev2.p, s->uprev.p);   // uprev2 <- u_{n+2}
         std::swap(s->uprev.p, s->u0.p);   // uprev <- u_{n+1}, u0 <- u_{n+2} or u_{n+3} (free)
         total_it += iters;

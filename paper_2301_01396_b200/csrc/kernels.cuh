@@ -1094,7 +1094,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
                                                             const double4 *__restrict__ xkey, const float *__restrict__ target,
                                                             const float *__restrict__ weights, const float *__restrict__ wv,
                                                             float3 *__restrict__ bout, float3 *__restrict__ r0out,
-                                                            float3 *__restrict__ u0out, int t0 = 0) {
+                                                            float3 *__restrict__ u0out, int t0 = 0,
+                                                            float3 *__restrict__ p0out = nullptr, CGState cs = CGState{}) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
@@ -1190,11 +1191,30 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
         // re-arm the stage (write-after-read ordered by the barrier; see tma_tile_colors)
         if (threadIdx.x == kTmaThreads - 32 && c + kTmaStages < T.ncol) tma_issue(&bars[st], stage, sb[c + kTmaStages], T);
     }
+    // epilogue; with p0out the PCG start is fused (k_cg_start): p_0 = M^-1 r_0, slot 0 gets r.z and
+    // r.r, s.bnorm2 gets |b|^2
+    float acc[3] = {0.f, 0.f, 0.f};
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         const int v = v0 + i, si = T.vslot[(size_t)t * kTileV + i];
-        const bool fr = wv[v] > 0.f;
-        bout[v] = fr ? xyz(sqb[si]) : make_float3(0.f, 0.f, 0.f);
-        r0out[v] = fr ? xyz(sqr[si]) : make_float3(0.f, 0.f, 0.f);
+        const float w = wv[v];
+        const bool fr = w > 0.f;
+        const float3 bv = fr ? xyz(sqb[si]) : make_float3(0.f, 0.f, 0.f);
+        const float3 rv = fr ? xyz(sqr[si]) : make_float3(0.f, 0.f, 0.f);
+        bout[v] = bv;
+        r0out[v] = rv;
+        if (p0out) {
+            p0out[v] = w * rv;
+            const float r2 = dot3(rv, rv);
+            acc[0] += w * r2;
+            acc[1] += r2;
+            acc[2] += dot3(bv, bv);
+        }
+    }
+    if (p0out) {
+        float a2[2] = {acc[0], acc[1]};
+        block_reduce_add<2>(a2, cs.sc + 1);
+        float bb[1] = {acc[2]};
+        block_reduce_add<1>(bb, cs.bnorm2);
     }
 }
 
