@@ -475,7 +475,6 @@ struct dxpbd_scene {
     // CG-local tile structure (TMA-staged matvec, QF = 1)
     bool use_tma = false;
     int capm = 0;             // TMA stage capacity: largest combined (own + foreign) segment
-    int mv_minb = 4;          // TMA matvec: resident CTAs per SM (launch bounds)
     int hcap = 0;
     size_t tma_smem = 0, tma_rhs_smem = 0;
     DBuf<int> d_hpad, d_fpos;
@@ -522,6 +521,7 @@ struct dxpbd_scene {
     int nb = 1;                                        // K = 1 forward projection: constraints per thread
     int nb_rep = 2;                                    // K = 1 replay: constraints per thread
     int rep_minb = 3;                                  // K = 1 replay: launch-bounds CTAs per SM (measured best)
+    bool defer_u = true;                               // PCG: u += alpha p deferred into the next matvec (measured best)
     DBuf<float3> r1, s1, w1;                           // single-reduction PCG ping-pong partners
     bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
                                                        // measured 10 % slower than matvec + update)
@@ -848,6 +848,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     TmaTiles tt = s->tma_tiles();
     // single-reduction PCG (kernels.cuh k_cgcg_tma): cloth-only TMA path
     const bool cgcg = s->use_tma && !s->T && s->cgcg;
+    const bool defer = s->use_tma && !cgcg && s->defer_u;   // u update deferred into the next matvec
     CGCGBufs cb{s->ax.p, s->p.p, {s->r.p, s->r1.p}, {s->p1.p, s->s1.p}, {s->q.p, s->w1.p}, s->rhs.p};
     auto cgcg_launch = [&](int i) {
         if (s->cgcg_minb == 3)
@@ -872,10 +873,9 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
                 ++launches;
                 continue;
             }
-            if (s->use_tma && s->mv_minb == 5)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 5><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
-            else if (s->use_tma)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs)));
+            if (s->use_tma)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
+                                                                                                         defer ? s->ax.p : nullptr)));
             else if (s->qf == 1)
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             else
@@ -885,7 +885,10 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
                 LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), s->t_Q.p, bufs, xw, cs));
                 ++launches;
             }
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
+            if (defer)
+                LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<false><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
+            else
+                LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<true><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
             ++launches;
         }
         // convergence check: rr of the last completed iteration against |b|^2
@@ -901,6 +904,10 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         }
         if (iters_out >= 0) break;
         relres_out = std::sqrt(s->h_scal[it * 4 + 2] / bb);
+    }
+    if (defer && iters_out > 0) {
+        LAUNCH(DXPBD_K_CG_UPDATE, k_cg_ufinal<<<nblk(V), kBlock, 0, st>>>(V, iters_out, bufs, cs));
+        ++launches;
     }
     DX_CHECK_CUDA(cudaGetLastError());
     if (iters_out < 0) {
@@ -988,6 +995,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_NB")) s->nb = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
+    if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
 
     cudaStream_t st = 0;
 
@@ -1154,8 +1162,6 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 s->tma_smem = tma_smem_bytes(s->hcap, s->capm);
                 s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                if (const char *ev = getenv("DXPBD_MV_MINB")) s->mv_minb = atoi(ev);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 if (const char *ev = getenv("DXPBD_CGCG_MINB")) s->cgcg_minb = atoi(ev);

@@ -796,7 +796,8 @@ DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const flo
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, int V,
                                                                   const float *__restrict__ Qc, CGBufs B,
-                                                                  const float *__restrict__ wv, CGState s, int t0 = 0) {
+                                                                  const float *__restrict__ wv, CGState s, int t0 = 0,
+                                                                  float3 *__restrict__ ufix = nullptr) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
@@ -838,6 +839,11 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
     float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
     const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
+    float alpha_prev = 0.f;
+    if (ufix && it > 0) {
+        const double pq = s.sc[it * 4 + 0];
+        alpha_prev = pq > 0.0 ? (float)(s.sc[(it - 1) * 4 + 1] / pq) : 0.f;
+    }
     float acc[1] = {0.f};
     float3 ro[NO], po[NO];
 #pragma unroll
@@ -876,6 +882,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
                 acc[0] += dot3(pv, qv);
             }
             if (it > 0) pnew[v] = pv;
+            if (ufix && it > 0) ufix[v] = ufix[v] + alpha_prev * po[u];   // deferred u += alpha_{it-1} p_{it-1}
         }
         if (i < kTileV) {
             sp[so[u]] = f4of(pv);
@@ -1362,6 +1369,7 @@ __global__ void k_cg_update2(int V, int it, CGBufs B, const float *__restrict__ 
 
 // Vectorized PCG update: 4 vertices per thread read as 3 float4 per field of the packed float3
 // arrays (16-byte accesses); same arithmetic as k_cg_update2.  Vertices [4*nq, V) by k_cg_update2.
+template <bool UPD_U>
 __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ wv, CGState s) {
     if (cg_done(s, it + 1)) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1379,7 +1387,8 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         float uu[12], rr[12], pp[12], qq[12];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float4 a = u[3 * t + c], b = r[3 * t + c], cc = p[3 * t + c], d = q[3 * t + c];
+            const float4 a = UPD_U ? u[3 * t + c] : make_float4(0.f, 0.f, 0.f, 0.f), b = r[3 * t + c],
+                         cc = UPD_U ? p[3 * t + c] : a, d = q[3 * t + c];
             uu[4 * c] = a.x; uu[4 * c + 1] = a.y; uu[4 * c + 2] = a.z; uu[4 * c + 3] = a.w;
             rr[4 * c] = b.x; rr[4 * c + 1] = b.y; rr[4 * c + 2] = b.z; rr[4 * c + 3] = b.w;
             pp[4 * c] = cc.x; pp[4 * c + 1] = cc.y; pp[4 * c + 2] = cc.z; pp[4 * c + 3] = cc.w;
@@ -1395,7 +1404,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            u[3 * t + c] = make_float4(uu[4 * c], uu[4 * c + 1], uu[4 * c + 2], uu[4 * c + 3]);
+            if (UPD_U) u[3 * t + c] = make_float4(uu[4 * c], uu[4 * c + 1], uu[4 * c + 2], uu[4 * c + 3]);
             r[3 * t + c] = make_float4(rr[4 * c], rr[4 * c + 1], rr[4 * c + 2], rr[4 * c + 3]);
         }
     } else if (t == nq) {   // tail vertices
@@ -1407,7 +1416,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
             float3 uv = B.u[v], rv = B.r[v], pv = p[v], qv = B.q[v];
             uv = uv + alpha * pv;
             rv = w > 0.f ? rv - alpha * qv : make_float3(0.f, 0.f, 0.f);
-            B.u[v] = uv;
+            if (UPD_U) B.u[v] = uv;
             B.r[v] = rv;
             const float r2 = dot3(rv, rv);
             acc[0] += w * r2;
@@ -1415,6 +1424,18 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         }
     }
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
+}
+
+// Deferred solution update (UPD_U = false above): the matvec of iteration it adds
+// alpha_{it-1} p_{it-1} to u in its vertex phase; after convergence at K iterations this adds the
+// last term alpha_{K-1} p_{K-1}.
+__global__ void k_cg_ufinal(int V, int K, CGBufs B, CGState s) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V || K <= 0) return;
+    const double pq = s.sc[K * 4 + 0];
+    const float alpha = pq > 0.0 ? (float)(s.sc[(K - 1) * 4 + 1] / pq) : 0.f;
+    const float3 *__restrict__ p = ((K - 1) & 1) ? B.p1 : B.p0;
+    B.u[v] = B.u[v] + alpha * p[v];
 }
 
 // after the solve: y_n = y_{n+1} + u_n ; dphi/df_frame += dt^2 y_n (R8)
