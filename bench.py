@@ -167,11 +167,12 @@ def algo_bytes(cls, st, units_per_launch=None):
         return 144.0 * units_per_launch
     if cls == "dist_replay":    # + Q 16 + foreign slot 4 (+ its fQ copy for foreign constraints)
         return (164.0 + 16.0 * NF / max(E, 1)) * units_per_launch
-    if cls == "cg_dist":        # TMA matvec: cpair 4 + Q 16 per constraint, fpair 4 + fQ 16 per foreign entry,
-        # hlist 4 + (r, p_old 24 + w 4) per halo slot, own r 12 + p_old 12 + w 4 + p_new 12 + q 12 (float3 fields)
-        return 20.0 * E + 20.0 * NF + 32.0 * H + 52.0 * V
-    if cls == "cg_update":      # u r/w 24, r r/w 24, p 12, q 12, w 4
-        return 76.0 * V
+    if cls == "cg_dist":        # TMA matvec: slot pair 4 + Q 16 per entry of the combined segments (own constraints
+        # and foreign copies), halo id 4 + slot 2 + (w 4, r 12, p_old 12) per halo entry, own w 4 + slot 2 + r 12 +
+        # p_old 12 + p_new 12 + q 12 and the deferred u += alpha p (u r/w 24)
+        return 20.0 * E + 20.0 * NF + 34.0 * H + 78.0 * V
+    if cls == "cg_update":      # r r/w 24, q 12, w 4 (u is updated in the next matvec)
+        return 40.0 * V
     if cls == "predict":        # x_n 32, x_{n-1} 32, f 12, out 32
         return 108.0 * V
     return None
@@ -367,9 +368,11 @@ def run_ours(a):
     if sst["tma"]:
         S = substeps_total
         mv = algo_bytes("cg_dist", sst)
+        # per substep: predict, projection, replay, rhs (~ one matvec + b, r0, u0, p0 and the extrapolation
+        # inputs: 60 B/vertex), the final u += alpha p (36 B/vertex), adjoint accumulation (~40 B/vertex)
         per_step = (S * (algo_bytes("predict", sst) + algo_bytes("dist_project", sst, E * a.iterations)
                          + algo_bytes("dist_replay", sst, E * a.iterations)
-                         + mv + 36.0 * V + 40.0 * V)
+                         + mv + 60.0 * V + 36.0 * V + 40.0 * V)
                     + (cg_mv / a.steps) * mv + (cg_iters / a.steps) * algo_bytes("cg_update", sst))
         ach = per_step / (ms_per_step / 1e3) / 1e9
         step_roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
