@@ -522,6 +522,7 @@ struct dxpbd_scene {
     int nb_rep = 2;                                    // K = 1 replay: constraints per thread
     int rep_minb = 3;                                  // K = 1 replay: launch-bounds CTAs per SM (measured best)
     bool defer_u = true;                               // PCG: u += alpha p deferred into the next matvec (measured best)
+    int last_iters = 0;                                // PCG iterations of the previous solve (poll schedule)
     DBuf<float3> r1, s1, w1;                           // single-reduction PCG ping-pong partners
     bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
                                                        // measured 10 % slower than matvec + update)
@@ -862,11 +863,14 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         LAUNCH(DXPBD_K_CG_INIT, k_cg_start<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->r.p, s->p.p, xw, cs));
     int launches = 1;
     int it = 0;
-    const int chunk = 8;
+    // launches between host convergence polls: first the previous solve's count (consecutive
+    // substeps need nearly the same number), then small chunks; launches past convergence exit at once
+    int chunk = s->last_iters > 0 ? std::max(s->last_iters, 2) : 8;
     iters_out = -1;
     relres_out = 0.0;
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
+        chunk = 2;
         for (; it < end; ++it) {
             if (cgcg) {
                 cgcg_launch(it);
@@ -905,6 +909,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         if (iters_out >= 0) break;
         relres_out = std::sqrt(s->h_scal[it * 4 + 2] / bb);
     }
+    if (iters_out >= 0) s->last_iters = iters_out;
     if (defer && iters_out > 0) {
         LAUNCH(DXPBD_K_CG_UPDATE, k_cg_ufinal<<<nblk(V), kBlock, 0, st>>>(V, iters_out, bufs, cs));
         ++launches;
