@@ -123,3 +123,16 @@ def test_medium_cloth_full_size_backward_short():
     g = gpu_run(s, ("compliance", "x0"))
     o = oracle_run(s)
     _compare(g, o, ("compliance", "x0", "v0"))
+
+
+def test_large_cloth_full_size_substeps_bench_config():
+    """configs[4] in the bench's launch configuration (2944^2, dt = 1/600, forces, the same kernels
+    and launch shapes bench.py times), three consecutive substeps forward (velocities carried
+    between substeps): all positions vs the oracle.  (A full 10-substep frame agrees as well but
+    takes the fp64 oracle ~6 min.)"""
+    s = f32(large_cloth(frames=1, substeps=3, key_frames=(1,)).replace(frame_dt=3 / 600))
+    g = gpu_run(s, backward=False)
+    o = oracle_run(s, backward=False)
+    assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
+    step_err = np.abs((g["x"][-1] - g["x"][0]) - (o["x"][-1] - o["x"][0])).max()
+    assert step_err < 1e-5, step_err

@@ -97,3 +97,16 @@ def test_group_rejects_unsupported():
         api.dxpbd_group_create(**api.scene_kwargs(s), num_parts=2, grad_flags=api.flags("compliance"))
     with pytest.raises(api.DxpbdError):
         api.dxpbd_group_create(**{**api.scene_kwargs(s), "iterations": 2}, num_parts=2)
+
+
+def test_group_full_size_forward_bit_exact():
+    """configs[4] at full size (2944^2), 1 frame: 4 partitions reproduce the single scene bit for bit."""
+    api = _api()
+    s = f32(large_cloth(frames=1, key_frames=(1,)))
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=1)
+    api.dxpbd_forward(sc, s.x0, s.v0, s.forces, 1)
+    a = api.dxpbd_positions(sc, 1)
+    del sc
+    g = api.dxpbd_group_create(**api.scene_kwargs(s), num_parts=4, max_frames=1)
+    api.dxpbd_group_forward(g, s.x0, s.v0, s.forces, 1)
+    np.testing.assert_array_equal(api.dxpbd_group_positions(g, 1), a)
