@@ -186,22 +186,32 @@ def run_partitioned(a):
     import numpy as np
     import torch
     from paper_2301_01396_b200 import api
+    from paper_2301_01396_b200 import parallel as par
     from synth import large_cloth
-    torch.cuda.set_device(0)
+    env = par.init("nccl")
+    world, rank, local = env.world, env.rank, env.local_rank
+    torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
     side = 10.0 * (a.n - 1) / 2943.0
     s = large_cloth(n=a.n, frames=a.frames, substeps=a.substeps, iterations=a.iterations, seed=4, side=side,
                     with_forces=False, key_frames=tuple(k for k in (10, 20, 30) if k <= a.frames) or (a.frames,))
     V, E = s.num_vertices, len(s.dist_idx)
     g = torch.Generator(device="cpu").manual_seed(1234)
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", local)
     forces = (torch.randn((a.frames, V, 3), generator=g, dtype=torch.float32) * 0.1).to(dev)
     x0, v0 = (torch.as_tensor(t, dtype=torch.float32, device=dev) for t in (s.x0, s.v0))
     tg = torch.as_tensor(s.targets, dtype=torch.float32, device=dev)
     kf = np.asarray(s.key_frames, np.int32)
     t_create = time.perf_counter()
-    grp = api.dxpbd_group_create(**api.scene_kwargs(s), num_parts=a.partitions, max_frames=a.frames,
-                                 grad_flags=api.flags("forces"), cg_tol=a.cg_tol, cg_max_iter=1000)
+    kw = dict(max_frames=a.frames, grad_flags=api.flags("forces"), cg_tol=a.cg_tol, cg_max_iter=1000, device=local)
+    if world > 1:
+        # one partition per rank over NCCL; the NCCL id travels over the process group
+        import torch.distributed as dist
+        obj = [api.dxpbd_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        grp = api.dxpbd_group_create_dist(**api.scene_kwargs(s), rank=rank, world=world, nccl_id=obj[0], **kw)
+    else:
+        grp = api.dxpbd_group_create(**api.scene_kwargs(s), num_parts=a.partitions, **kw)
     t_create = time.perf_counter() - t_create
     del s
     gf = torch.empty((a.frames, V, 3), dtype=torch.float32, device=dev)
@@ -215,27 +225,35 @@ def run_partitioned(a):
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
+    par.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(a.steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.steps
+    par.barrier()
+    ms = par.reduce_max(e0.elapsed_time(e1), device=dev) / a.steps
     st = api.dxpbd_group_stats(grp)
+    if rank != 0:
+        par.shutdown()
+        return
     solves = E * a.iterations * a.frames * a.substeps
-    line = {"metric": METRIC, "value": solves / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": a.steps,
+    line = {"metric": METRIC, "value": solves / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"large_cloth {a.n}x{a.n} (BASELINE configs[4] shape), {a.frames} frames",
                        "vertices": V, "constraints": E, "frames": a.frames, "substeps": a.substeps,
-                       "parallelism": f"domain decomposition, {a.partitions} partitions on 1 GPU (serialized, "
-                                      "device-to-device halo exchange)"},
+                       "parallelism": (f"domain decomposition, {world} partitions on {world} GPUs (NCCL halo exchange)"
+                                       if world > 1 else
+                                       f"domain decomposition, {a.partitions} partitions on 1 GPU (serialized, "
+                                       "device-to-device halo exchange)")},
             "exchange": {"vertices_per_sweep": st["xchg_sweep"], "halo_vertices": st["xchg_halo"],
                          "cross_blocks": st["xchg_blocks"],
                          "bytes_per_substep_forward": 32.0 * st["xchg_sweep"]},
             "cg_iters_per_substep": st["cg_iters_total"] / max(st["solves"], 1), "create_s": t_create}
     print(json.dumps(line), flush=True)
+    par.shutdown()
 
 
 def run_ours(a):

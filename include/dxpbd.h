@@ -167,6 +167,14 @@ int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
  * the scene calls above. */
 typedef struct dxpbd_group dxpbd_group;
 int dxpbd_group_create(const dxpbd_scene_desc *desc, int32_t num_parts, dxpbd_group **out);
+/* Distributed group: this process holds partition `rank` of `world` (one GPU per process,
+ * desc->device); exchanges and PCG all-reduces go through NCCL on the call's stream.  nccl_id:
+ * 128 bytes from dxpbd_nccl_unique_id() on rank 0, broadcast by the caller.  NCCL is loaded at
+ * run time (the libnccl already in the process, else DXPBD_NCCL_LIB or libnccl.so.2).  All ranks
+ * call every group function collectively; positions and gradients are gathered on every rank. */
+int dxpbd_nccl_unique_id(void *out_128_bytes);
+int dxpbd_group_create_dist(const dxpbd_scene_desc *desc, int32_t rank, int32_t world, const void *nccl_id,
+                            dxpbd_group **out);
 int dxpbd_group_destroy(dxpbd_group *group);
 int dxpbd_group_forward(dxpbd_group *group, const float *x0, const float *v0, const float *forces,
                         int32_t num_frames, int32_t mem, void *stream);

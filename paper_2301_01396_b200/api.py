@@ -74,6 +74,8 @@ def lib():
             "dxpbd_kernel_times": ([vp, vp, vp, i32], ctypes.c_int),
             "dxpbd_group_create": ([ctypes.POINTER(SceneDesc), i32, ctypes.POINTER(vp)], ctypes.c_int),
             "dxpbd_group_destroy": ([vp], ctypes.c_int),
+            "dxpbd_nccl_unique_id": ([vp], ctypes.c_int),
+            "dxpbd_group_create_dist": ([ctypes.POINTER(SceneDesc), i32, i32, vp, ctypes.POINTER(vp)], ctypes.c_int),
             "dxpbd_group_forward": ([vp, vp, vp, vp, i32, i32, vp], ctypes.c_int),
             "dxpbd_group_positions": ([vp, i32, vp, i32, vp], ctypes.c_int),
             "dxpbd_group_backward": ([vp, i32, vp, vp, vp, i32, vp, vp], ctypes.c_int),
@@ -94,7 +96,7 @@ EXPORTED = ["dxpbd_create", "dxpbd_destroy", "dxpbd_forward", "dxpbd_positions",
             "dxpbd_grads", "dxpbd_set_params", "dxpbd_coloring", "dxpbd_stats", "dxpbd_last_error",
             "dxpbd_version", "dxpbd_profile", "dxpbd_kernel_times", "dxpbd_group_create", "dxpbd_group_destroy",
             "dxpbd_group_forward", "dxpbd_group_positions", "dxpbd_group_backward", "dxpbd_group_grads",
-            "dxpbd_group_stats"]
+            "dxpbd_group_stats", "dxpbd_nccl_unique_id", "dxpbd_group_create_dist"]
 
 KCLASSES = ["predict", "dist_project", "contact_project", "tet_project", "dist_replay", "contact_replay",
             "tet_replay", "cg_vertex", "cg_dist", "cg_tet", "cg_update", "cg_init", "rhs", "adjoint", "grads",
@@ -349,6 +351,23 @@ def dxpbd_group_create(x_rest, inv_mass, num_parts: int = 2, **kw) -> DxGroup:
     out = ctypes.c_void_p()
     _check(lib().dxpbd_group_create(ctypes.byref(d), int(num_parts), ctypes.byref(out)), "dxpbd_group_create")
     return DxGroup(out.value, int(num_parts), *dims)
+
+
+def dxpbd_nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to be broadcast to the other ranks."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().dxpbd_nccl_unique_id(buf), "dxpbd_nccl_unique_id")
+    return buf.raw
+
+
+def dxpbd_group_create_dist(x_rest, inv_mass, rank: int, world: int, nccl_id: bytes, **kw) -> DxGroup:
+    """Partition `rank` of a world-size domain decomposition, one GPU per process (NCCL transport)."""
+    d, keep, dims = _desc(x_rest, inv_mass, **kw)
+    uid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    out = ctypes.c_void_p()
+    _check(lib().dxpbd_group_create_dist(ctypes.byref(d), int(rank), int(world), uid, ctypes.byref(out)),
+           "dxpbd_group_create_dist")
+    return DxGroup(out.value, int(world), *dims)
 
 
 def dxpbd_group_destroy(group: DxGroup):

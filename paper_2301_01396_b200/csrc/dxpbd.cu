@@ -3,6 +3,8 @@
 // substep loop with checkpoints, the backward loop (replay -> PCG -> adjoint update ->
 // gradients).  Every arithmetic step of the path runs in the kernels of kernels.cuh.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -11,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <memory>
 #include <thread>
 #include <utility>
 #include <vector>

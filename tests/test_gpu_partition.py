@@ -110,3 +110,21 @@ def test_group_full_size_forward_bit_exact():
     g = api.dxpbd_group_create(**api.scene_kwargs(s), num_parts=4, max_frames=1)
     api.dxpbd_group_forward(g, s.x0, s.v0, s.forces, 1)
     np.testing.assert_array_equal(api.dxpbd_group_positions(g, 1), a)
+
+
+def test_distributed_group_world1_equals_single():
+    """The NCCL transport path (dxpbd_group_create_dist) with a one-rank communicator: the same
+    schedule as the in-process group with NCCL all-reduces; equals the single scene exactly."""
+    api = _api()
+    s = _scene(n=64, frames=2, substeps=3)
+    a = _single(s)
+    uid = api.dxpbd_nccl_unique_id()
+    g = api.dxpbd_group_create_dist(**api.scene_kwargs(s), rank=0, world=1, nccl_id=uid, max_frames=s.frames,
+                                    grad_flags=api.flags(*GRADS), cg_max_iter=1000)
+    api.dxpbd_group_forward(g, s.x0, s.v0, s.forces, s.frames)
+    for f in range(s.frames + 1):
+        np.testing.assert_array_equal(api.dxpbd_group_positions(g, f), a["x"][f])
+    loss = api.dxpbd_group_backward(g, s.key_frames, s.targets)
+    assert loss == pytest.approx(a["loss"], rel=1e-6)
+    for k in GRADS:
+        assert rel_l2(api.dxpbd_group_grads(g, k), a[k]) < 1e-5
