@@ -668,7 +668,13 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
             float *eo = want_e ? s->ed.p : nullptr;
-            if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3)
+            const bool last_color = c == s->n_dist_colors - 1 && !s->T && !s->NC;   // nothing reads its iterate
+            if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3 && last_color)
+                LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 3, false><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
+                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p)));
+            else if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3)
                 LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 3><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
                     s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,

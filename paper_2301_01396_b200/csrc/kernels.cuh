@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kBlock) k_dist_project1(int begin, int count, 
 // iterate, stores the closed-form block Q_j at its TMA-layout position tpos[j] (and the foreign copy),
 // and the compliance control vector e_j = t n, t = -dl / (dt^2 J) (the general replay with
 // lambda_0 = T = 0).  Same arithmetic as k_dist_replay<true, true, 1>.
-template <int NB, int MINB = 1>
+template <int NB, int MINB = 1, bool WRITE_X = true>
 __global__ void __launch_bounds__(kBlock, MINB) k_dist_replay1(int begin, int count, int E, const int2 *__restrict__ idx,
                                                          const float *__restrict__ rest,
                                                          const float *__restrict__ alpha, float inv_dt2,
@@ -221,9 +221,11 @@ __global__ void __launch_bounds__(kBlock, MINB) k_dist_replay1(int begin, int co
             const float iJ = 1.f / o.J;
             const float tt = (-(0.f + o.dl) * inv_dt2 - at * 0.f) * iJ;
             ec = ec + tt * o.n;
-            dist_apply(pa[k], pb[k], o);
-            x[e[k].x] = pa[k];
-            x[e[k].y] = pb[k];
+            if (WRITE_X) {   // the last color's iterate is not read again (checkpoint x_{n+1} exists)
+                dist_apply(pa[k], pb[k], o);
+                x[e[k].x] = pa[k];
+                x[e[k].y] = pb[k];
+            }
         }
         Q4[tp[k]] = q4;
         if (fp[k] >= 0) fQ[fp[k]] = q4;
