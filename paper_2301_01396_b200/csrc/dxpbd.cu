@@ -495,6 +495,7 @@ struct dxpbd_scene {
     DBuf<int4> t_idx;
     DBuf<double> t_Dm, t_vol;
     DBuf<float> t_a, t_b, t_Q, t_e, t_g, lam_t;
+    DBuf<double4> t_xsave;   // K = 1 tet replay: pre-update vertices of every tet [4T]
     DBuf<int32_t> t_perm;
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
     TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
@@ -711,10 +712,17 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
                 int b = s->tet_off[c], cnt = s->tet_off[c + 1] - b;
                 if (!cnt) continue;
                 const int tb = (cnt + 127) / 128;
-                if (first && last) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<true, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
+                if (first && last)   // K = 1: iterate only, derivative blocks of all tets after the colors
+                    LAUNCH(DXPBD_K_TET_REPLAY, (k_tet_replay<true, true, 1><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x,
+                                                                                               s->t_xsave.p)));
                 else if (first) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<true, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
                 else if (last) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
                 else LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
+                ++launches;
+            }
+            if (first && last) {
+                LAUNCH(DXPBD_K_TET_REPLAY, (k_tet_replay<true, true, 2><<<(s->T + 127) / 128, 128, 0, st>>>(
+                                               0, s->T, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x, s->t_xsave.p)));
                 ++launches;
             }
         }
@@ -802,6 +810,7 @@ BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frame
         if (s->t_Q.n < 45 * T) s->t_Q.alloc(45 * T);
         if (((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) && s->t_e.n < 18 * T) s->t_e.alloc(18 * T);
         if (s->t_g.n < 2 * T) s->t_g.alloc(2 * T);
+        if (s->iterations == 1 && s->t_xsave.n < 4 * T) s->t_xsave.alloc(4 * T);
         if (s->iterations > 1 && s->ts_lam.n < 2 * T) {
             s->ts_lam.alloc(2 * T); s->ts_S.alloc(18 * T); s->ts_Dt.alloc(45 * T); s->ts_Tu.alloc(4 * T); s->ts_e.alloc(18 * T);
         }

@@ -278,16 +278,30 @@ struct TetScratch {
 //   e~_u += Sum_a t_{u,a} P_a ;  T_u += t_u
 //   dat_D/da = -2 at_D / a, dat_H/db = -2 at_H / b, dC_H/da = -2a/b^2, dC_H/db = 2a^2/b^3.
 // After the last iteration: Qt~ = psd(-sym D~) (45 floats, upper triangle) and e~ (18 floats).
-template <bool FIRST, bool LAST>
+// MODE 0: one pass per color (any K).  K = 1 splits it in two so the heavy derivative algebra and
+// the 9x9 PSD projection run once over all tets instead of color by color (a color is a few
+// thousand tets: long per-thread chains on a mostly idle GPU):
+//   MODE 1 (per color): regenerate the iterate (tet_core / tet_apply, as the forward) and save the
+//           tet's pre-update vertices to xsave[4 j .. 4 j + 3];
+//   MODE 2 (all tets, one launch): the derivative blocks from the saved vertices (same arithmetic
+//           as MODE 0 with FIRST = LAST = true), no position writes.
+template <bool FIRST, bool LAST, int MODE = 0>
 __global__ void __launch_bounds__(128) k_tet_replay(int begin, int count, TetDev D, double inv_dt2, TetScratch sc, int pd,
                                                     float *__restrict__ Qt, float *__restrict__ eout,
-                                                    double4 *__restrict__ x) {
+                                                    double4 *__restrict__ x, double4 *__restrict__ xsave = nullptr) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= count) return;
     const int j = begin + tid;
     const int T = D.T;
     const int4 id = D.idx[j];
-    double4 xs[4] = {x[id.x], x[id.y], x[id.z], x[id.w]};
+    double4 xs[4];
+    if (MODE == 2) {
+        for (int k = 0; k < 4; ++k) xs[k] = xsave[4 * (size_t)j + k];
+    } else {
+        xs[0] = x[id.x]; xs[1] = x[id.y]; xs[2] = x[id.z]; xs[3] = x[id.w];
+    }
+    if (MODE == 1)
+        for (int k = 0; k < 4; ++k) xsave[4 * (size_t)j + k] = xs[k];
     tr c[4][3];
     tet_load_c(D, j, c);
     const tr a = D.ta[j], b = D.tb[j];
@@ -310,6 +324,16 @@ __global__ void __launch_bounds__(128) k_tet_replay(int begin, int count, TetDev
     const tr at0 = tet_at(D, j, 0, inv_dt2), at1 = tet_at(D, j, 1, inv_dt2);
     TetCore o;
     const bool ok = tet_core(xs, c, at0, at1, 1.0 + (a * a) / (b * b), lam0, o);
+    if (MODE == 1) {
+        if (ok) {
+            tet_apply(xs, o);
+            x[id.x] = xs[0];
+            x[id.y] = xs[1];
+            x[id.z] = xs[2];
+            x[id.w] = xs[3];
+        }
+        return;
+    }
     if (ok) {
         tr WP[2][9], sumP[9], Dx[9];
         tet_Wmul(o.K, o.P[0], WP[0]);
@@ -372,11 +396,13 @@ __global__ void __launch_bounds__(128) k_tet_replay(int begin, int count, TetDev
         }
         lam0[0] += o.dl[0];
         lam0[1] += o.dl[1];
-        tet_apply(xs, o);
-        x[id.x] = xs[0];
-        x[id.y] = xs[1];
-        x[id.z] = xs[2];
-        x[id.w] = xs[3];
+        if (MODE == 0) {
+            tet_apply(xs, o);
+            x[id.x] = xs[0];
+            x[id.y] = xs[1];
+            x[id.z] = xs[2];
+            x[id.w] = xs[3];
+        }
     }
     if (LAST) {
         float A[9][9];

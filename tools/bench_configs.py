@@ -1,0 +1,59 @@
+"""Full-length forward + adjoint of every BASELINE config (configs[0..4]) once on cuda:0 through the
+C-ABI, with each config's gradient families; prints one JSON line per config (ms per step, per
+substep, PCG iterations).  Not the driver's bench (bench.py times configs[4]); this records that
+the other four configs run at their full size and length.  Synthetic seeded inputs (synth/)."""
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+from paper_2301_01396_b200 import api  # noqa: E402
+from synth import as_float32_exact, garment, large_cloth, medium_cloth, tiny_cloth, volumetric_block  # noqa: E402
+
+CASES = [
+    ("configs[0] tiny_cloth 16x16, 30 frames x 10 substeps", lambda: tiny_cloth(), ("compliance", "v0")),
+    ("configs[1] medium_cloth 256x256 + sphere, 60 frames x 10", lambda: medium_cloth(), ("compliance", "x0")),
+    ("configs[2] volumetric_block 40^3 (~300k tets), 50 frames x 20", lambda: volumetric_block(), ("material",)),
+    ("configs[3] garment 512x512 tube + 12 capsules, 120 frames x 10", lambda: garment(), ("shape",)),
+    ("configs[4] large_cloth 2944x2944, 30 frames x 10", lambda: large_cloth(), ("forces",)),
+]
+
+
+def run(name, make, grads):
+    s = as_float32_exact(make())
+    dev = "cuda:0"
+    t = lambda a: None if a is None else torch.as_tensor(np.asarray(a, np.float32), device=dev)  # noqa: E731
+    t0 = time.perf_counter()
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=s.frames, grad_flags=api.flags(*grads), cg_max_iter=2000)
+    t_create = time.perf_counter() - t0
+    x0, v0, f, tg = t(s.x0), t(s.v0), t(s.forces), t(s.targets)
+    w = t(s.weights) if s.weights is not None else None
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    api.dxpbd_forward(sc, x0, v0, f, s.frames)
+    ev[1].record()
+    loss = api.dxpbd_backward(sc, s.key_frames, tg, w)
+    for g in grads:
+        api.dxpbd_grads(sc, g)
+    ev[2].record()
+    torch.cuda.synchronize()
+    st = api.dxpbd_stats(sc)
+    N = s.frames * s.substeps
+    fwd, tot = ev[0].elapsed_time(ev[1]), ev[0].elapsed_time(ev[2])
+    line = dict(config=name, vertices=s.num_vertices, constraints=len(s.dist_idx), tets=len(s.tet_idx),
+                colliders=len(s.spheres) + len(s.cap_center), frames=s.frames, substeps=s.substeps, grads=list(grads),
+                ms_forward=fwd, ms_forward_adjoint=tot, ms_per_substep_fwd=fwd / N, ms_per_substep_fwd_adjoint=tot / N,
+                cg_iters_per_substep=st["cg_iters_total"] / max(st["solves"], 1), cg_iters_max=st["cg_iters_max"],
+                worst_relres=st["worst_relres"], tma_path=st["tma"], loss=loss, create_s=t_create)
+    print(json.dumps(line), flush=True)
+    del sc
+
+
+if __name__ == "__main__":
+    which = [int(a) for a in sys.argv[1:]] or range(len(CASES))
+    for i in which:
+        run(*CASES[i])
