@@ -724,6 +724,10 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
                 LAUNCH(DXPBD_K_TET_REPLAY, (k_tet_replay<true, true, 2><<<(s->T + 127) / 128, 128, 0, st>>>(
                                                0, s->T, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x, s->t_xsave.p)));
                 ++launches;
+                if (s->pd) {
+                    LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p));
+                    ++launches;
+                }
             }
         }
         if (s->NC) {

@@ -212,37 +212,49 @@ __global__ void __launch_bounds__(128) k_tet_project(int begin, int count, TetDe
 
 // 9x9 symmetric PSD projection by cyclic Jacobi (R5), in place on A (full), V scratch.
 DX_INLINE void psd9(float (&A)[9][9]) {
+    // cyclic Jacobi; every index is a compile-time constant (fully unrolled rotations) so A and V
+    // stay in registers (a rolled loop with runtime indices puts both in local memory)
     float V[9][9];
 #pragma unroll
     for (int i = 0; i < 9; ++i)
 #pragma unroll
         for (int j = 0; j < 9; ++j) V[i][j] = i == j ? 1.f : 0.f;
     float scale = 0.f;
+#pragma unroll
     for (int i = 0; i < 9; ++i)
+#pragma unroll
         for (int j = 0; j < 9; ++j) scale += fabsf(A[i][j]);
     if (scale == 0.f) return;
+#pragma unroll 1
     for (int sweep = 0; sweep < 12; ++sweep) {
         float off = 0.f;
+#pragma unroll
         for (int p = 0; p < 9; ++p)
+#pragma unroll
             for (int q = p + 1; q < 9; ++q) off += fabsf(A[p][q]);
         if (off <= 1e-8f * scale) break;
+#pragma unroll
         for (int p = 0; p < 8; ++p) {
+#pragma unroll
             for (int q = p + 1; q < 9; ++q) {
                 const float apq = A[p][q];
                 if (fabsf(apq) < 1e-30f) continue;
                 const float theta = (A[q][q] - A[p][p]) / (2.f * apq);
                 const float tt = copysignf(1.f, theta) / (fabsf(theta) + sqrtf(theta * theta + 1.f));
                 const float cc = rsqrtf(tt * tt + 1.f), ss = tt * cc;
+#pragma unroll
                 for (int k = 0; k < 9; ++k) {
                     const float akp = A[k][p], akq = A[k][q];
                     A[k][p] = cc * akp - ss * akq;
                     A[k][q] = ss * akp + cc * akq;
                 }
+#pragma unroll
                 for (int k = 0; k < 9; ++k) {
                     const float apk = A[p][k], aqk = A[q][k];
                     A[p][k] = cc * apk - ss * aqk;
                     A[q][k] = ss * apk + cc * aqk;
                 }
+#pragma unroll
                 for (int k = 0; k < 9; ++k) {
                     const float vkp = V[k][p], vkq = V[k][q];
                     V[k][p] = cc * vkp - ss * vkq;
@@ -252,14 +264,35 @@ DX_INLINE void psd9(float (&A)[9][9]) {
         }
     }
     float l[9];
+#pragma unroll
     for (int i = 0; i < 9; ++i) l[i] = fmaxf(A[i][i], 0.f);
+#pragma unroll
     for (int i = 0; i < 9; ++i)
+#pragma unroll
         for (int j = i; j < 9; ++j) {
             float s = 0.f;
+#pragma unroll
             for (int k = 0; k < 9; ++k) s += l[k] * V[i][k] * V[j][k];
             A[i][j] = s;
             A[j][i] = s;
         }
+}
+
+// PD projection (R5) of every tet's F-space block in place: Qt~ <- psd(Qt~) (45 floats, upper
+// triangle, SoA), one thread per tet with the 9x9 Jacobi in registers.
+__global__ void __launch_bounds__(128) k_tet_psd(int T, float *__restrict__ Qt) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= T) return;
+    float A[9][9];
+#pragma unroll
+    for (int p = 0; p < 9; ++p)
+#pragma unroll
+        for (int q = p; q < 9; ++q) A[p][q] = A[q][p] = Qt[(size_t)(p * 9 - (p * (p - 1)) / 2 + (q - p)) * T + j];
+    psd9(A);
+#pragma unroll
+    for (int p = 0; p < 9; ++p)
+#pragma unroll
+        for (int q = p; q < 9; ++q) Qt[(size_t)(p * 9 - (p * (p - 1)) / 2 + (q - p)) * T + j] = A[p][q];
 }
 
 // Running state of the differentiable replay (iterations > 1), SoA per tet.
@@ -406,15 +439,15 @@ __global__ void __launch_bounds__(128) k_tet_replay(int begin, int count, TetDev
     }
     if (LAST) {
         float A[9][9];
-        {
-            int m = 0;
-            for (int p = 0; p < 9; ++p)
-                for (int q = p; q < 9; ++q, ++m) A[p][q] = A[q][p] = (float)(-Dt[m]);
-        }
-        if (pd) psd9(A);
-        int m = 0;
+#pragma unroll
         for (int p = 0; p < 9; ++p)
-            for (int q = p; q < 9; ++q) Qt[(size_t)(m++) * T + j] = A[p][q];
+#pragma unroll
+            for (int q = p; q < 9; ++q) A[p][q] = A[q][p] = (float)(-Dt[p * 9 - (p * (p - 1)) / 2 + (q - p)]);
+        if (pd && MODE != 2) psd9(A);   // MODE 2: k_tet_psd projects all tets afterwards
+#pragma unroll
+        for (int p = 0; p < 9; ++p)
+#pragma unroll
+            for (int q = p; q < 9; ++q) Qt[(size_t)(p * 9 - (p * (p - 1)) / 2 + (q - p)) * T + j] = A[p][q];
         if (eout)
             for (int k = 0; k < 9; ++k) {
                 eout[(size_t)k * T + j] = (float)e[0][k];
