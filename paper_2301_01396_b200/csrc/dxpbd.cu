@@ -500,8 +500,16 @@ struct dxpbd_scene {
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
     TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
     TmaTiles tma_tiles() const {
-        return TmaTiles{n_dist_colors, ntiles, hcap, capm, d_tseg.p, d_cpair.p, d_hpad.p, d_Qt.p, d_vslot.p, d_hslot.p};
+        return TmaTiles{n_dist_colors, ntiles, hcap, capm, d_tseg.p, d_cpair.p, d_hpad.p, qt_read ? qt_read : d_Qt.p,
+                        d_vslot.p, d_hslot.p};
     }
+    // replay / PCG overlap (backward): the replay of substep n-1 runs on `aux` while the PCG of
+    // substep n runs on the caller's stream; Q blocks alternate between d_Qt and d_Qt2
+    DBuf<float4> d_Qt2;
+    float4 *qt_read = nullptr, *qt_write = nullptr;   // null: d_Qt
+    cudaStream_t aux = nullptr, hi = nullptr;   // aux: replay (lowest priority), hi: PCG path (highest)
+    cudaEvent_t ev_rep[2] = {nullptr, nullptr}, ev_pcg[2] = {nullptr, nullptr}, ev_go = nullptr, ev_end = nullptr;
+    bool overlap = true;
     // colliders
     DBuf<float> sph, cap_c, cap_a, cap_r0, cap_L0, cap_Rb, cap_Lb, beta;
     DBuf<Collider> cols;
@@ -651,6 +659,7 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
 // ------------------------------------------------------------------ replay of substep n
 int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int V = s->V, E = s->E;
+    float4 *qtw = s->qt_write ? s->qt_write : s->d_Qt.p;   // TMA-layout block buffer written
     const int frame = n / s->substeps;
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
     double4 *x = s->xr.p;
@@ -673,28 +682,28 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3 && last_color)
                 LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 3, false><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
-                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
-                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p)));
+                    s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, qtw)));
             else if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3)
                 LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 3><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
-                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
-                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p)));
+                    s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, qtw)));
             else if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 4)
                 LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 4><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
-                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
-                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p)));
+                    s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, qtw)));
             else if (first && last && s->qf == 1 && s->nb_rep == 2)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay1<2><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
-                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
-                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p));
+                    s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, qtw));
             else if (first && last && s->qf == 1)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay1<1><<<nblk(cnt), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
-                    s->use_tma ? s->d_Qt.p : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
-                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, s->d_Qt.p));
+                    s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, qtw));
             else if (first && last)
                 LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
             else if (first)
@@ -958,6 +967,10 @@ int dxpbd_destroy(dxpbd_scene *s) {
     cudaSetDevice(s->device);
     if (s->h_scal) cudaFreeHost(s->h_scal);
     for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : {s->ev_rep[0], s->ev_rep[1], s->ev_pcg[0], s->ev_pcg[1], s->ev_go, s->ev_end})
+        if (e) cudaEventDestroy(e);
+    if (s->aux) cudaStreamDestroy(s->aux);
+    if (s->hi) cudaStreamDestroy(s->hi);
     delete s;
     return DXPBD_OK;
 }
@@ -1023,6 +1036,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_OVERLAP")) s->overlap = atoi(ev) != 0;
 
     cudaStream_t st = 0;
 
@@ -1361,10 +1375,51 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     const float *Qc = s->NC ? s->Qc.p : nullptr;
     // PCG start fused into the TMA rhs kernel (no tet rhs pass after it, standard PCG)
     const bool fuse_start = s->use_tma && !s->T && !(s->cgcg);
-    for (int n = std::min(N, last_key_state) - 1; n >= 0; --n) {
+    // replay of substep n-1 on the aux stream during the PCG of substep n (independent work: the
+    // replay reads only checkpoints); blocks double-buffered, ordered by events
+    const bool ovl = s->overlap && s->use_tma && !s->T && !s->NC && !g_comp && !s->cgcg;
+    cudaStream_t user_st = st;
+    const int n_hi = std::min(N, last_key_state) - 1;
+    if (ovl && n_hi >= 0) {
+        if (s->d_Qt2.n < s->d_Qt.n) s->d_Qt2.alloc(s->d_Qt.n);
+        if (!s->aux) {
+            int least = 0, greatest = 0;
+            DX_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            DX_CHECK_CUDA(cudaStreamCreateWithPriority(&s->aux, cudaStreamNonBlocking, least));
+            DX_CHECK_CUDA(cudaStreamCreateWithPriority(&s->hi, cudaStreamNonBlocking, greatest));
+            for (int k = 0; k < 2; ++k) {
+                DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_rep[k], cudaEventDisableTiming));
+                DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_pcg[k], cudaEventDisableTiming));
+            }
+            DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_go, cudaEventDisableTiming));
+            DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_end, cudaEventDisableTiming));
+        }
+        DX_CHECK_CUDA(cudaEventRecord(s->ev_go, st));   // inputs of this call are on `st`
+        DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_go, 0));
+        // the PCG path runs on the high-priority stream; the replay fills the SMs it leaves idle
+        DX_CHECK_CUDA(cudaStreamWaitEvent(s->hi, s->ev_go, 0));
+        user_st = st;
+        st = s->hi;
+        s->qt_write = (n_hi & 1) ? s->d_Qt2.p : s->d_Qt.p;
+        launches += replay_substep(s, n_hi, s->aux);
+        DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[n_hi & 1], s->aux));
+    }
+    for (int n = n_hi; n >= 0; --n) {
         const int frame = n / sub;
         float *gf = g_forces ? s->g_force.p + (size_t)frame * V * 3 : nullptr;
-        launches += replay_substep(s, n, st);
+        if (ovl) {
+            if (n >= 1) {   // blocks of substep n-1 into the buffer PCG(n+1) finished reading
+                if (n + 1 <= n_hi) DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_pcg[(n - 1) & 1], 0));
+                s->qt_write = ((n - 1) & 1) ? s->d_Qt2.p : s->d_Qt.p;
+                launches += replay_substep(s, n - 1, s->aux);
+                DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[(n - 1) & 1], s->aux));
+            }
+            DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_rep[n & 1], 0));
+            s->qt_read = (n & 1) ? s->d_Qt2.p : s->d_Qt.p;
+        } else {
+            s->qt_write = s->qt_read = nullptr;
+            launches += replay_substep(s, n, st);
+        }
         // b = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1} and the warm-start residual r0 = b - A_n u_{n+1}
         // (one tiled pass, own vertices stored once); the PCG then starts from u_n := u_{n+1}.
         DX_CHECK_CUDA(cudaMemsetAsync(s->cg_sc.p, 0, sizeof(double) * (size_t)(s->cg_max_iter + 2) * 4, st));
@@ -1416,6 +1471,13 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             LAUNCH(DXPBD_K_GRADS, k_grad_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->t_e.p, s->y.p, s->t_g.p));
             ++launches;
         }
+        if (ovl) DX_CHECK_CUDA(cudaEventRecord(s->ev_pcg[n & 1], st));   // buffer n & 1 free again
+    }
+    s->qt_read = s->qt_write = nullptr;
+    if (st != user_st) {   // back onto the caller's stream
+        DX_CHECK_CUDA(cudaEventRecord(s->ev_end, st));
+        DX_CHECK_CUDA(cudaStreamWaitEvent(user_st, s->ev_end, 0));
+        st = user_st;
     }
     if (s->g_x0.n < (size_t)3 * V) s->g_x0.alloc((size_t)3 * V);
     if (s->g_v0.n < (size_t)3 * V) s->g_v0.alloc((size_t)3 * V);
