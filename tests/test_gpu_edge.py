@@ -136,3 +136,24 @@ def test_large_cloth_full_size_substeps_bench_config():
     assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
     step_err = np.abs((g["x"][-1] - g["x"][0]) - (o["x"][-1] - o["x"][0])).max()
     assert step_err < 1e-5, step_err
+
+
+def test_schedule_switches_do_not_change_results(monkeypatch):
+    """The performance schedules (replay / PCG stream overlap with double-buffered blocks, deferred
+    u += alpha p) reorder launches but not arithmetic: results equal the plain schedule bit for bit."""
+    api = _api()
+    s = f32(large_cloth(n=96, frames=2, substeps=3, side=10.0 * 95 / 2943.0, key_frames=(2,)).replace(frame_dt=3 / 600))
+
+    def run():
+        sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=2, grad_flags=api.flags("forces", "x0", "v0"))
+        api.dxpbd_forward(sc, s.x0, s.v0, s.forces, 2)
+        loss = api.dxpbd_backward(sc, s.key_frames, s.targets)
+        return loss, [api.dxpbd_grads(sc, k) for k in ("forces", "x0", "v0")]
+
+    la, ga = run()
+    for k, v in (("DXPBD_OVERLAP", "0"), ("DXPBD_DEFER_U", "0")):
+        monkeypatch.setenv(k, v)
+    lb, gb = run()
+    assert la == lb
+    for a, b in zip(ga, gb):
+        np.testing.assert_array_equal(a, b)
