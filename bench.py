@@ -360,7 +360,11 @@ def run_ours(a):
     peak = peaks["hbm_gbs"] if peaks else 6650.0
     roof = None
     if ktimes:
-        dom = max(ktimes, key=lambda k: ktimes[k][0])
+        # the replay runs on a low-priority stream overlapping the PCG, so its
+        # event-timed class duration includes time spent waiting behind the PCG: the dominant kernel is
+        # chosen among the critical-path classes
+        crit = {k: v for k, v in ktimes.items() if not k.endswith("_replay") and k != "predict"}
+        dom = max(crit or ktimes, key=lambda k: (crit or ktimes)[k][0])
         ms, cnt = ktimes[dom]
         sst = api.dxpbd_stats(sc)
         # color launches: constraints of one launch on average
@@ -372,7 +376,7 @@ def run_ours(a):
         work = {"cg_dist": cg_mv, "cg_update": cg_iters}.get(dom, 0) or cnt
         avg_ms = ms / work
         ach = (b / (avg_ms / 1e3)) / 1e9 if b else None
-        share = ms / sum(v[0] for v in ktimes.values())
+        share = ms / sum(v[0] for v in crit.values()) if crit else ms / sum(v[0] for v in ktimes.values())
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None, "traffic": TRAFFIC.get(dom), "kernel": dom,
                 "algorithmic_bytes_per_launch": b,
@@ -421,6 +425,8 @@ def run_ours(a):
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "create_s": t_create, "loss": loss,
             "kernel_ms_per_step": {k: v[0] / a.steps for k, v in ktimes.items()},
+            "kernel_ms_note": "event-timed per class; the replay classes (dist_replay and the replay's predict) run "
+                              "on a low-priority stream concurrently with the PCG, so their times include waiting",
         }
         print(json.dumps(line), flush=True)
     par.shutdown()
