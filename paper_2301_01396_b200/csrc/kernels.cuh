@@ -847,12 +847,13 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
         alpha_prev = pq > 0.0 ? (float)(s.sc[(it - 1) * 4 + 1] / pq) : 0.f;
     }
     float acc[1] = {0.f};
-    float3 ro[NO], po[NO];
+    float3 ro[NO], po[NO], uo[NO];
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
         const int v = min(v0 + (int)threadIdx.x + u * NT, V - 1);
         ro[u] = it > 0 ? B.r[v] : pnew[v];
         po[u] = it > 0 ? pold[v] : make_float3(0.f, 0.f, 0.f);
+        uo[u] = (ufix && it > 0) ? ufix[v] : make_float3(0.f, 0.f, 0.f);   // deferred update, same batch
     }
     float hw[NH];
     float3 hr[NH], hp[NH];
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
                 acc[0] += dot3(pv, qv);
             }
             if (it > 0) pnew[v] = pv;
-            if (ufix && it > 0) ufix[v] = ufix[v] + alpha_prev * po[u];   // deferred u += alpha_{it-1} p_{it-1}
+            if (ufix && it > 0) ufix[v] = uo[u] + alpha_prev * po[u];   // deferred u += alpha_{it-1} p_{it-1}
         }
         if (i < kTileV) {
             sp[so[u]] = f4of(pv);
