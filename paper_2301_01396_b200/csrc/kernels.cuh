@@ -1097,7 +1097,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V,
 
 // rhs (warm start): b = M u - Q_n y + dphi, r0 = b - A_n (u + du); A_dist applied tile-locally
 // with the same staging / slot layout as the matvec.
-__global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, const float *__restrict__ Qc,
+__global__ void __launch_bounds__(kTmaThreads, 3) k_rhs_tma(TmaTiles T, int V, const float *__restrict__ Qc,
                                                             const float3 *__restrict__ u, const float3 *__restrict__ uprev,
                                                             const float3 *__restrict__ uprev2,
                                                             const float3 *__restrict__ y,
@@ -1119,25 +1119,72 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
     __shared__ int4 sb[kMaxColors];
+    constexpr int NO = kTileV / kTmaThreads, NH = 2;
+    // ---- round trip 1: descriptors, slots, halo ids, inverse masses
     if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
+    float wo[NO];
+    int so[NO];
+#pragma unroll
+    for (int k = 0; k < NO; ++k) {
+        const int i = threadIdx.x + k * kTmaThreads;
+        wo[k] = wv[min(v0 + i, V - 1)];
+        so[k] = T.vslot[(size_t)t * kTileV + i];
+    }
+    int hv[NH], hs[NH];
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+        const int h = threadIdx.x + k * kTmaThreads;
+        hv[k] = h < hcap ? T.hpad[(size_t)t * hcap + h] : -1;
+        hs[k] = h < hcap ? T.hslot[(size_t)t * hcap + h] : 0;
+    }
     __syncthreads();
     if (threadIdx.x == kTmaThreads - 32) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
-    for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
-        float3 yv = make_float3(0.f, 0.f, 0.f), zv = yv, bb = yv, rr = yv;
+    // ---- round trip 2: all vector values of own and halo vertices in one batch
+    const float3 z3 = make_float3(0.f, 0.f, 0.f);
+    float3 yo[NO], uo[NO], po[NO], p2o[NO];
+    double4 xo[NO];
+    float3 to[NO];
+    float Wo[NO];
+#pragma unroll
+    for (int k = 0; k < NO; ++k) {
+        const int v = min(v0 + (int)threadIdx.x + k * kTmaThreads, V - 1);
+        yo[k] = f3(y[v]);
+        uo[k] = f3(u[v]);
+        po[k] = f3(uprev[v]);
+        p2o[k] = uprev2 ? f3(uprev2[v]) : z3;
+        if (target) {
+            xo[k] = xkey[v];
+            to[k] = make_float3(target[3 * v], target[3 * v + 1], target[3 * v + 2]);
+            Wo[k] = weights ? weights[v] : 1.f;
+        }
+    }
+    float3 hy[NH], hu[NH], hp[NH], hp2[NH];
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+        const int v = max(hv[k], 0);
+        hy[k] = f3(y[v]);
+        hu[k] = f3(u[v]);
+        hp[k] = f3(uprev[v]);
+        hp2[k] = uprev2 ? f3(uprev2[v]) : z3;
+    }
+#pragma unroll
+    for (int k = 0; k < NO; ++k) {
+        const int i = threadIdx.x + k * kTmaThreads;
+        float3 yv = z3, zv = z3, bb = z3, rr = z3;
         if (i < nv) {
             const int v = v0 + i;
-            const float w = wv[v];
-            yv = f3(y[v]);
-            const float3 uv = f3(u[v]);
+            const float w = wo[k];
+            yv = yo[k];
+            const float3 uv = uo[k];
             // warm start u0 = u + dv: linear 2u_{n+1} - u_{n+2}, or quadratic 3u_{n+1} - 3u_{n+2} + u_{n+3}
-            const float3 dv = uprev2 ? 2.f * uv - 3.f * f3(uprev[v]) + f3(uprev2[v]) : uv - f3(uprev[v]);
+            const float3 dv = uprev2 ? 2.f * uv - 3.f * po[k] + p2o[k] : uv - po[k];
             const float3 u0 = uv + dv;
             zv = yv + u0;
-            u0out[v] = w > 0.f ? u0 : make_float3(0.f, 0.f, 0.f);
+            u0out[v] = w > 0.f ? u0 : z3;
             if (w > 0.f) {
                 bb = (1.f / w) * uv;
                 rr = (-1.f / w) * dv;
@@ -1148,30 +1195,35 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_rhs_tma(TmaTiles T, int V, c
                     rr = rr - sym3_mul(A, zv);
                 }
                 if (target) {
-                    double4 x = xkey[v];
-                    float W = weights ? weights[v] : 1.f;
-                    float3 g = W * make_float3((float)(x.x - target[3 * v]), (float)(x.y - target[3 * v + 1]),
-                                               (float)(x.z - target[3 * v + 2]));
+                    const double4 x = xo[k];
+                    const float3 g = Wo[k] * make_float3((float)(x.x - to[k].x), (float)(x.y - to[k].y), (float)(x.z - to[k].z));
                     bb = bb + g;
                     rr = rr + g;
                 }
             }
         }
-        const int si = T.vslot[(size_t)t * kTileV + i];
+        const int si = so[k];
         sy[si] = f4of(yv);
         sz[si] = f4of(zv);
         sqb[si] = f4of(bb);
         sqr[si] = f4of(rr);
     }
-    for (int h = threadIdx.x; h < hcap; h += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+        if (hv[k] < 0) continue;
+        const float3 dh = uprev2 ? 2.f * hu[k] - 3.f * hp[k] + hp2[k] : hu[k] - hp[k];
+        sy[hs[k]] = f4of(hy[k]);
+        sz[hs[k]] = f4of(hy[k] + hu[k] + dh);
+    }
+    for (int h = threadIdx.x + NH * kTmaThreads; h < hcap; h += blockDim.x) {   // rare: large halos
         const int v = T.hpad[(size_t)t * hcap + h];
         if (v < 0) continue;
         const float3 uh = f3(u[v]);
         const float3 dh = uprev2 ? 2.f * uh - 3.f * f3(uprev[v]) + f3(uprev2[v]) : uh - f3(uprev[v]);
-        const float3 yv = f3(y[v]), zv = yv + uh + dh;
+        const float3 yv = f3(y[v]);
         const int sh = T.hslot[(size_t)t * hcap + h];
         sy[sh] = f4of(yv);
-        sz[sh] = f4of(zv);
+        sz[sh] = f4of(yv + uh + dh);
     }
     __syncthreads();
     // b -= A_dist y, r0 -= A_dist z (same per-color scheme as tma_tile_colors)
