@@ -829,24 +829,10 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
         hv[u] = h < hcap ? T.hpad[(size_t)t * hcap + h] : -1;
         hs[u] = h < hcap ? T.hslot[(size_t)t * hcap + h] : 0;
     }
-    if (done) return;
-    __syncthreads();
-    if (threadIdx.x == NT - 32) {
-        for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
-        fence_mbar_init();
-        const uint32_t sbytes = tma_stage_bytes(T.cap);
-        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
-    }
-    // ---- round trip 2
+    // own vector values need nothing from round trip 1: issued with it (early-exit launches after
+    // convergence are rare with the host's poll schedule)
     const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
     float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
-    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
-    float alpha_prev = 0.f;
-    if (ufix && it > 0) {
-        const double pq = s.sc[it * 4 + 0];
-        alpha_prev = pq > 0.0 ? (float)(s.sc[(it - 1) * 4 + 1] / pq) : 0.f;
-    }
-    float acc[1] = {0.f};
     float3 ro[NO], po[NO], uo[NO];
 #pragma unroll
     for (int u = 0; u < NO; ++u) {
@@ -855,6 +841,22 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
         po[u] = it > 0 ? pold[v] : make_float3(0.f, 0.f, 0.f);
         uo[u] = (ufix && it > 0) ? ufix[v] : make_float3(0.f, 0.f, 0.f);   // deferred update, same batch
     }
+    if (done) return;
+    __syncthreads();
+    if (threadIdx.x == NT - 32) {
+        for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
+        fence_mbar_init();
+        const uint32_t sbytes = tma_stage_bytes(T.cap);
+        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
+    }
+    // ---- round trip 2: halo values
+    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
+    float alpha_prev = 0.f;
+    if (ufix && it > 0) {
+        const double pq = s.sc[it * 4 + 0];
+        alpha_prev = pq > 0.0 ? (float)(s.sc[(it - 1) * 4 + 1] / pq) : 0.f;
+    }
+    float acc[1] = {0.f};
     float hw[NH];
     float3 hr[NH], hp[NH];
 #pragma unroll
