@@ -1401,31 +1401,10 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const 
     }
 }
 
-// u += alpha p_it, r -= alpha q; accumulates rz = r.M^-1 r and rr = r.r (slot it+1)
-__global__ void k_cg_update2(int V, int it, CGBufs B, const float *__restrict__ wv, CGState s) {
-    if (cg_done(s, it + 1)) return;
-    int v = blockIdx.x * blockDim.x + threadIdx.x;
-    float acc[2] = {0.f, 0.f};
-    if (v < V) {
-        const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
-        double pq = s.sc[(it + 1) * 4 + 0];
-        float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
-        float w = wv[v];
-        float3 uv = B.u[v], rv = B.r[v], pv = p[v], qv = B.q[v];
-        uv.x += alpha * pv.x; uv.y += alpha * pv.y; uv.z += alpha * pv.z;
-        rv.x -= alpha * qv.x; rv.y -= alpha * qv.y; rv.z -= alpha * qv.z;
-        if (!(w > 0.f)) rv = make_float3(0.f, 0.f, 0.f);
-        B.u[v] = uv;
-        B.r[v] = rv;
-        float r2 = rv.x * rv.x + rv.y * rv.y + rv.z * rv.z;
-        acc[0] = w * r2;
-        acc[1] = r2;
-    }
-    block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
-}
 
 // Vectorized PCG update: 4 vertices per thread read as 3 float4 per field of the packed float3
-// arrays (16-byte accesses); same arithmetic as k_cg_update2.  Vertices [4*nq, V) by k_cg_update2.
+// arrays (16-byte accesses): u += alpha p (unless deferred to the next matvec), r -= alpha q,
+// r.M^-1 r and r.r into slot it+1; the V % 4 tail vertices by one extra thread.
 template <bool UPD_U>
 __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ wv, CGState s) {
     if (cg_done(s, it + 1)) return;
