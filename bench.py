@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 METRIC = "constraint solves/s & ms/step fwd+adjoint at ~26M DoF cloth; HBM GB/s vs peak"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed `ncu --set full`
 # capture of the dominant kernel at configs[4] size (profiles/ncu/)
-TRAFFIC = {"cg_dist": 1.479445e9 + 0.266695e9}
+TRAFFIC = {"cg_dist": 1.548254e9 + 0.299441e9}   # profiles/ncu/r01_k_cg_matvec_tma_v16.ncu-rep
 UNIT = "constraint solves/s"
 
 
