@@ -1,5 +1,7 @@
+"""Kernel-class profile of configs[2] (volumetric block, 2 frames) through dxpbd_profile /
+dxpbd_kernel_times; used to find the tet replay bottleneck."""
 import sys, numpy as np, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2301_01396_b200 import api
 from synth import as_float32_exact, volumetric_block
 s = as_float32_exact(volumetric_block(frames=2))
