@@ -496,6 +496,7 @@ struct dxpbd_scene {
     DBuf<double> t_Dm, t_vol;
     DBuf<float> t_a, t_b, t_Q, t_e, t_g, lam_t;
     DBuf<double4> t_xsave;   // K = 1 tet replay: pre-update vertices of every tet [4T]
+    DBuf<float4> t_q4;       // tet matvec accumulator (16-byte vector atomics), folded into q
     DBuf<int32_t> t_perm;
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
     TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
@@ -824,6 +825,10 @@ BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frame
         if (((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) && s->t_e.n < 18 * T) s->t_e.alloc(18 * T);
         if (s->t_g.n < 2 * T) s->t_g.alloc(2 * T);
         if (s->iterations == 1 && s->t_xsave.n < 4 * T) s->t_xsave.alloc(4 * T);
+        if (s->t_q4.n < (size_t)V) {
+            s->t_q4.alloc(V);
+            DX_CHECK_CUDA(cudaMemsetAsync(s->t_q4.p, 0, sizeof(float4) * V, st));
+        }
         if (s->iterations > 1 && s->ts_lam.n < 2 * T) {
             s->ts_lam.alloc(2 * T); s->ts_S.alloc(18 * T); s->ts_Dt.alloc(45 * T); s->ts_Tu.alloc(4 * T); s->ts_e.alloc(18 * T);
         }
@@ -917,7 +922,8 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<0><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             ++launches;
             if (s->T) {
-                LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), s->t_Q.p, bufs, xw, cs));
+                LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), s->t_Q.p, bufs, xw, cs, s->t_q4.p));
+                LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->t_q4.p, cs));
                 ++launches;
             }
             if (defer)

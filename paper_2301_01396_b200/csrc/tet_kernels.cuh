@@ -493,7 +493,8 @@ DX_INLINE void tet_Qmul(const float *__restrict__ Qt, int T, int j, const float 
 // Tet part of the PCG matvec (after the tile kernel wrote q): q += G^T Qt~ G p per tet with
 // vector reductions, and the p.q partial dF^T Qt~ dF.  p = p_it buffer (written by the tile kernel).
 __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float *__restrict__ Qt, CGBufs B,
-                                                   const float *__restrict__ wv, CGState s) {
+                                                   const float *__restrict__ wv, CGState s,
+                                                   float4 *__restrict__ q4 = nullptr) {
     if (cg_done(s, it + 1)) return;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     float acc[1] = {0.f};
@@ -515,10 +516,21 @@ __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float
         for (int v = 0; v < 4; ++v) {
             if (!(wv[vid[v]] > 0.f)) continue;
             float3 g = c[v][0] * f3at(q, 0) + c[v][1] * f3at(q, 1) + c[v][2] * f3at(q, 2);
-            red_add_f3(B.q + vid[v], g);
+            if (q4) red_add_f4(q4 + vid[v], make_float4(g.x, g.y, g.z, 0.f));   // one 16-byte atomic
+            else red_add_f3(B.q + vid[v], g);
         }
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
+}
+
+// q += xyz(q4) (the tet matvec's float4 accumulator), q4 <- 0 for the next iteration
+__global__ void k_fold_q4(int V, int it, CGBufs B, float4 *__restrict__ q4, CGState s) {
+    if (cg_done(s, it + 1)) return;
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    const float4 a = q4[v];
+    B.q[v] = B.q[v] + make_float3(a.x, a.y, a.z);
+    q4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // Tet part of the increment rhs: b -= G^T Qt~ G y, r0 -= G^T Qt~ G (y + u0), u0 = warm start
