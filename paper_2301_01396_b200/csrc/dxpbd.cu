@@ -484,6 +484,7 @@ struct dxpbd_scene {
     DBuf<int4> d_tseg;
     DBuf<uint32_t> d_cpair;
     DBuf<float4> d_Qt;                  // Q blocks in the TMA layout (own at tpos[j], foreign copy at fpos[j])
+    DBuf<float2> d_Qt2b;                // general blocks (qf == 0): (yz, zz) in the same layout
     DBuf<uint16_t> d_vslot, d_hslot;   // tile-local shared-memory slots (own vertices, halo entries)
     // host layout kept for partition groups (g_keep_host at create)
     std::vector<int> seg_h;                 // [nc][nt + 1] sorted-constraint offsets per (color, tile)
@@ -502,7 +503,7 @@ struct dxpbd_scene {
     TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
     TmaTiles tma_tiles() const {
         return TmaTiles{n_dist_colors, ntiles, hcap, capm, d_tseg.p, d_cpair.p, d_hpad.p, qt_read ? qt_read : d_Qt.p,
-                        d_vslot.p, d_hslot.p};
+                        qf == 1 ? nullptr : d_Qt2b.p, d_vslot.p, d_hslot.p};
     }
     // replay / PCG overlap (backward): the replay of substep n-1 runs on `aux` while the PCG of
     // substep n runs on the caller's stream; Q blocks alternate between d_Qt and d_Qt2
@@ -661,6 +662,7 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
 int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int V = s->V, E = s->E;
     float4 *qtw = s->qt_write ? s->qt_write : s->d_Qt.p;   // TMA-layout block buffer written
+    const bool lay = s->use_tma && s->qf == 0;              // general blocks into the TMA layout
     const int frame = n / s->substeps;
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
     double4 *x = s->xr.p;
@@ -706,13 +708,21 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
                     s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
                     s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, qtw));
             else if (first && last)
-                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x,
+                                                                                       lay ? s->d_fpos.p : nullptr, lay ? s->d_Qt.p : nullptr,
+                                                                                       lay ? s->d_tpos.p : nullptr, lay ? s->d_Qt2b.p : nullptr));
             else if (first)
-                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<true, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x,
+                                                                                       lay ? s->d_fpos.p : nullptr, lay ? s->d_Qt.p : nullptr,
+                                                                                       lay ? s->d_tpos.p : nullptr, lay ? s->d_Qt2b.p : nullptr));
             else if (last)
-                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<false, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<false, true><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x,
+                                                                                       lay ? s->d_fpos.p : nullptr, lay ? s->d_Qt.p : nullptr,
+                                                                                       lay ? s->d_tpos.p : nullptr, lay ? s->d_Qt2b.p : nullptr));
             else
-                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x));
+                LAUNCH(DXPBD_K_DIST_REPLAY, k_dist_replay<false, false><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, ds, s->pd, s->Qd.p, eo, x,
+                                                                                       lay ? s->d_fpos.p : nullptr, lay ? s->d_Qt.p : nullptr,
+                                                                                       lay ? s->d_tpos.p : nullptr, lay ? s->d_Qt2b.p : nullptr));
             ++launches;
         }
         if (s->T) {
@@ -796,7 +806,7 @@ BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frame
     if (s->xr.n < (size_t)V) s->xr.alloc(V);
     auto ensure4 = [&](DBuf<float3> &b) { if (b.n < (size_t)V) b.alloc(V); };
     ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
-    if (s->use_tma && !s->T && s->cgcg) { ensure4(s->r1); ensure4(s->s1); ensure4(s->w1); }
+    if (s->use_tma && s->qf == 1 && !s->T && s->cgcg) { ensure4(s->r1); ensure4(s->s1); ensure4(s->w1); }
     ensure4(s->uprev); ensure4(s->u0);
     if (s->warm_order == 2 && s->use_tma) ensure4(s->uprev2);
     const bool warm2 = su.warm2 = s->warm_order == 2 && s->use_tma;
@@ -884,7 +894,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
     TmaTiles tt = s->tma_tiles();
     // single-reduction PCG (kernels.cuh k_cgcg_tma): cloth-only TMA path
-    const bool cgcg = s->use_tma && !s->T && s->cgcg;
+    const bool cgcg = s->use_tma && s->qf == 1 && !s->T && s->cgcg;
     const bool defer = s->use_tma && !cgcg && s->defer_u;   // u update deferred into the next matvec
     CGCGBufs cb{s->ax.p, s->p.p, {s->r.p, s->r1.p}, {s->p1.p, s->s1.p}, {s->q.p, s->w1.p}, s->rhs.p};
     auto cgcg_launch = [&](int i) {
@@ -1160,8 +1170,8 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                     maxn = std::max<int>(maxn, (int)n);
                 }
             s->capm = (maxn + 7) & ~7;
-            s->use_tma = s->qf == 1 && hmax <= 4096 && nc <= kMaxColors && cbase.back() < (int64_t)INT32_MAX &&
-                         tma_rhs_smem_bytes(s->hcap, s->capm) <= 200 * 1024;
+            s->use_tma = hmax <= 4096 && nc <= kMaxColors && cbase.back() < (int64_t)INT32_MAX &&
+                         tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0) <= 200 * 1024;
             if (s->use_tma) {
                 const int hc = s->hcap;
                 std::vector<int> hpad((size_t)nt * hc, -1);
@@ -1206,8 +1216,9 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 s->d_tpos.alloc(E);
                 upload(s->d_tpos.p, tpos.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
                 s->d_Qt.alloc((size_t)NTOT + 1);
-                s->tma_smem = tma_smem_bytes(s->hcap, s->capm);
-                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm);
+                if (s->qf == 0) s->d_Qt2b.alloc((size_t)NTOT + 2);
+                s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->qf == 0);
+                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
@@ -1380,10 +1391,10 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     int solves = 0;
     const float *Qc = s->NC ? s->Qc.p : nullptr;
     // PCG start fused into the TMA rhs kernel (no tet rhs pass after it, standard PCG)
-    const bool fuse_start = s->use_tma && !s->T && !(s->cgcg);
+    const bool fuse_start = s->use_tma && !s->T && !(s->cgcg && s->qf == 1);
     // replay of substep n-1 on the aux stream during the PCG of substep n (independent work: the
     // replay reads only checkpoints); blocks double-buffered, ordered by events
-    const bool ovl = s->overlap && s->use_tma && !s->T && !s->NC && !g_comp && !s->cgcg;
+    const bool ovl = s->overlap && s->use_tma && s->qf == 1 && !s->T && !s->NC && !g_comp && !s->cgcg;
     cudaStream_t user_st = st;
     const int n_hi = std::min(N, last_key_state) - 1;
     if (ovl && n_hi >= 0) {
@@ -1499,7 +1510,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     s->stats[0] = total_it;
     // PCG matvec launches that did work: one per iteration (+ the start matvec per solve for the
     // single-reduction form)
-    s->stats[14] = total_it + ((s->use_tma && !s->T && s->cgcg) ? solves : 0);
+    s->stats[14] = total_it + ((s->use_tma && s->qf == 1 && !s->T && s->cgcg) ? solves : 0);
     s->stats[1] = max_it;
     s->stats[3] = launches;
     s->stats[4] = solves;

@@ -240,8 +240,9 @@ __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, in
                                                         DistScratch sc, int pd, float *__restrict__ Qout,
                                                         float *__restrict__ eout, double4 *__restrict__ x,
                                                         const int *__restrict__ fpos = nullptr,
-                                                        float4 *__restrict__ fQ = nullptr,
-                                                        const int *__restrict__ tpos = nullptr) {
+                                                        float4 *__restrict__ LQa = nullptr,
+                                                        const int *__restrict__ tpos = nullptr,
+                                                        float2 *__restrict__ LQb = nullptr) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= count) return;
     int j = begin + t;
@@ -276,20 +277,20 @@ __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, in
         x[ev.x] = pa;
         x[ev.y] = pb;
     }
-    if (LAST && QF == 1) {
-        // K = 1, PD projection on (host guarantees): closed form, no eigen-solve
-        float4 q4 = ok ? qpack_iso_rank1(o.n, o.dl, (float)(1.0 / o.len), o.J) : make_float4(0.f, 0.f, 0.f, 0.f);
-        reinterpret_cast<float4 *>(Qout)[tpos ? tpos[j] : j] = q4;   // TMA layout position
-        if (fpos) {
-            const int fp = fpos[j];
-            if (fp >= 0) fQ[fp] = q4;   // copy for the tile of b (TMA-staged foreign list)
-        }
-        if (eout) { eout[j] = ec.x; eout[E + j] = ec.y; eout[2 * E + j] = ec.z; }
-    } else if (LAST) {
+    if (LAST) {
         Sym3 mB = Sym3{-B.xx, -B.xy, -B.xz, -B.yy, -B.yz, -B.zz};
         Sym3 Q = pd ? sym3_psd(mB) : mB;
-        Qout[j] = Q.xx; Qout[E + j] = Q.xy; Qout[2 * E + j] = Q.xz;
-        Qout[3 * E + j] = Q.yy; Qout[4 * E + j] = Q.yz; Qout[5 * E + j] = Q.zz;
+        if (tpos) {   // TMA layout (general blocks: xx xy xz yy | yz zz), own-tile position + b-tile copy
+            const float4 qa = make_float4(Q.xx, Q.xy, Q.xz, Q.yy);
+            const float2 qb = make_float2(Q.yz, Q.zz);
+            LQa[tpos[j]] = qa;
+            LQb[tpos[j]] = qb;
+            const int fp = fpos[j];
+            if (fp >= 0) { LQa[fp] = qa; LQb[fp] = qb; }
+        } else {
+            Qout[j] = Q.xx; Qout[E + j] = Q.xy; Qout[2 * E + j] = Q.xz;
+            Qout[3 * E + j] = Q.yy; Qout[4 * E + j] = Q.yz; Qout[5 * E + j] = Q.zz;
+        }
         if (eout) { eout[j] = ec.x; eout[E + j] = ec.y; eout[2 * E + j] = ec.z; }
     } else {
         sc.lam[j] = lam0;
@@ -712,31 +713,44 @@ struct TmaTiles {
     const uint32_t *cpair;           // slot pairs (la | lb << 16); la >= kTileV marks a foreign entry
     const int *hpad;                 // [tile][hcap]: halo vertex ids, -1 padded (fixed stride)
     const float4 *Q4;                // blocks in the same layout (the replay writes both copies)
+    const float2 *Q2;                // general blocks only (K > 1 or no PD): Q4 = (xx, xy, xz, yy), Q2 = (yz, zz);
+                                     // null: Q4 is the K = 1 closed form c I + s n n^T
     const uint16_t *vslot;           // [tile][kTileV]: slot of own vertex i
     const uint16_t *hslot;           // [tile][hcap]: slot of halo entry h
 };
 
-// One stage (bytes, 16-aligned parts): q[cap] | cp[cap + 4, rounded to 16 bytes]
-__host__ __device__ inline uint32_t tma_stage_bytes(int cap) {
-    return (uint32_t)(16 * cap + ((4 * (cap + 4) + 15) & ~15));
+// One stage (bytes, 16-aligned parts): q[cap] | cp[cap + 4, rounded to 16 bytes] | (general blocks)
+// q2[cap + 2, rounded to 16 bytes]; `gen` is 1 for general blocks (TmaTiles::Q2 set)
+__host__ __device__ inline uint32_t tma_stage_bytes(int cap, int gen = 0) {
+    return (uint32_t)(16 * cap + ((4 * (cap + 4) + 15) & ~15) + (gen ? ((8 * (cap + 2) + 15) & ~15) : 0));
 }
 struct StageView {
     const float4 *q;
     const uint32_t *cp;
+    const float2 *q2;
 };
 DX_INLINE StageView stage_view(unsigned char *base, int cap) {
     StageView v;
     v.q = reinterpret_cast<const float4 *>(base);
     v.cp = reinterpret_cast<const uint32_t *>(v.q + cap);
+    v.q2 = reinterpret_cast<const float2 *>(base + 16 * cap + ((4 * (cap + 4) + 15) & ~15));
     return v;
 }
 // dynamic smem of the matvec: [bars 64][stages][sq float4 kTileV][sp float4 kTileV + hcap]
-__host__ __device__ inline size_t tma_smem_bytes(int hcap, int cap) {
-    return 64 + (size_t)tma_stage_bytes(cap) * kTmaStages + 16 * (size_t)kTileV + 16 * (size_t)(kTileV + hcap);
+__host__ __device__ inline size_t tma_smem_bytes(int hcap, int cap, int gen = 0) {
+    return 64 + (size_t)tma_stage_bytes(cap, gen) * kTmaStages + 16 * (size_t)kTileV + 16 * (size_t)(kTileV + hcap);
 }
 // rhs: [bars][stages][sqb, sqr float4 kTileV][sy, sz float4 kTileV + hcap]
-__host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap, int cap) {
-    return 64 + (size_t)tma_stage_bytes(cap) * kTmaStages + 32 * (size_t)kTileV + 32 * (size_t)(kTileV + hcap);
+__host__ __device__ inline size_t tma_rhs_smem_bytes(int hcap, int cap, int gen = 0) {
+    return 64 + (size_t)tma_stage_bytes(cap, gen) * kTmaStages + 32 * (size_t)kTileV + 32 * (size_t)(kTileV + hcap);
+}
+// Q d for an entry: closed form (Q2 null) or general symmetric block
+DX_INLINE float3 qmul_entry(const StageView &S, bool gen, int i, int off2, float3 d) {
+    const float4 a = S.q[i];
+    if (!gen) return qmul_iso_rank1(a, d);
+    const float2 b = S.q2[off2 + i];
+    return make_float3(a.x * d.x + a.y * d.y + a.z * d.z, a.y * d.x + a.w * d.y + b.x * d.z,
+                       a.z * d.x + b.x * d.y + b.y * d.z);
 }
 
 DX_INLINE void tma_issue(uint64_t *bar, unsigned char *stage, int4 g, const TmaTiles &T) {
@@ -746,10 +760,16 @@ DX_INLINE void tma_issue(uint64_t *bar, unsigned char *stage, int4 g, const TmaT
         return;
     }
     const size_t c0 = ((size_t)b * 4) & ~(size_t)15, c1 = ((size_t)e * 4 + 15) & ~(size_t)15;
-    mbar_expect_tx(bar, (uint32_t)(c1 - c0) + (uint32_t)(e - b) * 16u);
+    size_t d0 = 0, d1 = 0;
+    if (T.Q2) {
+        d0 = ((size_t)b * 8) & ~(size_t)15;
+        d1 = ((size_t)e * 8 + 15) & ~(size_t)15;
+    }
+    mbar_expect_tx(bar, (uint32_t)(c1 - c0) + (uint32_t)(e - b) * 16u + (uint32_t)(d1 - d0));
     const StageView S = stage_view(stage, T.cap);
     bulk_g2s((void *)S.cp, reinterpret_cast<const char *>(T.cpair) + c0, (uint32_t)(c1 - c0), bar);
     bulk_g2s((void *)S.q, T.Q4 + b, (uint32_t)(e - b) * 16u, bar);
+    if (T.Q2) bulk_g2s((void *)S.q2, reinterpret_cast<const char *>(T.Q2) + d0, (uint32_t)(d1 - d0), bar);
 }
 
 DX_INLINE float3 xyz(float4 v) { return make_float3(v.x, v.y, v.z); }
@@ -762,19 +782,20 @@ template <int NT>
 DX_INLINE float tma_tile_colors(uint64_t *bars, unsigned char *stages, const float4 *sp, float4 *sq, const int4 *sb,
                                 const TmaTiles &T) {
     float dotacc = 0.f;
-    const uint32_t sbytes = tma_stage_bytes(T.cap);
+    const uint32_t sbytes = tma_stage_bytes(T.cap, T.Q2 != nullptr);
     for (int c = 0; c < T.ncol; ++c) {
         const int st = c % kTmaStages;
         unsigned char *stage = stages + (size_t)st * sbytes;
         const StageView S = stage_view(stage, T.cap);
         mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
         const int4 g = sb[c];
-        const int n = g.y - g.x, off = g.x & 3;
+        const int n = g.y - g.x, off = g.x & 3, off2 = g.x & 1;
+        const bool gen = T.Q2 != nullptr;
         for (int i = threadIdx.x; i < n; i += NT) {
             const uint32_t pr = S.cp[off + i];
             const int la = pr & 0xffff, lb = pr >> 16;
             const float3 d = xyz(sp[la]) - xyz(sp[lb]);
-            const float3 y = qmul_iso_rank1(S.q[i], d);
+            const float3 y = qmul_entry(S, gen, i, off2, d);
             if (la < kTileV) {
                 dotacc += dot3(d, y);
                 sq[la] = f4of(xyz(sq[la]) + y);
@@ -803,7 +824,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
-    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap) * kTmaStages);
+    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap, T.Q2 != nullptr) * kTmaStages);
     float4 *sp = sq + kTileV;
     const int hcap = T.hcap;
     const int t = blockIdx.x + t0;   // t0: first tile of a partition (domain decomposition)
@@ -846,7 +867,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     if (threadIdx.x == NT - 32) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
-        const uint32_t sbytes = tma_stage_bytes(T.cap);
+        const uint32_t sbytes = tma_stage_bytes(T.cap, T.Q2 != nullptr);
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
     // ---- round trip 2: halo values
@@ -944,7 +965,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V,
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
-    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap) * kTmaStages);
+    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap, T.Q2 != nullptr) * kTmaStages);
     float4 *sp = sq + kTileV;
     const int hcap = T.hcap;
     const int t = blockIdx.x;
@@ -975,7 +996,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V,
     if (threadIdx.x == NT - 32) {
         for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
-        const uint32_t sbytes = tma_stage_bytes(T.cap);
+        const uint32_t sbytes = tma_stage_bytes(T.cap, T.Q2 != nullptr);
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
     // ---- scalars of this iteration (double, from the previous launches' reductions)
@@ -1111,7 +1132,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_rhs_tma(TmaTiles T, int V, c
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     unsigned char *stages = smem_raw + 64;
-    const uint32_t sbytes = tma_stage_bytes(T.cap);
+    const uint32_t sbytes = tma_stage_bytes(T.cap, T.Q2 != nullptr);
     float4 *sqb = reinterpret_cast<float4 *>(stages + (size_t)sbytes * kTmaStages);
     float4 *sqr = sqb + kTileV;
     const int hcap = T.hcap;
@@ -1235,13 +1256,13 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_rhs_tma(TmaTiles T, int V, c
         const StageView S = stage_view(stage, T.cap);
         mbar_wait(&bars[st], (uint32_t)((c / kTmaStages) & 1));
         const int4 g = sb[c];
-        const int n = g.y - g.x, off = g.x & 3;
+        const int n = g.y - g.x, off = g.x & 3, off2 = g.x & 1;
+        const bool gen = T.Q2 != nullptr;
         for (int i = threadIdx.x; i < n; i += kTmaThreads) {
             const uint32_t pr = S.cp[off + i];
-            const float4 q4 = S.q[i];
             const int la = pr & 0xffff, lb = pr >> 16;
-            const float3 qy = qmul_iso_rank1(q4, xyz(sy[la]) - xyz(sy[lb]));
-            const float3 qz = qmul_iso_rank1(q4, xyz(sz[la]) - xyz(sz[lb]));
+            const float3 qy = qmul_entry(S, gen, i, off2, xyz(sy[la]) - xyz(sy[lb]));
+            const float3 qz = qmul_entry(S, gen, i, off2, xyz(sz[la]) - xyz(sz[lb]));
             if (la < kTileV) {
                 sqb[la] = f4of(xyz(sqb[la]) - qy);
                 sqr[la] = f4of(xyz(sqr[la]) - qz);
