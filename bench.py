@@ -390,15 +390,20 @@ def run_ours(a):
     if sst["tma"]:
         S = substeps_total
         mv = algo_bytes("cg_dist", sst)
-        # per substep: predict, projection, replay, rhs (~ one matvec + b, r0, u0, p0 and the extrapolation
-        # inputs: 60 B/vertex), the final u += alpha p (36 B/vertex), adjoint accumulation (~40 B/vertex)
-        per_step = (S * (algo_bytes("predict", sst) + algo_bytes("dist_project", sst, E * a.iterations)
-                         + algo_bytes("dist_replay", sst, E * a.iterations)
-                         + mv + 60.0 * V + 36.0 * V + 40.0 * V)
+        # forward: predict + projection per substep, plus the block writes (Q + copy + layout indices) of the
+        # substeps cached for the backward; backward: predict + replay per substep not cached, rhs (~ one
+        # matvec + b, r0, u0, p0 and the extrapolation inputs: 60 B/vertex), the final u += alpha p (36 B/vertex),
+        # adjoint accumulation (~40 B/vertex) per substep, and the PCG matvecs / updates
+        M = sst.get("cached_substeps", 0)
+        NF = sst["n_foreign"]
+        per_step = (S * (algo_bytes("predict", sst) + algo_bytes("dist_project", sst, E * a.iterations))
+                    + M * (16.0 * (E + NF) + 8.0 * E)
+                    + (S - M) * (algo_bytes("predict", sst) + algo_bytes("dist_replay", sst, E * a.iterations))
+                    + S * (mv + 60.0 * V + 36.0 * V + 40.0 * V)
                     + (cg_mv / a.steps) * mv + (cg_iters / a.steps) * algo_bytes("cg_update", sst))
         ach = per_step / (ms_per_step / 1e3) / 1e9
         step_roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "algorithmic_bytes_per_step": per_step}
+                     "algorithmic_bytes_per_step": per_step, "substeps_with_cached_blocks": M}
 
     # ---- CPU baseline (oracle on a bounded crop, rank 0 at N = 1 only)
     cpu = None

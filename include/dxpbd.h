@@ -150,7 +150,8 @@ int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out
  *  5: worst final relative residual, 6: last loss, 7: foreign constraint entries (tiled PCG),
  *  8: halo slots summed over tiles, 9: E, 10: V, 11: T, 12: vertex tiles, 13: TMA path on,
  *  14: PCG matvec launches of the last backward that did work (iterations, plus one start
- *      matvec per solve for the single-reduction PCG). */
+ *      matvec per solve for the single-reduction PCG), 15: substeps of the last backward whose
+ *      derivative blocks came from the forward's cache (no replay). */
 int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
 
 /* ---- Vertex-partitioned domain decomposition -------------------------

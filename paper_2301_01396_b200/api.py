@@ -305,7 +305,8 @@ def dxpbd_stats(scene: DxScene) -> dict:
     _check(lib().dxpbd_stats(scene.handle, out.ctypes.data, 16), "dxpbd_stats")
     return dict(cg_iters_total=out[0], cg_iters_max=out[1], fwd_launches=out[2], bwd_launches=out[3],
                 solves=out[4], worst_relres=out[5], loss=out[6], n_foreign=out[7], halo_total=out[8],
-                E=out[9], V=out[10], T=out[11], tiles=out[12], tma=bool(out[13]), cg_matvecs=out[14])
+                E=out[9], V=out[10], T=out[11], tiles=out[12], tma=bool(out[13]), cg_matvecs=out[14],
+                cached_substeps=out[15])
 
 
 def dxpbd_profile(scene: DxScene, enable: bool = True):

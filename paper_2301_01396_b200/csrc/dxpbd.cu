@@ -512,6 +512,11 @@ struct dxpbd_scene {
     cudaStream_t aux = nullptr, hi = nullptr;   // aux: replay (lowest priority), hi: PCG path (highest)
     cudaEvent_t ev_rep[2] = {nullptr, nullptr}, ev_pcg[2] = {nullptr, nullptr}, ev_go = nullptr, ev_end = nullptr;
     bool overlap = true;
+    // block cache (forward -> backward): the derivative blocks of substeps [qc_first, qc_first + qc_count)
+    // computed during the forward (replay kernels in place of the projection) into spare HBM
+    DBuf<float4> qcache;
+    int qc_first = 0, qc_count = 0;
+    bool qcache_on = true;
     // colliders
     DBuf<float> sph, cap_c, cap_a, cap_r0, cap_L0, cap_Rb, cap_Lb, beta;
     DBuf<Collider> cols;
@@ -623,7 +628,12 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         for (int c = 0; c < s->n_dist_colors; ++c) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
-            if (!rd && !wr && s->nb == 2)
+            if (!rd && !wr && s->qc_count && n >= s->qc_first) {
+                // cached substep: the replay kernel (same iterates bit for bit) also stores Q_n
+                float4 *slot = s->qcache.p + (size_t)(n - s->qc_first) * s->d_Qt.n;
+                LAUNCH(DXPBD_K_DIST_PROJECT, (k_dist_replay1<2, 3><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
+                    b, cnt, s->E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, slot, nullptr, xo, s->d_tpos.p, s->d_fpos.p, slot)));
+            } else if (!rd && !wr && s->nb == 2)
                 LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project1<2><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, xo));
             else if (!rd && !wr)
                 LAUNCH(DXPBD_K_DIST_PROJECT, k_dist_project1<1><<<nblk(cnt), kBlock, 0, st>>>(b, cnt, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, xo));
@@ -810,7 +820,7 @@ BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frame
     ensure4(s->uprev); ensure4(s->u0);
     if (s->warm_order == 2 && s->use_tma) ensure4(s->uprev2);
     const bool warm2 = su.warm2 = s->warm_order == 2 && s->use_tma;
-    if (E && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);
+    if (E && !s->use_tma && s->Qd.n < (size_t)6 * E) s->Qd.alloc((size_t)6 * E);   // TMA path: blocks in d_Qt
     const bool g_comp = su.g_comp = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
     const bool g_forces = su.g_forces = (s->grad_flags >> DXPBD_GRAD_FORCES) & 1;
     const bool g_coll = su.g_coll = (s->grad_flags & ((1u << DXPBD_GRAD_SHAPE) | (1u << DXPBD_GRAD_SPHERE))) != 0;
@@ -1053,6 +1063,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_OVERLAP")) s->overlap = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_QCACHE")) s->qcache_on = atoi(ev) != 0;
 
     cudaStream_t st = 0;
 
@@ -1342,6 +1353,27 @@ int dxpbd_forward(dxpbd_scene *s, const float *x0, const float *v0, const float 
     forward_inputs(s, x0, v0, forces, num_frames, mem, st);
     int launches = 4;
     const int N = num_frames * s->substeps;
+    // block cache for the last substeps in spare HBM (K = 1 TMA path without colliders / tets /
+    // compliance gradients, which need the replay's other outputs)
+    s->qc_count = 0;
+    if (s->qcache_on && s->use_tma && s->qf == 1 && !s->T && !s->NC && !((s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1) &&
+        N > 0) {
+        const size_t per = sizeof(float4) * s->d_Qt.n;
+        size_t freeb = 0, totalb = 0;
+        DX_CHECK_CUDA(cudaMemGetInfo(&freeb, &totalb));
+        freeb += s->qcache.n * sizeof(float4);   // the current cache is reusable
+        // keep room for the backward's buffers (~20 vertex vectors + the second block buffer) and 2 GB
+        const size_t reserve = (size_t)24 * 16 * s->V + per + ((size_t)2 << 30);
+        const int M = freeb > reserve ? (int)std::min<size_t>((size_t)N, (freeb - reserve) / 5 * 4 / per) : 0;
+        if (M > 0) {
+            if (s->qcache.n < (size_t)M * s->d_Qt.n) {
+                s->qcache.free();
+                s->qcache.alloc((size_t)M * s->d_Qt.n);
+            }
+            s->qc_first = N - M;
+            s->qc_count = M;
+        }
+    }
     for (int n = 0; n < N; ++n) launches += forward_substep(s, n, st);
     DX_CHECK_CUDA(cudaGetLastError());
     s->frames_done = num_frames;
@@ -1395,6 +1427,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     // replay of substep n-1 on the aux stream during the PCG of substep n (independent work: the
     // replay reads only checkpoints); blocks double-buffered, ordered by events
     const bool ovl = s->overlap && s->use_tma && s->qf == 1 && !s->T && !s->NC && !g_comp && !s->cgcg;
+    // blocks of the last substeps were cached by the forward (valid for the overlap path only)
+    auto cached = [&](int n) { return ovl && s->qc_count > 0 && n >= s->qc_first && n < s->qc_first + s->qc_count; };
     cudaStream_t user_st = st;
     const int n_hi = std::min(N, last_key_state) - 1;
     if (ovl && n_hi >= 0) {
@@ -1417,22 +1451,28 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         DX_CHECK_CUDA(cudaStreamWaitEvent(s->hi, s->ev_go, 0));
         user_st = st;
         st = s->hi;
-        s->qt_write = (n_hi & 1) ? s->d_Qt2.p : s->d_Qt.p;
-        launches += replay_substep(s, n_hi, s->aux);
-        DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[n_hi & 1], s->aux));
+        if (!cached(n_hi)) {
+            s->qt_write = (n_hi & 1) ? s->d_Qt2.p : s->d_Qt.p;
+            launches += replay_substep(s, n_hi, s->aux);
+            DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[n_hi & 1], s->aux));
+        }
     }
     for (int n = n_hi; n >= 0; --n) {
         const int frame = n / sub;
         float *gf = g_forces ? s->g_force.p + (size_t)frame * V * 3 : nullptr;
         if (ovl) {
-            if (n >= 1) {   // blocks of substep n-1 into the buffer PCG(n+1) finished reading
-                if (n + 1 <= n_hi) DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_pcg[(n - 1) & 1], 0));
+            if (n >= 1 && !cached(n - 1)) {   // blocks of substep n-1 into the buffer PCG(n+1) finished reading
+                if (n + 1 <= n_hi && !cached(n + 1)) DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_pcg[(n - 1) & 1], 0));
                 s->qt_write = ((n - 1) & 1) ? s->d_Qt2.p : s->d_Qt.p;
                 launches += replay_substep(s, n - 1, s->aux);
                 DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[(n - 1) & 1], s->aux));
             }
-            DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_rep[n & 1], 0));
-            s->qt_read = (n & 1) ? s->d_Qt2.p : s->d_Qt.p;
+            if (cached(n)) {
+                s->qt_read = s->qcache.p + (size_t)(n - s->qc_first) * s->d_Qt.n;
+            } else {
+                DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_rep[n & 1], 0));
+                s->qt_read = (n & 1) ? s->d_Qt2.p : s->d_Qt.p;
+            }
         } else {
             s->qt_write = s->qt_read = nullptr;
             launches += replay_substep(s, n, st);
@@ -1508,6 +1548,12 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     phi = s->h_scal[0];
     if (loss_out) *loss_out = (float)phi;
     s->stats[0] = total_it;
+    // substeps of this backward whose blocks came from the forward's cache (no replay)
+    {
+        int nc_used = 0;
+        for (int n = std::min(N, last_key_state) - 1; n >= 0; --n) nc_used += cached(n) ? 1 : 0;
+        s->stats[15] = nc_used;
+    }
     // PCG matvec launches that did work: one per iteration (+ the start matvec per solve for the
     // single-reduction form)
     s->stats[14] = total_it + ((s->use_tma && s->qf == 1 && !s->T && s->cgcg) ? solves : 0);
@@ -1598,6 +1644,7 @@ int dxpbd_grads(dxpbd_scene *s, int32_t kind, float *out, int64_t out_len, int32
 
 int dxpbd_set_params(dxpbd_scene *s, int32_t kind, const float *data, int64_t len, int32_t mem, void *stream) {
     DX_API_BEGIN
+    if (s) s->qc_count = 0;   // cached blocks belong to the previous parameters
     DX_REQUIRE(s && data, DXPBD_ERR_ARG, "null argument");
     DX_CHECK_CUDA(cudaSetDevice(s->device));
     cudaStream_t st = (cudaStream_t)stream;

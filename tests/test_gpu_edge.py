@@ -140,7 +140,8 @@ def test_large_cloth_full_size_substeps_bench_config():
 
 def test_schedule_switches_do_not_change_results(monkeypatch):
     """The performance schedules (replay / PCG stream overlap with double-buffered blocks, deferred
-    u += alpha p) reorder launches but not arithmetic: results equal the plain schedule bit for bit."""
+    u += alpha p, derivative blocks cached by the forward) reorder work but not arithmetic: results
+    equal the plain schedule bit for bit."""
     api = _api()
     s = f32(large_cloth(n=96, frames=2, substeps=3, side=10.0 * 95 / 2943.0, key_frames=(2,)).replace(frame_dt=3 / 600))
 
@@ -151,7 +152,7 @@ def test_schedule_switches_do_not_change_results(monkeypatch):
         return loss, [api.dxpbd_grads(sc, k) for k in ("forces", "x0", "v0")]
 
     la, ga = run()
-    for k, v in (("DXPBD_OVERLAP", "0"), ("DXPBD_DEFER_U", "0")):
+    for k, v in (("DXPBD_OVERLAP", "0"), ("DXPBD_DEFER_U", "0"), ("DXPBD_QCACHE", "0")):
         monkeypatch.setenv(k, v)
     lb, gb = run()
     assert la == lb
