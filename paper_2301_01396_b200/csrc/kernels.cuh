@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_rhs_tma(TmaTiles T, int V, c
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
     __shared__ int4 sb[kMaxColors];
-    constexpr int NO = kTileV / kTmaThreads, NH = 2;
+    constexpr int NO = (kTileV + kTmaThreads - 1) / kTmaThreads, NH = 2;
     // ---- round trip 1: descriptors, slots, halo ids, inverse masses
     if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
     float wo[NO];
@@ -1151,7 +1151,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_rhs_tma(TmaTiles T, int V, c
     for (int k = 0; k < NO; ++k) {
         const int i = threadIdx.x + k * kTmaThreads;
         wo[k] = wv[min(v0 + i, V - 1)];
-        so[k] = T.vslot[(size_t)t * kTileV + i];
+        so[k] = i < kTileV ? T.vslot[(size_t)t * kTileV + i] : 0;
     }
     int hv[NH], hs[NH];
 #pragma unroll
@@ -1225,6 +1225,7 @@ __global__ void __launch_bounds__(kTmaThreads, 3) k_rhs_tma(TmaTiles T, int V, c
                 }
             }
         }
+        if (i >= kTileV) continue;
         const int si = so[k];
         sy[si] = f4of(yv);
         sz[si] = f4of(zv);
