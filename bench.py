@@ -165,8 +165,9 @@ def algo_bytes(cls, st, units_per_launch=None):
     E, V, NF, H = st["E"], st["V"], st["n_foreign"], st["halo_total"]
     if cls == "dist_project":   # per constraint: idx 8 + rest 4 + alpha 4 + 2 x (32 B read + 32 B write) fp64 state
         return 144.0 * units_per_launch
-    if cls == "dist_replay":    # + Q 16 + foreign slot 4 (+ its fQ copy for foreign constraints)
-        return (164.0 + 16.0 * NF / max(E, 1)) * units_per_launch
+    if cls == "dist_replay":    # projection bytes + Q 16 + layout positions tpos/fpos 8 (+ the b-tile copy 16 per
+        # cross-tile constraint)
+        return (168.0 + 16.0 * NF / max(E, 1)) * units_per_launch
     if cls == "cg_dist":        # TMA matvec: slot pair 4 + Q 16 per entry of the combined segments (own constraints
         # and foreign copies), halo id 4 + slot 2 + (w 4, r 12, p_old 12) per halo entry, own w 4 + slot 2 + r 12 +
         # p_old 12 + p_new 12 + q 12 and the deferred u += alpha p (u r/w 24)
