@@ -57,7 +57,12 @@ def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"DiffXPBD CUDA library missing: {LIB_PATH} (run __graft_entry__.build())")
+            # compile the CUDA library on demand (nvcc, sm_100a); no fallback if that fails
+            try:
+                from . import build as _build
+                _build.build()
+            except Exception as e:  # noqa: BLE001
+                raise RuntimeError(f"DiffXPBD CUDA library missing and could not be built: {LIB_PATH} ({e})") from e
         L = ctypes.CDLL(LIB_PATH)
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         sig = {
