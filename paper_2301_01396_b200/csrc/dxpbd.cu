@@ -542,6 +542,7 @@ struct dxpbd_scene {
     int rep_minb = 3;                                  // K = 1 replay: launch-bounds CTAs per SM (measured best)
     bool defer_u = true;                               // PCG: u += alpha p deferred into the next matvec (measured best)
     int last_iters = 0;                                // PCG iterations of the previous solve (poll schedule)
+    int poll_extra = 0;                                // iterations launched beyond last_iters before the first poll
     DBuf<float3> r1, s1, w1;                           // single-reduction PCG ping-pong partners
     bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
                                                        // measured 10 % slower than matvec + update)
@@ -921,7 +922,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     int it = 0;
     // launches between host convergence polls: first the previous solve's count (consecutive
     // substeps need nearly the same number), then small chunks; launches past convergence exit at once
-    int chunk = s->last_iters > 0 ? std::max(s->last_iters, 2) : 8;
+    int chunk = s->last_iters > 0 ? std::max(s->last_iters + s->poll_extra, 2) : 8;
     iters_out = -1;
     relres_out = 0.0;
     while (it < maxit) {
@@ -1064,6 +1065,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_OVERLAP")) s->overlap = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_QCACHE")) s->qcache_on = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_POLL_EXTRA")) s->poll_extra = atoi(ev);
 
     cudaStream_t st = 0;
 
