@@ -547,6 +547,11 @@ struct dxpbd_scene {
     bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
                                                        // measured 10 % slower than matvec + update)
     int cgcg_minb = 4;                                 // its resident CTAs per SM (launch bounds)
+    bool tetv = true;                                  // no distance constraints: 2-launch PCG iteration (k_cg_tetv)
+    int tetv_minb = 1;                                 // its launch-bounds CTAs per SM
+    float psd_tol = 1e-6f;                             // tet PD projection: Jacobi stop (off-diagonal / scale)
+    int psd_sweeps = 12;                               // and sweep cap
+    int psd_minb = 3;                                  // its launch-bounds CTAs per SM (measured best)
     int qf = 0;   // Q format: 0 = sym6 SoA, 1 = iso+rank1 float4 (K = 1 with PD projection)
     DBuf<float> Qd, ed, Qc, ec;
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
@@ -756,7 +761,12 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
                                                0, s->T, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x, s->t_xsave.p)));
                 ++launches;
                 if (s->pd) {
-                    LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p));
+                    if (s->psd_minb == 3)
+                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<3><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p, s->psd_tol, s->psd_sweeps));
+                    else if (s->psd_minb == 4)
+                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<4><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p, s->psd_tol, s->psd_sweeps));
+                    else
+                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<1><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p, s->psd_tol, s->psd_sweeps));
                     ++launches;
                 }
             }
@@ -907,6 +917,10 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     // single-reduction PCG (kernels.cuh k_cgcg_tma): cloth-only TMA path
     const bool cgcg = s->use_tma && s->qf == 1 && !s->T && s->cgcg;
     const bool defer = s->use_tma && !cgcg && s->defer_u;   // u update deferred into the next matvec
+    // no distance constraints (tets and contacts only): tet + vertex matvec in one launch, q folded
+    // into the update (tet_kernels.cuh k_cg_tetv)
+    const bool tetv = s->T && E == 0 && !s->use_tma && s->tetv;
+    const int nbt = tetv ? nblk(s->T) : 0;
     CGCGBufs cb{s->ax.p, s->p.p, {s->r.p, s->r1.p}, {s->p1.p, s->s1.p}, {s->q.p, s->w1.p}, s->rhs.p};
     auto cgcg_launch = [&](int i) {
         if (s->cgcg_minb == 3)
@@ -932,6 +946,17 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             if (cgcg) {
                 cgcg_launch(it);
                 ++launches;
+                continue;
+            }
+            if (tetv) {
+                if (s->tetv_minb == 3)
+                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<3><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), s->t_Q.p, bufs,
+                                                                                         xw, Qc, cs, s->t_q4.p));
+                else
+                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<1><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), s->t_Q.p, bufs,
+                                                                                         xw, Qc, cs, s->t_q4.p));
+                LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update_tet<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, Qc, cs, s->t_q4.p));
+                launches += 2;
                 continue;
             }
             if (s->use_tma)
@@ -1063,6 +1088,11 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_TETV")) s->tetv = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_TETV_MINB")) s->tetv_minb = atoi(ev);
+    if (const char *ev = getenv("DXPBD_PSD_TOL")) s->psd_tol = (float)atof(ev);
+    if (const char *ev = getenv("DXPBD_PSD_SWEEPS")) s->psd_sweeps = atoi(ev);
+    if (const char *ev = getenv("DXPBD_PSD_MINB")) s->psd_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_OVERLAP")) s->overlap = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_QCACHE")) s->qcache_on = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_POLL_EXTRA")) s->poll_extra = atoi(ev);

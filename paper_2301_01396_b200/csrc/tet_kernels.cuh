@@ -210,10 +210,15 @@ __global__ void __launch_bounds__(128) k_tet_project(int begin, int count, TetDe
     x[id.w] = xs[3];
 }
 
-// 9x9 symmetric PSD projection by cyclic Jacobi (R5), in place on A (full), V scratch.
-DX_INLINE void psd9(float (&A)[9][9]) {
-    // cyclic Jacobi; every index is a compile-time constant (fully unrolled rotations) so A and V
-    // stay in registers (a rolled loop with runtime indices puts both in local memory)
+// 9x9 symmetric PSD projection by cyclic Jacobi (R5), in place on the packed upper triangle
+// a[sx(p, q)] (the Qt~ layout).  Each rotation updates the two rows / columns p, q of the
+// symmetric matrix once (a_pp -= t a_pq, a_qq += t a_pq, a_pq = 0, a_kp / a_kq for k != p, q) and
+// the eigenvector matrix V; every index is a compile-time constant (fully unrolled), so a and V
+// stay in registers.  Eigenvalues are clamped at 0 and the block rebuilt as V diag(l) V^T.
+DX_INLINE constexpr int sx(int p, int q) {
+    return p <= q ? p * 9 - (p * (p - 1)) / 2 + (q - p) : q * 9 - (q * (q - 1)) / 2 + (p - q);
+}
+DX_INLINE void psd9p(float (&a)[45], float tol = 1e-6f, int max_sweeps = 12) {
     float V[9][9];
 #pragma unroll
     for (int i = 0; i < 9; ++i)
@@ -223,36 +228,34 @@ DX_INLINE void psd9(float (&A)[9][9]) {
 #pragma unroll
     for (int i = 0; i < 9; ++i)
 #pragma unroll
-        for (int j = 0; j < 9; ++j) scale += fabsf(A[i][j]);
+        for (int j = i; j < 9; ++j) scale += (i == j ? 1.f : 2.f) * fabsf(a[sx(i, j)]);
     if (scale == 0.f) return;
 #pragma unroll 1
-    for (int sweep = 0; sweep < 12; ++sweep) {
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
         float off = 0.f;
 #pragma unroll
         for (int p = 0; p < 9; ++p)
 #pragma unroll
-            for (int q = p + 1; q < 9; ++q) off += fabsf(A[p][q]);
-        if (off <= 1e-8f * scale) break;
+            for (int q = p + 1; q < 9; ++q) off += fabsf(a[sx(p, q)]);
+        if (off <= tol * scale) break;
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
 #pragma unroll
             for (int q = p + 1; q < 9; ++q) {
-                const float apq = A[p][q];
+                const float apq = a[sx(p, q)];
                 if (fabsf(apq) < 1e-30f) continue;
-                const float theta = (A[q][q] - A[p][p]) / (2.f * apq);
+                const float theta = (a[sx(q, q)] - a[sx(p, p)]) / (2.f * apq);
                 const float tt = copysignf(1.f, theta) / (fabsf(theta) + sqrtf(theta * theta + 1.f));
                 const float cc = rsqrtf(tt * tt + 1.f), ss = tt * cc;
+                a[sx(p, p)] -= tt * apq;
+                a[sx(q, q)] += tt * apq;
+                a[sx(p, q)] = 0.f;
 #pragma unroll
                 for (int k = 0; k < 9; ++k) {
-                    const float akp = A[k][p], akq = A[k][q];
-                    A[k][p] = cc * akp - ss * akq;
-                    A[k][q] = ss * akp + cc * akq;
-                }
-#pragma unroll
-                for (int k = 0; k < 9; ++k) {
-                    const float apk = A[p][k], aqk = A[q][k];
-                    A[p][k] = cc * apk - ss * aqk;
-                    A[q][k] = ss * apk + cc * aqk;
+                    if (k == p || k == q) continue;
+                    const float akp = a[sx(k, p)], akq = a[sx(k, q)];
+                    a[sx(k, p)] = cc * akp - ss * akq;
+                    a[sx(k, q)] = ss * akp + cc * akq;
                 }
 #pragma unroll
                 for (int k = 0; k < 9; ++k) {
@@ -265,7 +268,7 @@ DX_INLINE void psd9(float (&A)[9][9]) {
     }
     float l[9];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) l[i] = fmaxf(A[i][i], 0.f);
+    for (int i = 0; i < 9; ++i) l[i] = fmaxf(a[sx(i, i)], 0.f);
 #pragma unroll
     for (int i = 0; i < 9; ++i)
 #pragma unroll
@@ -273,26 +276,22 @@ DX_INLINE void psd9(float (&A)[9][9]) {
             float s = 0.f;
 #pragma unroll
             for (int k = 0; k < 9; ++k) s += l[k] * V[i][k] * V[j][k];
-            A[i][j] = s;
-            A[j][i] = s;
+            a[sx(i, j)] = s;
         }
 }
 
 // PD projection (R5) of every tet's F-space block in place: Qt~ <- psd(Qt~) (45 floats, upper
 // triangle, SoA), one thread per tet with the 9x9 Jacobi in registers.
-__global__ void __launch_bounds__(128) k_tet_psd(int T, float *__restrict__ Qt) {
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_tet_psd(int T, float *__restrict__ Qt, float tol, int max_sweeps) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= T) return;
-    float A[9][9];
+    float a[45];
 #pragma unroll
-    for (int p = 0; p < 9; ++p)
+    for (int m = 0; m < 45; ++m) a[m] = Qt[(size_t)m * T + j];
+    psd9p(a, tol, max_sweeps);
 #pragma unroll
-        for (int q = p; q < 9; ++q) A[p][q] = A[q][p] = Qt[(size_t)(p * 9 - (p * (p - 1)) / 2 + (q - p)) * T + j];
-    psd9(A);
-#pragma unroll
-    for (int p = 0; p < 9; ++p)
-#pragma unroll
-        for (int q = p; q < 9; ++q) Qt[(size_t)(p * 9 - (p * (p - 1)) / 2 + (q - p)) * T + j] = A[p][q];
+    for (int m = 0; m < 45; ++m) Qt[(size_t)m * T + j] = a[m];
 }
 
 // Running state of the differentiable replay (iterations > 1), SoA per tet.
@@ -438,16 +437,12 @@ __global__ void __launch_bounds__(128) k_tet_replay(int begin, int count, TetDev
         }
     }
     if (LAST) {
-        float A[9][9];
+        float a[45];
 #pragma unroll
-        for (int p = 0; p < 9; ++p)
+        for (int m = 0; m < 45; ++m) a[m] = (float)(-Dt[m]);
+        if (pd && MODE != 2) psd9p(a);   // MODE 2: k_tet_psd projects all tets afterwards
 #pragma unroll
-            for (int q = p; q < 9; ++q) A[p][q] = A[q][p] = (float)(-Dt[p * 9 - (p * (p - 1)) / 2 + (q - p)]);
-        if (pd && MODE != 2) psd9(A);   // MODE 2: k_tet_psd projects all tets afterwards
-#pragma unroll
-        for (int p = 0; p < 9; ++p)
-#pragma unroll
-            for (int q = p; q < 9; ++q) Qt[(size_t)(p * 9 - (p * (p - 1)) / 2 + (q - p)) * T + j] = A[p][q];
+        for (int m = 0; m < 45; ++m) Qt[(size_t)m * T + j] = a[m];
         if (eout)
             for (int k = 0; k < 9; ++k) {
                 eout[(size_t)k * T + j] = (float)e[0][k];
@@ -531,6 +526,116 @@ __global__ void k_fold_q4(int V, int it, CGBufs B, float4 *__restrict__ q4, CGSt
     const float4 a = q4[v];
     B.q[v] = B.q[v] + make_float3(a.x, a.y, a.z);
     q4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Scenes without distance constraints (tets, contacts): one PCG iteration in two launches instead
+// of four (tile matvec, k_cg_tet, k_fold_q4, update).  Blocks [0, nbt) are k_cg_tet's tets, which
+// form p_it at their corners on the fly (halo_p) instead of reading it; blocks [nbt, ..) form
+// p_it = M^-1 r_it + beta p_{it-1} per vertex (stored, the same halo_p expression) and add
+// p.(M + Qc) p to p.q.  q is not stored: k_cg_update_tet rebuilds q = (M + Qc) p + q4.
+template <int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_cg_tetv(int it, int nbt, int V, TetDev D, const float *__restrict__ Qt,
+                                                    CGBufs B, const float *__restrict__ wv,
+                                                    const float *__restrict__ Qc, CGState s,
+                                                    float4 *__restrict__ q4) {
+    if (cg_done(s, it + 1)) return;
+    const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;   // p_{it-1}
+    float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;         // p_it
+    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
+    float acc[1] = {0.f};
+    if ((int)blockIdx.x < nbt) {
+        const int j = blockIdx.x * blockDim.x + threadIdx.x;
+        if (j < D.T) {
+            // all 45 block entries in flight before the dependent corner gathers (memory-level
+            // parallelism: the kernel is latency-bound at 4 CTAs / SM otherwise)
+            float qt[45];
+#pragma unroll
+            for (int m = 0; m < 45; ++m) qt[m] = __ldg(Qt + (size_t)m * D.T + j);
+            const int4 id = D.idx[j];
+            const int vid[4] = {id.x, id.y, id.z, id.w};
+            float3 pv[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) pv[v] = halo_p(it, vid[v], beta, B.r, pold, pnew, wv);
+            float c[4][3];
+            tet_load_c(D, j, c);
+            float dF[9], q[9];
+            tet_Gmul(c, pv, dF);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) q[k] = 0.f;
+            {
+                int m = 0;
+#pragma unroll
+                for (int a = 0; a < 9; ++a)
+#pragma unroll
+                    for (int b = a; b < 9; ++b) {
+                        q[a] += qt[m] * dF[b];
+                        if (b != a) q[b] += qt[m] * dF[a];
+                        ++m;
+                    }
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc[0] += dF[k] * q[k];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                if (!(wv[vid[v]] > 0.f)) continue;
+                float3 g = c[v][0] * f3at(q, 0) + c[v][1] * f3at(q, 1) + c[v][2] * f3at(q, 2);
+                red_add_f4(q4 + vid[v], make_float4(g.x, g.y, g.z, 0.f));
+            }
+        }
+    } else {
+        const int v = (blockIdx.x - nbt) * blockDim.x + threadIdx.x;
+        if (v < V) {
+            const float3 pv = halo_p(it, v, beta, B.r, pold, pnew, wv);
+            if (it > 0) pnew[v] = pv;
+            const float w = wv[v];
+            if (w > 0.f) {
+                float3 qv = (1.f / w) * pv;
+                if (Qc) {
+                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                                  Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                    qv = qv + sym3_mul(A, pv);
+                }
+                acc[0] += dot3(pv, qv);
+            }
+        }
+    }
+    block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
+}
+
+// PCG update after k_cg_tetv: q = (M + Qc) p + q4 (q4 <- 0), u += alpha p, r -= alpha q,
+// r.M^-1 r and r.r into slot it+1.
+__global__ void __launch_bounds__(kBlock) k_cg_update_tet(int V, int it, CGBufs B, const float *__restrict__ wv,
+                                                          const float *__restrict__ Qc, CGState s,
+                                                          float4 *__restrict__ q4) {
+    if (cg_done(s, it + 1)) return;
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc[2] = {0.f, 0.f};
+    if (v < V) {
+        const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
+        const double pq = s.sc[(it + 1) * 4 + 0];
+        const float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
+        const float w = wv[v];
+        const float3 pv = p[v];
+        B.u[v] = B.u[v] + alpha * pv;
+        float3 rv = make_float3(0.f, 0.f, 0.f);
+        if (w > 0.f) {
+            float3 qv = (1.f / w) * pv;
+            if (Qc) {
+                Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
+                              Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
+                qv = qv + sym3_mul(A, pv);
+            }
+            const float4 a = q4[v];
+            qv = qv + make_float3(a.x, a.y, a.z);
+            q4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            rv = B.r[v] - alpha * qv;
+        }
+        B.r[v] = rv;
+        const float r2 = dot3(rv, rv);
+        acc[0] += w * r2;
+        acc[1] += r2;
+    }
+    block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
 }
 
 // Tet part of the increment rhs: b -= G^T Qt~ G y, r0 -= G^T Qt~ G (y + u0), u0 = warm start

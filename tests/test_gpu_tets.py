@@ -73,3 +73,31 @@ def test_volumetric_full_size_forward_substeps():
     g = gpu_run(s, backward=False)
     o = oracle_run(s, backward=False)
     assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
+
+
+def test_volumetric_sphere_contacts():
+    """Tets plus a sphere pressed into the top corner (the tet-only PCG path with contact blocks
+    Qc): positions, material and sphere gradients vs the oracle."""
+    s = _block(6, 3)
+    h = float(s.x0[:, 1].max())
+    s = s.replace(spheres=np.array([[h, h + 0.012, h, 0.025]], np.float32).astype(np.float64))
+    g = gpu_run(s, ("material", "sphere"))
+    o = oracle_run(s)
+    assert np.abs(o["x"][-1] - o["x"][0]).max() > 1e-3   # the contacts push vertices
+    _compare(g, o, ("material", "sphere", "v0", "x0"))
+
+
+def test_tet_pcg_paths_agree(monkeypatch):
+    """The 2-launch tet PCG iteration (k_cg_tetv + k_cg_update_tet) against the 4-launch one
+    (tile matvec, k_cg_tet, k_fold_q4, update): same arithmetic per vertex, only the p.q block
+    sums are grouped differently."""
+    s = _block(16, 2, soft=True)
+    h = float(s.x0[:, 1].max())
+    s = s.replace(spheres=np.array([[h, h + 0.02, h, 0.06]], np.float32).astype(np.float64))
+    a = gpu_run(s, ("material", "sphere"))
+    monkeypatch.setenv("DXPBD_TETV", "0")
+    b = gpu_run(s, ("material", "sphere"))
+    assert rel_l2(a["x"][-1], b["x"][-1]) < 1e-6
+    for k in ("material", "sphere", "x0"):
+        assert rel_l2(a[k], b[k]) < 1e-4, k
+    assert a["stats"]["cg_iters_total"] == b["stats"]["cg_iters_total"]
