@@ -8,7 +8,7 @@ import time
 
 import numpy as np
 
-sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+sys.path.insert(0, __file__.rsplit("/tests/", 1)[0])
 from synth import as_float32_exact, large_cloth  # noqa: E402
 from tests.gpu_helpers import gpu_run, oracle_run, rel_l2  # noqa: E402
 
