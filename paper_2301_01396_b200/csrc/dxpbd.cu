@@ -497,6 +497,8 @@ struct dxpbd_scene {
     DBuf<double> t_Dm, t_vol;
     DBuf<float> t_a, t_b, t_Q, t_e, t_g, lam_t;
     DBuf<double4> t_xsave;   // K = 1 tet replay: pre-update vertices of every tet [4T]
+    DBuf<float> t_Q2, t_e2;  // second tet block / control buffers (replay / PCG overlap)
+    float *tq_w = nullptr, *te_w = nullptr, *tq_r = nullptr, *te_r = nullptr;   // overlap: replay writes, PCG reads
     DBuf<float4> t_q4;       // tet matvec accumulator (16-byte vector atomics), folded into q
     DBuf<int32_t> t_perm;
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
@@ -743,30 +745,31 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         }
         if (s->T) {
             TetScratch tsc{s->ts_lam.p, s->ts_S.p, s->ts_Dt.p, s->ts_Tu.p, s->ts_e.p};
-            float *teo = ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) ? s->t_e.p : nullptr;
+            float *const tQ = s->tq_w ? s->tq_w : s->t_Q.p;   // this replay's block buffer
+            float *teo = ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) ? (s->te_w ? s->te_w : s->t_e.p) : nullptr;
             for (int c = 0; c < s->n_tet_colors; ++c) {
                 int b = s->tet_off[c], cnt = s->tet_off[c + 1] - b;
                 if (!cnt) continue;
                 const int tb = (cnt + 127) / 128;
                 if (first && last)   // K = 1: iterate only, derivative blocks of all tets after the colors
-                    LAUNCH(DXPBD_K_TET_REPLAY, (k_tet_replay<true, true, 1><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x,
+                    LAUNCH(DXPBD_K_TET_REPLAY, (k_tet_replay<true, true, 1><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, tQ, teo, x,
                                                                                                s->t_xsave.p)));
-                else if (first) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<true, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
-                else if (last) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
-                else LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x));
+                else if (first) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<true, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, tQ, teo, x));
+                else if (last) LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, true><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, tQ, teo, x));
+                else LAUNCH(DXPBD_K_TET_REPLAY, k_tet_replay<false, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, tsc, s->pd, tQ, teo, x));
                 ++launches;
             }
             if (first && last) {
                 LAUNCH(DXPBD_K_TET_REPLAY, (k_tet_replay<true, true, 2><<<(s->T + 127) / 128, 128, 0, st>>>(
-                                               0, s->T, s->tdev(), s->inv_dt2d, tsc, s->pd, s->t_Q.p, teo, x, s->t_xsave.p)));
+                                               0, s->T, s->tdev(), s->inv_dt2d, tsc, s->pd, tQ, teo, x, s->t_xsave.p)));
                 ++launches;
                 if (s->pd) {
                     if (s->psd_minb == 3)
-                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<3><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p, s->psd_tol, s->psd_sweeps));
+                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<3><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
                     else if (s->psd_minb == 4)
-                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<4><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p, s->psd_tol, s->psd_sweeps));
+                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<4><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
                     else
-                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<1><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, s->t_Q.p, s->psd_tol, s->psd_sweeps));
+                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<1><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
                     ++launches;
                 }
             }
@@ -920,6 +923,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     // no distance constraints (tets and contacts only): tet + vertex matvec in one launch, q folded
     // into the update (tet_kernels.cuh k_cg_tetv)
     const bool tetv = s->T && E == 0 && !s->use_tma && s->tetv;
+    const float *const tQr = s->tq_r ? s->tq_r : s->t_Q.p;   // tet blocks of this substep
     const int nbt = tetv ? nblk(s->T) : 0;
     CGCGBufs cb{s->ax.p, s->p.p, {s->r.p, s->r1.p}, {s->p1.p, s->s1.p}, {s->q.p, s->w1.p}, s->rhs.p};
     auto cgcg_launch = [&](int i) {
@@ -950,10 +954,10 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             }
             if (tetv) {
                 if (s->tetv_minb == 3)
-                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<3><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), s->t_Q.p, bufs,
+                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<3><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
                                                                                          xw, Qc, cs, s->t_q4.p));
                 else
-                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<1><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), s->t_Q.p, bufs,
+                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<1><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
                                                                                          xw, Qc, cs, s->t_q4.p));
                 LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update_tet<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, Qc, cs, s->t_q4.p));
                 launches += 2;
@@ -968,7 +972,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
                 LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<0><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
             ++launches;
             if (s->T) {
-                LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), s->t_Q.p, bufs, xw, cs, s->t_q4.p));
+                LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), tQr, bufs, xw, cs, s->t_q4.p));
                 LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->t_q4.p, cs));
                 ++launches;
             }
@@ -1458,13 +1462,37 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     const bool fuse_start = s->use_tma && !s->T && !(s->cgcg && s->qf == 1);
     // replay of substep n-1 on the aux stream during the PCG of substep n (independent work: the
     // replay reads only checkpoints); blocks double-buffered, ordered by events
-    const bool ovl = s->overlap && s->use_tma && s->qf == 1 && !s->T && !s->NC && !g_comp && !s->cgcg;
+    const bool ovl_cloth = s->overlap && s->use_tma && s->qf == 1 && !s->T && !s->NC && !g_comp && !s->cgcg;
+    // tet-only scenes: the tet blocks (and material controls) are double-buffered the same way
+    const bool ovl_tet = s->overlap && s->T && E == 0 && !s->NC && !s->use_tma;
+    const bool ovl = ovl_cloth || ovl_tet;
+    const bool g_mat = ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) != 0;
+    auto set_write = [&](int k) {   // replay output buffers of parity k
+        if (ovl_tet) {
+            s->tq_w = k ? s->t_Q2.p : s->t_Q.p;
+            s->te_w = g_mat ? (k ? s->t_e2.p : s->t_e.p) : nullptr;
+        } else {
+            s->qt_write = k ? s->d_Qt2.p : s->d_Qt.p;
+        }
+    };
+    auto set_read = [&](int k) {
+        if (ovl_tet) {
+            s->tq_r = k ? s->t_Q2.p : s->t_Q.p;
+            s->te_r = g_mat ? (k ? s->t_e2.p : s->t_e.p) : nullptr;
+        } else {
+            s->qt_read = k ? s->d_Qt2.p : s->d_Qt.p;
+        }
+    };
     // blocks of the last substeps were cached by the forward (valid for the overlap path only)
     auto cached = [&](int n) { return ovl && s->qc_count > 0 && n >= s->qc_first && n < s->qc_first + s->qc_count; };
     cudaStream_t user_st = st;
     const int n_hi = std::min(N, last_key_state) - 1;
     if (ovl && n_hi >= 0) {
-        if (s->d_Qt2.n < s->d_Qt.n) s->d_Qt2.alloc(s->d_Qt.n);
+        if (ovl_cloth && s->d_Qt2.n < s->d_Qt.n) s->d_Qt2.alloc(s->d_Qt.n);
+        if (ovl_tet) {
+            if (s->t_Q2.n < s->t_Q.n) s->t_Q2.alloc(s->t_Q.n);
+            if (g_mat && s->t_e2.n < s->t_e.n) s->t_e2.alloc(s->t_e.n);
+        }
         if (!s->aux) {
             int least = 0, greatest = 0;
             DX_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -1484,7 +1512,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         user_st = st;
         st = s->hi;
         if (!cached(n_hi)) {
-            s->qt_write = (n_hi & 1) ? s->d_Qt2.p : s->d_Qt.p;
+            set_write(n_hi & 1);
             launches += replay_substep(s, n_hi, s->aux);
             DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[n_hi & 1], s->aux));
         }
@@ -1495,7 +1523,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         if (ovl) {
             if (n >= 1 && !cached(n - 1)) {   // blocks of substep n-1 into the buffer PCG(n+1) finished reading
                 if (n + 1 <= n_hi && !cached(n + 1)) DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_pcg[(n - 1) & 1], 0));
-                s->qt_write = ((n - 1) & 1) ? s->d_Qt2.p : s->d_Qt.p;
+                set_write((n - 1) & 1);
                 launches += replay_substep(s, n - 1, s->aux);
                 DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[(n - 1) & 1], s->aux));
             }
@@ -1503,7 +1531,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
                 s->qt_read = s->qcache.p + (size_t)(n - s->qc_first) * s->d_Qt.n;
             } else {
                 DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_rep[n & 1], 0));
-                s->qt_read = (n & 1) ? s->d_Qt2.p : s->d_Qt.p;
+                set_read(n & 1);
             }
         } else {
             s->qt_write = s->qt_read = nullptr;
@@ -1531,7 +1559,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             ++launches;
         }
         if (s->T) {
-            LAUNCH(DXPBD_K_RHS, k_rhs_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->t_Q.p, s->y.p, s->u0.p, s->rhs.p, s->r.p,
+            LAUNCH(DXPBD_K_RHS, k_rhs_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->tq_r ? s->tq_r : s->t_Q.p, s->y.p, s->u0.p, s->rhs.p, s->r.p,
                                                                         s->inv_mass.p));
             ++launches;
         }
@@ -1557,12 +1585,13 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             ++launches;
         }
         if (s->T && ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1)) {
-            LAUNCH(DXPBD_K_GRADS, k_grad_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->t_e.p, s->y.p, s->t_g.p));
+            LAUNCH(DXPBD_K_GRADS, k_grad_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->te_r ? s->te_r : s->t_e.p, s->y.p, s->t_g.p));
             ++launches;
         }
         if (ovl) DX_CHECK_CUDA(cudaEventRecord(s->ev_pcg[n & 1], st));   // buffer n & 1 free again
     }
     s->qt_read = s->qt_write = nullptr;
+    s->tq_w = s->te_w = s->tq_r = s->te_r = nullptr;
     if (st != user_st) {   // back onto the caller's stream
         DX_CHECK_CUDA(cudaEventRecord(s->ev_end, st));
         DX_CHECK_CUDA(cudaStreamWaitEvent(user_st, s->ev_end, 0));
