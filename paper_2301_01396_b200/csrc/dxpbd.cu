@@ -556,6 +556,8 @@ struct dxpbd_scene {
     int psd_minb = 3;                                  // its launch-bounds CTAs per SM (measured best)
     int qf = 0;   // Q format: 0 = sym6 SoA, 1 = iso+rank1 float4 (K = 1 with PD projection)
     DBuf<float> Qd, ed, Qc, ec;
+    DBuf<float> Qc2, ec2;                              // second contact block / control buffers (overlap)
+    float *qc_w = nullptr, *ec_w = nullptr, *qc_r = nullptr, *ec_r = nullptr;   // overlap: replay writes, PCG reads
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
     DBuf<float> cc_lam, cc_T, cc_sig, cc_B, cc_e;               // contact scratch (K>1)
     DBuf<double> cg_sc, acc;
@@ -776,11 +778,12 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         }
         if (s->NC) {
             float at = s->coll_alpha * inv_dt2;
-            float *eo = want_ce ? s->ec.p : nullptr;
-            if (first && last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
-            else if (first) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
-            else if (last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
-            else LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, s->Qc.p, eo, x));
+            float *eo = want_ce ? (s->ec_w ? s->ec_w : s->ec.p) : nullptr;
+            float *const Qcw = s->qc_w ? s->qc_w : s->Qc.p;
+            if (first && last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
+            else if (first) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
+            else if (last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
+            else LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
             ++launches;
         }
     }
@@ -913,7 +916,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     const int maxit = s->cg_max_iter;
     CGState cs{s->cg_sc.p, s->cg_sc.p + (size_t)(maxit + 1) * 4, s->cg_tol * s->cg_tol};
     const float *xw = s->inv_mass.p;
-    const float *Qc = s->NC ? s->Qc.p : nullptr;
+    const float *Qc = s->NC ? (s->qc_r ? s->qc_r : s->Qc.p) : nullptr;
     CGBufs bufs{s->ax.p, s->r.p, s->p.p, s->p1.p, s->q.p, nullptr};
     TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
     TmaTiles tt = s->tma_tiles();
@@ -1457,12 +1460,11 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     int launches = num_keys + 2, total_it = 0, max_it = 0;
     double worst = 0.0;
     int solves = 0;
-    const float *Qc = s->NC ? s->Qc.p : nullptr;
     // PCG start fused into the TMA rhs kernel (no tet rhs pass after it, standard PCG)
     const bool fuse_start = s->use_tma && !s->T && !(s->cgcg && s->qf == 1);
     // replay of substep n-1 on the aux stream during the PCG of substep n (independent work: the
     // replay reads only checkpoints); blocks double-buffered, ordered by events
-    const bool ovl_cloth = s->overlap && s->use_tma && s->qf == 1 && !s->T && !s->NC && !g_comp && !s->cgcg;
+    const bool ovl_cloth = s->overlap && s->use_tma && s->qf == 1 && !s->T && !g_comp && !s->cgcg;
     // tet-only scenes: the tet blocks (and material controls) are double-buffered the same way
     const bool ovl_tet = s->overlap && s->T && E == 0 && !s->NC && !s->use_tma;
     const bool ovl = ovl_cloth || ovl_tet;
@@ -1474,6 +1476,10 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         } else {
             s->qt_write = k ? s->d_Qt2.p : s->d_Qt.p;
         }
+        if (s->NC) {   // contact blocks and collider controls
+            s->qc_w = k ? s->Qc2.p : s->Qc.p;
+            s->ec_w = g_coll ? (k ? s->ec2.p : s->ec.p) : nullptr;
+        }
     };
     auto set_read = [&](int k) {
         if (ovl_tet) {
@@ -1482,6 +1488,10 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         } else {
             s->qt_read = k ? s->d_Qt2.p : s->d_Qt.p;
         }
+        if (s->NC) {
+            s->qc_r = k ? s->Qc2.p : s->Qc.p;
+            s->ec_r = g_coll ? (k ? s->ec2.p : s->ec.p) : nullptr;
+        }
     };
     // blocks of the last substeps were cached by the forward (valid for the overlap path only)
     auto cached = [&](int n) { return ovl && s->qc_count > 0 && n >= s->qc_first && n < s->qc_first + s->qc_count; };
@@ -1489,6 +1499,10 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     const int n_hi = std::min(N, last_key_state) - 1;
     if (ovl && n_hi >= 0) {
         if (ovl_cloth && s->d_Qt2.n < s->d_Qt.n) s->d_Qt2.alloc(s->d_Qt.n);
+        if (s->NC) {
+            if (s->Qc2.n < s->Qc.n) s->Qc2.alloc(s->Qc.n);
+            if (g_coll && s->ec2.n < s->ec.n) s->ec2.alloc(s->ec.n);
+        }
         if (ovl_tet) {
             if (s->t_Q2.n < s->t_Q.n) s->t_Q2.alloc(s->t_Q.n);
             if (g_mat && s->t_e2.n < s->t_e.n) s->t_e2.alloc(s->t_e.n);
@@ -1537,6 +1551,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             s->qt_write = s->qt_read = nullptr;
             launches += replay_substep(s, n, st);
         }
+        const float *Qc = s->NC ? (s->qc_r ? s->qc_r : s->Qc.p) : nullptr;   // contact blocks of substep n
         // b = M u_{n+1} - Q_n y_{n+1} + dphi/dx_{n+1} and the warm-start residual r0 = b - A_n u_{n+1}
         // (one tiled pass, own vertices stored once); the PCG then starts from u_n := u_{n+1}.
         DX_CHECK_CUDA(cudaMemsetAsync(s->cg_sc.p, 0, sizeof(double) * (size_t)(s->cg_max_iter + 2) * 4, st));
@@ -1581,7 +1596,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             ++launches;
         }
         if (g_coll && s->NC) {
-            LAUNCH(DXPBD_K_GRADS, k_grad_colliders<<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->ec.p, s->y.p, s->acc.p + 1));
+            LAUNCH(DXPBD_K_GRADS, k_grad_colliders<<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->ec_r ? s->ec_r : s->ec.p, s->y.p, s->acc.p + 1));
             ++launches;
         }
         if (s->T && ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1)) {
@@ -1592,6 +1607,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     }
     s->qt_read = s->qt_write = nullptr;
     s->tq_w = s->te_w = s->tq_r = s->te_r = nullptr;
+    s->qc_w = s->ec_w = s->qc_r = s->ec_r = nullptr;
     if (st != user_st) {   // back onto the caller's stream
         DX_CHECK_CUDA(cudaEventRecord(s->ev_end, st));
         DX_CHECK_CUDA(cudaStreamWaitEvent(user_st, s->ev_end, 0));

@@ -158,3 +158,26 @@ def test_schedule_switches_do_not_change_results(monkeypatch):
     assert la == lb
     for a, b in zip(ga, gb):
         np.testing.assert_array_equal(a, b)
+
+
+def test_contact_overlap_schedule_matches_serial(monkeypatch):
+    """Cloth with a sphere collider: replay of substep n-1 overlapped with the PCG of substep n
+    (contact blocks and collider controls double-buffered) against DXPBD_OVERLAP=0.  The cloth
+    path is deterministic, so the adjoint state gradients are bit-identical; the collider
+    gradient is a double-atomic sum over vertices (order may differ), so it is compared to 1e-12."""
+    api = _api()
+    s = f32(medium_cloth(n=48, frames=3))
+
+    def run():
+        sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=3, grad_flags=api.flags("sphere", "x0", "v0"))
+        api.dxpbd_forward(sc, s.x0, s.v0, s.forces, 3)
+        loss = api.dxpbd_backward(sc, s.key_frames, s.targets)
+        return loss, {k: api.dxpbd_grads(sc, k) for k in ("sphere", "x0", "v0")}
+
+    la, ga = run()
+    monkeypatch.setenv("DXPBD_OVERLAP", "0")
+    lb, gb = run()
+    assert la == lb
+    for k in ("x0", "v0"):
+        np.testing.assert_array_equal(ga[k], gb[k])
+    np.testing.assert_allclose(ga["sphere"], gb["sphere"], rtol=1e-12, atol=0)
