@@ -517,6 +517,8 @@ struct dxpbd_scene {
     // block cache (forward -> backward): the derivative blocks of substeps [qc_first, qc_first + qc_count)
     // computed during the forward (replay kernels in place of the projection) into spare HBM
     DBuf<float4> qcache;
+    DBuf<float> qccache;      // contact blocks (6V) [+ collider controls (12 NC V)] of the cached substeps
+    size_t qc_cper = 0;       // floats per cached substep in qccache
     int qc_first = 0, qc_count = 0;
     bool qcache_on = true;
     // colliders
@@ -665,7 +667,16 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             else LAUNCH(DXPBD_K_TET_PROJECT, k_tet_project<true, false><<<tb, 128, 0, st>>>(b, cnt, s->tdev(), s->inv_dt2d, s->lam_t.p, xo));
             ++launches;
         }
-        if (s->NC) {
+        if (s->NC && !rd && !wr && s->qc_count && n >= s->qc_first) {
+            // cached substep: the replay kernel (same iterate) also stores the contact blocks and controls
+            float at = s->coll_alpha * inv_dt2;
+            float *slot = s->qccache.p + (size_t)(n - s->qc_first) * s->qc_cper;
+            float *eo = s->qc_cper > (size_t)6 * V ? slot + (size_t)6 * V : nullptr;
+            ContactScratch cs{s->cc_lam.p, s->cc_T.p, s->cc_sig.p, s->cc_B.p, s->cc_e.p};
+            LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd,
+                                                                                                   slot, eo, xo));
+            ++launches;
+        } else if (s->NC) {
             float at = s->coll_alpha * inv_dt2;
             if (!rd && !wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
             else if (!rd && wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
@@ -1392,22 +1403,29 @@ int dxpbd_forward(dxpbd_scene *s, const float *x0, const float *v0, const float 
     forward_inputs(s, x0, v0, forces, num_frames, mem, st);
     int launches = 4;
     const int N = num_frames * s->substeps;
-    // block cache for the last substeps in spare HBM (K = 1 TMA path without colliders / tets /
-    // compliance gradients, which need the replay's other outputs)
+    // block cache for the last substeps in spare HBM (K = 1 TMA path without tets / compliance
+    // gradients, which need the replay's other outputs): distance blocks, and with colliders the
+    // per-vertex contact blocks and (collider gradients) the collider controls
     s->qc_count = 0;
-    if (s->qcache_on && s->use_tma && s->qf == 1 && !s->T && !s->NC && !((s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1) &&
-        N > 0) {
-        const size_t per = sizeof(float4) * s->d_Qt.n;
+    if (s->qcache_on && s->use_tma && s->qf == 1 && !s->T && !((s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1) &&
+        s->iterations == 1 && N > 0) {
+        const bool want_ce = (s->grad_flags & ((1u << DXPBD_GRAD_SHAPE) | (1u << DXPBD_GRAD_SPHERE))) != 0;
+        s->qc_cper = s->NC ? (size_t)6 * s->V + (want_ce ? (size_t)12 * s->NC * s->V : 0) : 0;
+        const size_t per = sizeof(float4) * s->d_Qt.n + sizeof(float) * s->qc_cper;
         size_t freeb = 0, totalb = 0;
         DX_CHECK_CUDA(cudaMemGetInfo(&freeb, &totalb));
-        freeb += s->qcache.n * sizeof(float4);   // the current cache is reusable
-        // keep room for the backward's buffers (~20 vertex vectors + the second block buffer) and 2 GB
+        freeb += s->qcache.n * sizeof(float4) + s->qccache.n * sizeof(float);   // the current cache is reusable
+        // keep room for the backward's buffers (~20 vertex vectors + the second block buffers) and 2 GB
         const size_t reserve = (size_t)24 * 16 * s->V + per + ((size_t)2 << 30);
         const int M = freeb > reserve ? (int)std::min<size_t>((size_t)N, (freeb - reserve) / 5 * 4 / per) : 0;
         if (M > 0) {
             if (s->qcache.n < (size_t)M * s->d_Qt.n) {
                 s->qcache.free();
                 s->qcache.alloc((size_t)M * s->d_Qt.n);
+            }
+            if (s->qccache.n < (size_t)M * s->qc_cper) {
+                s->qccache.free();
+                s->qccache.alloc((size_t)M * s->qc_cper);
             }
             s->qc_first = N - M;
             s->qc_count = M;
@@ -1543,6 +1561,11 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             }
             if (cached(n)) {
                 s->qt_read = s->qcache.p + (size_t)(n - s->qc_first) * s->d_Qt.n;
+                if (s->NC) {
+                    float *slot = s->qccache.p + (size_t)(n - s->qc_first) * s->qc_cper;
+                    s->qc_r = slot;
+                    s->ec_r = g_coll ? slot + (size_t)6 * V : nullptr;
+                }
             } else {
                 DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_rep[n & 1], 0));
                 set_read(n & 1);

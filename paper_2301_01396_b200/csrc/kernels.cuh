@@ -441,9 +441,13 @@ __global__ void __launch_bounds__(kBlock) k_contact_replay(int V, int NC, const 
     if (v >= V) return;
     double4 p = x[v];
     if (!(p.w > 0.f)) {
-        if (LAST) {
+        if (LAST) {   // pinned: zero block and zero controls (every output entry written each replay)
 #pragma unroll
             for (int k = 0; k < 6; ++k) Qc[(size_t)k * V + v] = 0.f;
+            if (eout)
+                for (int c = 0; c < NC; ++c)
+#pragma unroll
+                    for (int k = 0; k < 12; ++k) eout[k * (size_t)NC * V + (size_t)c * V + v] = 0.f;
         }
         return;
     }
