@@ -495,6 +495,7 @@ struct dxpbd_scene {
     // tets (color-sorted, internal vertex ids)
     DBuf<int4> t_idx;
     DBuf<double> t_Dm, t_vol;
+    DBuf<float> t_Dmf;
     DBuf<float> t_a, t_b, t_Q, t_e, t_g, lam_t;
     DBuf<double4> t_xsave;   // K = 1 tet replay: pre-update vertices of every tet [4T]
     DBuf<float> t_Q2, t_e2;  // second tet block / control buffers (replay / PCG overlap)
@@ -502,7 +503,7 @@ struct dxpbd_scene {
     DBuf<float4> t_q4;       // tet matvec accumulator (16-byte vector atomics), folded into q
     DBuf<int32_t> t_perm;
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
-    TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p}; }
+    TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p, t_Dmf.p}; }
     TmaTiles tma_tiles() const {
         return TmaTiles{n_dist_colors, ntiles, hcap, capm, d_tseg.p, d_cpair.p, d_hpad.p, qt_read ? qt_read : d_Qt.p,
                         qf == 1 ? nullptr : d_Qt2b.p, d_vslot.p, d_hslot.p};
@@ -1346,6 +1347,8 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         s->t_Dm.alloc((size_t)9 * T);
         s->t_vol.alloc(T);
         k_tet_rest<<<nblk(T), kBlock, 0, st>>>(T, s->t_idx.p, xr3.p, s->t_Dm.p, s->t_vol.p);
+        s->t_Dmf.alloc((size_t)9 * T);
+        k_d2f<<<nblk((int64_t)9 * T), kBlock, 0, st>>>((size_t)9 * T, s->t_Dm.p, s->t_Dmf.p);
         if (s->iterations > 1) s->lam_t.alloc((size_t)2 * T);
         DX_CHECK_CUDA(cudaGetLastError());
         DX_CHECK_CUDA(cudaStreamSynchronize(st));

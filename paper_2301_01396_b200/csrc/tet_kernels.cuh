@@ -21,6 +21,7 @@ struct TetDev {
     const double *Dm;     // [9T] Dm^-1 SoA (fp64), element (i, col) at (3*i + col) * T + j
     const double *vol;    // [T] rest volume (fp64)
     const float *ta, *tb; // [T] material a, b
+    const float *Dmf;     // [9T] Dm^-1 rounded to fp32 (the fp32 kernels' copy: half the bytes)
 };
 
 struct TetCore {
@@ -51,6 +52,20 @@ DX_INLINE void tet_load_c(const TetDev &D, int j, R (&c)[4][3]) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             c[i + 1][col] = D.Dm[(size_t)(3 * i + col) * D.T + j];
+            s += c[i + 1][col];
+        }
+        c[0][col] = -s;
+    }
+}
+
+// fp32 coefficients: the same values as the template above with R = float (rounded once at create)
+DX_INLINE void tet_load_c(const TetDev &D, int j, float (&c)[4][3]) {
+#pragma unroll
+    for (int col = 0; col < 3; ++col) {
+        float s = 0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            c[i + 1][col] = D.Dmf[(size_t)(3 * i + col) * D.T + j];
             s += c[i + 1][col];
         }
         c[0][col] = -s;
@@ -690,6 +705,11 @@ __global__ void k_grad_tet(TetDev D, const float *__restrict__ e, const float3 *
 }
 
 // rest quantities: Dm^-1 (SoA) and volume from internal rest positions
+__global__ void k_d2f(size_t n, const double *__restrict__ a, float *__restrict__ b) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (float)a[i];
+}
+
 __global__ void k_tet_rest(int T, const int4 *__restrict__ idx, const float *__restrict__ xr, double *__restrict__ Dm,
                            double *__restrict__ vol) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
