@@ -68,7 +68,7 @@ typedef struct dxpbd_scene_desc {
     const int32_t *dist_idx;         /* [E][2] vertex ids, distinct, < V                     */
     const float *dist_compliance;    /* [E] alpha >= 0 (PAPER.md Eq. xpbdUenergy l.76)      */
 
-    /* stable Neo-Hookean tets (Sec.5.2 l.229; R6)                        */
+    /* Neo-Hookean tets, C_D = ||F|| - sqrt3, C_H = det F - 1 (Sec.5.2 l.229; R6)   */
     int32_t num_tets;                /* T >= 0                                              */
     const int32_t *tet_idx;          /* [T][4] vertex ids, positive rest orientation        */
     const float *tet_a;              /* [T] a, mu = a^2                                     */

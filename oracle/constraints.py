@@ -7,8 +7,10 @@ Families (BASELINE.json north_star):
   * distance   C = |x_a - x_b| - L          (cloth stretch/shear/bend; Eq.1 C(x))
   * sphere     C = |x - c| - r - h          ("stiff springs ... thickness")
   * capsule    C = |x - cp(x)| - r - h      (same; cp = closest point on the segment)
-  * tet_dev    C_D = sqrt(tr(F^T F))
-  * tet_hyd    C_H = det(F) - gamma         (gamma = 1 + mu/lambda: DESIGN.md R6)
+  * tet_dev    C_D = sqrt(tr(F^T F)) - sqrt(3)   (offset so that C_D(I) = 0: DESIGN.md R6)
+  * tet_hyd    C_H = det(F) - 1                  (PAPER.md l.229 as printed; R6)
+  Both vanish at the rest state F = I, so U = 1/2 C^T alpha^-1 C (Eq. xpbdUenergy l.76) is zero
+  there and the rest state is a fixed point of the XPBD substep (reading R6).
 """
 from __future__ import annotations
 
@@ -113,21 +115,25 @@ def tet_F(xs: np.ndarray, Dminv: np.ndarray):
     return Ds @ Dminv
 
 
+SQRT3 = np.sqrt(3.0)
+
+
 def tet_dev_F(F: np.ndarray):
-    """C_D = ||F||_F; returns C, dC/dvecF (T,9), d2C/dvecF2 (T,9,9)."""
+    """C_D = ||F||_F - sqrt(3); returns C, dC/dvecF (T,9), d2C/dvecF2 (T,9,9)."""
     f = F.transpose(0, 2, 1).reshape(len(F), 9)
-    C = np.linalg.norm(f, axis=1)
-    P = f / C[:, None]
-    HF = (np.eye(9)[None] - _outer(P, P)) / C[:, None, None]
+    nrm = np.linalg.norm(f, axis=1)
+    C = nrm - SQRT3
+    P = f / nrm[:, None]
+    HF = (np.eye(9)[None] - _outer(P, P)) / nrm[:, None, None]
     return C, P, HF
 
 
-def tet_hyd_F(F: np.ndarray, gamma: np.ndarray):
-    """C_H = det F - gamma; dC/dF = cof(F) = [f1 x f2, f2 x f0, f0 x f1]."""
+def tet_hyd_F(F: np.ndarray):
+    """C_H = det F - 1; dC/dF = cof(F) = [f1 x f2, f2 x f0, f0 x f1]."""
     f0, f1, f2 = F[:, :, 0], F[:, :, 1], F[:, :, 2]
     c0, c1, c2 = np.cross(f1, f2), np.cross(f2, f0), np.cross(f0, f1)
     det = np.einsum("ni,ni->n", f0, c0)
-    C = det - gamma
+    C = det - 1.0
     P = np.concatenate([c0, c1, c2], 1)
     HF = np.zeros((len(F), 9, 9))
     # block (i,j) = d cof_i / d f_j ; d(a x b)/da = -[b]x, d(a x b)/db = [a]x
@@ -140,13 +146,13 @@ def tet_hyd_F(F: np.ndarray, gamma: np.ndarray):
     return C, P, HF
 
 
-def tet(xs: np.ndarray, Dminv: np.ndarray, G: np.ndarray, kind: str, gamma=None, need_H=True):
+def tet(xs: np.ndarray, Dminv: np.ndarray, G: np.ndarray, kind: str, need_H=True):
     """Returns C, g (T,12) = G^T dC/dvecF, H (T,12,12) = G^T H_F G (None if not need_H)."""
     F = tet_F(xs, Dminv)
     if kind == "D":
         C, P, HF = tet_dev_F(F)
     else:
-        C, P, HF = tet_hyd_F(F, gamma)
+        C, P, HF = tet_hyd_F(F)
     g = np.einsum("nij,ni->nj", G, P)
     H = np.einsum("nai,nab,nbj->nij", G, HF, G) if need_H else None
     return C, g, H

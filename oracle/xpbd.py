@@ -120,7 +120,6 @@ class OracleModel:
             dt2 = self.dt ** 2
             self.at_D = 1.0 / (self.ta ** 2 * self.vol * dt2)
             self.at_H = 1.0 / (self.tb ** 2 * self.vol * dt2)
-            self.gamma = 1.0 + self.ta ** 2 / self.tb ** 2
 
     def set_shape(self, beta):
         s = self.s
@@ -208,20 +207,19 @@ class OracleModel:
                            datdu=np.full((n, 1), 1.0 / self.dt ** 2)))
 
     def ev_tet(self, x, grp, need_H=True):
-        """stable Neo-Hookean block (PAPER.md Sec.5.2, R6): rows (C_D, C_H) solved together;
-        controls u = (a, b), mu = a^2, lambda = b^2, alpha_D = 1/(mu V), alpha_H = 1/(lambda V),
-        gamma = 1 + mu/lambda."""
+        """Neo-Hookean block (Sec.5.2 l.229, R6): rows (C_D, C_H) = (||F|| - sqrt3,
+        det F - 1) solved together; controls u = (a, b), mu = a^2, lambda = b^2,
+        alpha_D = 1/(mu V), alpha_H = 1/(lambda V).  C does not depend on u (dC/du = 0)."""
         n = len(grp)
         a, b, V = self.ta[grp], self.tb[grp], self.vol[grp]
         dt2 = self.dt ** 2
         st = self.tet_idx[grp]
         CD, gD, HD = cf.tet(x[st], self.Dminv[grp], self.G[grp], "D", need_H=need_H)
-        CH, gH, HH = cf.tet(x[st], self.Dminv[grp], self.G[grp], "H", self.gamma[grp], need_H=need_H)
+        CH, gH, HH = cf.tet(x[st], self.Dminv[grp], self.G[grp], "H", need_H=need_H)
         z = np.zeros(n)
         datdu = np.stack([np.stack([-2.0 / (a ** 3 * V * dt2), z], 1),        # d/da (rows D, H)
                           np.stack([z, -2.0 / (b ** 3 * V * dt2)], 1)], 1)     # d/db
-        dCdu = np.stack([np.stack([z, -2.0 * a / b ** 2], 1),                  # d(-gamma)/da
-                         np.stack([z, 2.0 * a ** 2 / b ** 3], 1)], 1)          # d(-gamma)/db
+        dCdu = np.zeros((n, 2, 2))
         return dict(C=np.stack([CD, CH], 1), g=np.stack([gD, gH], 1),
                     H=np.stack([HD, HH], 1) if need_H else None,
                     len=np.ones(n), dCdu=dCdu, dgdu=np.zeros((n, 2, 2, 12)), datdu=datdu)

@@ -1,6 +1,6 @@
-// Tetrahedral stable Neo-Hookean block constraints (Sec.5.2 l.229; R6):
-// per tet the rows (C_D, C_H) = (||F||_F, det F - gamma), gamma = 1 + mu/lambda, are projected
-// together as one 2-row block (Eq. xpbd in matrix form), alpha_D = 1/(mu V), alpha_H = 1/(lambda V),
+// Tetrahedral Neo-Hookean block constraints (Sec.5.2 l.229; R6):
+// per tet the rows (C_D, C_H) = (||F||_F - sqrt 3, det F - 1), both zero at the rest state F = I
+// (Eq. xpbdUenergy l.76: U = 0 at rest), are projected together as one 2-row block (Eq. xpbd in matrix form), alpha_D = 1/(mu V), alpha_H = 1/(lambda V),
 // mu = a^2, lambda = b^2.  Everything in deformation-gradient coordinates vec F = G x (column-
 // major, index 3*col + row): grad C_a = G^T P_a, H_a = G^T HF_a G, M^-1 -> W~ = K (x) I3 with
 // K = Sum_v w_v c_v c_v^T, c_v the Dm^-1 coefficients of vertex v.  Derivative blocks are
@@ -34,7 +34,6 @@ struct TetCore {
     tr J[2][2], Ji[2][2];
     tr at[2];
     tr dl[2];
-    tr gamma;
 };
 DX_INLINE double3 operator+(double3 a, double3 b) { return make_double3(a.x + b.x, a.y + b.y, a.z + b.z); }
 DX_INLINE double3 operator-(double3 a, double3 b) { return make_double3(a.x - b.x, a.y - b.y, a.z - b.z); }
@@ -107,7 +106,7 @@ DX_INLINE void tet_HH_mul(const TetCore &o, const tr *v, tr *out) {
 }
 
 // Projection core (Eq. xpbd, 2-row block), fp64.  Returns false when skipped (R13).
-DX_INLINE bool tet_core(const double4 (&x)[4], const tr (&c)[4][3], tr at0, tr at1, tr gam, const tr (&lam0)[2],
+DX_INLINE bool tet_core(const double4 (&x)[4], const tr (&c)[4][3], tr at0, tr at1, const tr (&lam0)[2],
                         TetCore &o) {
     tr w[4];
 #pragma unroll
@@ -142,9 +141,8 @@ DX_INLINE bool tet_core(const double4 (&x)[4], const tr (&c)[4][3], tr at0, tr a
     dput3(o.P[1], 1, c1);
     dput3(o.P[1], 2, c2);
     const tr det = ddot3p(f0, c0);
-    o.gamma = gam;
-    o.C[0] = o.CD;
-    o.C[1] = det - gam;
+    o.C[0] = o.CD - 1.7320508075688772;   // ||F|| - sqrt 3
+    o.C[1] = det - 1.0;
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -210,10 +208,9 @@ __global__ void __launch_bounds__(128) k_tet_project(int begin, int count, TetDe
     double4 xs[4] = {x[id.x], x[id.y], x[id.z], x[id.w]};
     tr c[4][3];
     tet_load_c(D, j, c);
-    const tr a = D.ta[j], b = D.tb[j];
     tr lam0[2] = {READ_LAM ? (tr)lam[2 * j] : 0.0, READ_LAM ? (tr)lam[2 * j + 1] : 0.0};
     TetCore o;
-    if (!tet_core(xs, c, tet_at(D, j, 0, inv_dt2), tet_at(D, j, 1, inv_dt2), 1.0 + (a * a) / (b * b), lam0, o)) return;
+    if (!tet_core(xs, c, tet_at(D, j, 0, inv_dt2), tet_at(D, j, 1, inv_dt2), lam0, o)) return;
     if (WRITE_LAM) {
         lam[2 * j] = (float)(lam0[0] + o.dl[0]);
         lam[2 * j + 1] = (float)(lam0[1] + o.dl[1]);
@@ -321,9 +318,9 @@ struct TetScratch {
 // Differentiable replay of one tet color (Sec.4.3/4.4, R3, R5, R6) in F-space:
 //   Dx~ = W~ Sum_b P_b dl_b ; j_a = HF_a Dx~ + Sum_b dl_b HF_b (W~ P_a)
 //   s~_a = Sum_b Ji_ab (-P_b - at_b S~_b - j_b) ;  D~ += Sum_a dl_a HF_a + Sum_a P_a s~_a^T ; S~ += s~
-// controls u = (a, b): t_u = Ji (-dC/du - dat/du lam0 - at T_u - diag(dat/du) dl) ;
+// controls u = (a, b): t_u = Ji (-dat/du lam0 - at T_u - diag(dat/du) dl) ;   (dC/du = 0, R6)
 //   e~_u += Sum_a t_{u,a} P_a ;  T_u += t_u
-//   dat_D/da = -2 at_D / a, dat_H/db = -2 at_H / b, dC_H/da = -2a/b^2, dC_H/db = 2a^2/b^3.
+//   dat_D/da = -2 at_D / a, dat_H/db = -2 at_H / b.
 // After the last iteration: Qt~ = psd(-sym D~) (45 floats, upper triangle) and e~ (18 floats).
 // MODE 0: one pass per color (any K).  K = 1 splits it in two so the heavy derivative algebra and
 // the 9x9 PSD projection run once over all tets instead of color by color (a color is a few
@@ -370,7 +367,7 @@ __global__ void __launch_bounds__(128) k_tet_replay(int begin, int count, TetDev
     }
     const tr at0 = tet_at(D, j, 0, inv_dt2), at1 = tet_at(D, j, 1, inv_dt2);
     TetCore o;
-    const bool ok = tet_core(xs, c, at0, at1, 1.0 + (a * a) / (b * b), lam0, o);
+    const bool ok = tet_core(xs, c, at0, at1, lam0, o);
     if (MODE == 1) {
         if (ok) {
             tet_apply(xs, o);
@@ -430,11 +427,10 @@ __global__ void __launch_bounds__(128) k_tet_replay(int begin, int count, TetDev
             for (int k = 0; k < 9; ++k) S[r][k] += sv[r][k];
         // controls (a, b)
         const tr datdu[2][2] = {{-2.0 * at0 / a, 0.0}, {0.0, -2.0 * at1 / b}};   // [u][row]
-        const tr dCdu[2][2] = {{0.0, -2.0 * a / (b * b)}, {0.0, 2.0 * a * a / (b * b * b)}};
         for (int u = 0; u < 2; ++u) {
             tr rr[2];
             for (int r = 0; r < 2; ++r)
-                rr[r] = -dCdu[u][r] - datdu[u][r] * lam0[r] - o.at[r] * Tu[u][r] - datdu[u][r] * o.dl[r];
+                rr[r] = -datdu[u][r] * lam0[r] - o.at[r] * Tu[u][r] - datdu[u][r] * o.dl[r];
             const tr t0 = o.Ji[0][0] * rr[0] + o.Ji[0][1] * rr[1];
             const tr t1 = o.Ji[1][0] * rr[0] + o.Ji[1][1] * rr[1];
             for (int k = 0; k < 9; ++k) e[u][k] += t0 * o.P[0][k] + t1 * o.P[1][k];

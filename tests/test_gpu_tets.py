@@ -1,11 +1,11 @@
-"""GPU parity for the tetrahedral stable Neo-Hookean blocks (configs[2] regime: 1.03 cm spacing,
+"""GPU parity for the tetrahedral Neo-Hookean blocks (configs[2] regime: 1.03 cm spacing,
 dt = 1/1200 s, E ~ U(1e4, 1e6) Pa, nu ~ U(0.3, 0.45)): positions within 1e-4 and material /
 initial-state gradients within 1e-3 relative L2 vs the fp64 oracle.
 
-Horizons: with one Gauss-Seidel iteration per substep the stiff block is chaotic in the fp64
-oracle itself (a 1e-9 m perturbation of x0 grows to ~1e-1 relative within 40 substeps;
-DESIGN.md "Conditioning"), so parity at the config's stiffness is asserted over 2-3 substeps, and
-over a full 20-substep frame for E <= 1e5 Pa where the oracle's own sensitivity stays ~1e-6."""
+With C_D = ||F|| - sqrt 3 and C_H = det F - 1 (reading R6) the rest state is a fixed point and the
+block is well conditioned at the config's stiffness (oracle pins in tests/test_oracle_forward.py),
+so parity is asserted over whole frames (20 substeps): at 40^3 (full size) forward, at 16^3
+(multi-tile) forward + adjoint."""
 import numpy as np
 import pytest
 
@@ -29,19 +29,32 @@ def _block(n, substeps, iterations=1, soft=False, frames=1):
 
 
 @pytest.mark.parametrize("iters", [1, 2])
-def test_volumetric_stiff_short(iters):
-    s = _block(6, 3, iters)
+def test_volumetric_stiff_frame(iters):
+    """configs[2] stiffness, one full frame (20 substeps), 6^3 vertices."""
+    s = _block(6, 20, iters)
+    g = gpu_run(s, ("material",))
+    o = oracle_run(s)
+    assert np.abs(o["x"][-1] - o["x"][0]).max() > 1e-4   # the block actually sags
+    _compare(g, o, ("material", "v0", "x0"))
+
+
+def test_volumetric_two_frames():
+    """Two frames of 20 substeps at the config's stiffness, keyframe at the end (8^3)."""
+    s = _block(8, 20, frames=2)
     g = gpu_run(s, ("material",))
     o = oracle_run(s)
     _compare(g, o, ("material", "v0", "x0"))
 
 
-def test_volumetric_soft_frame():
-    s = _block(6, 20, soft=True)
+def test_volumetric_mid_size_frame_backward():
+    """16^3 vertices (16875 tets, several PCG tiles), config stiffness, one frame x 20 substeps,
+    forward + adjoint: positions and material gradients element-wise diagnostics."""
+    s = _block(16, 20)
     g = gpu_run(s, ("material",))
     o = oracle_run(s)
-    assert np.abs(o["x"][-1] - o["x"][0]).max() > 1e-4   # the block actually deforms
     _compare(g, o, ("material", "v0", "x0"))
+    d = np.abs(np.asarray(g["material"], float) - o["material"])
+    assert d.max() <= 1e-2 * np.abs(o["material"]).max(), d.max()
 
 
 def test_volumetric_no_pd():
@@ -59,19 +72,12 @@ def test_tet_coloring_bit_exact():
     np.testing.assert_array_equal(api.dxpbd_coloring(g["scene"], 1), greedy_color(s.tet_idx, s.num_vertices))
 
 
-def test_volumetric_mid_size_soft_forward():
-    """16^3 vertices (16875 tets), softer material, 1 frame x 20 substeps."""
-    s = _block(16, 20, soft=True)
+def test_volumetric_full_size_forward_frame():
+    """configs[2] at full size (40^3 vertices, ~300k tets), one full frame (20 substeps) at its dt."""
+    s = _block(40, 20)
     g = gpu_run(s, backward=False)
     o = oracle_run(s, backward=False)
-    assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
-
-
-def test_volumetric_full_size_forward_substeps():
-    """configs[2] at full size (40^3 vertices, ~300k tets), 2 substeps at its dt."""
-    s = _block(40, 2)
-    g = gpu_run(s, backward=False)
-    o = oracle_run(s, backward=False)
+    assert np.abs(o["x"][-1] - o["x"][0]).max() > 1e-4
     assert rel_l2(g["x"][-1], o["x"][-1]) < 1e-4
 
 

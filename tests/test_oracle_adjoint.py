@@ -428,3 +428,54 @@ def test_tet_material_fd_sanity():
     ga = np.concatenate([gr["material"][:, 0], gr["material"][:, 1]])[sel]
     cos = g @ ga / (np.linalg.norm(g) * np.linalg.norm(ga))
     assert cos > 0.98, cos
+
+
+# ----------------------------------------------------------------------------------------------
+# Tet PD projection in deformation-gradient coordinates (Sec.4.3.2 l.201, reading R5):
+# Q = G^T psd(-sym D~) G with D~ = Gp^T D Gp.  Pinned without re-deriving the formula: the
+# result must be PSD, keep the translation null space, equal -sym(D) when that is already PSD,
+# and its F-space image must be the Frobenius-nearest PSD matrix to -S (checked against random
+# PSD candidates).
+# ----------------------------------------------------------------------------------------------
+def _tet_blocks_case(S):
+    from synth import tet_block
+    t = tet_block(2, 0.3, 1000.0, seed=4)
+    s = mk(t["x_rest"], t["inv_mass"] + 1.0, tet_idx=t["tet_idx"][:3], tet_a=t["tet_a"][:3],
+           tet_b=t["tet_b"][:3])
+    m = OracleModel(s, pd_projection=True)
+    rec = m.new_record()
+    rec["tet.D"] = np.einsum("nai,nab,nbj->nij", m.G, S, m.G)    # D = G^T S G (a function of F)
+    return m, m.blocks(rec)["tet"]
+
+
+def test_tet_fspace_pd_projection_psd_input_unchanged():
+    Z = rng.normal(size=(3, 9, 9))
+    S = -(Z @ np.swapaxes(Z, 1, 2))                      # -S PSD
+    m, Q = _tet_blocks_case(S)
+    D = np.einsum("nai,nab,nbj->nij", m.G, S, m.G)
+    np.testing.assert_allclose(Q, -0.5 * (D + np.swapaxes(D, 1, 2)), atol=1e-9 * np.abs(D).max())
+
+
+def test_tet_fspace_pd_projection_properties():
+    B = rng.normal(size=(3, 9, 9))
+    S = B + np.swapaxes(B, 1, 2)                         # indefinite
+    m, Q = _tet_blocks_case(S)
+    for j in range(3):
+        ev = np.linalg.eigvalsh(Q[j])
+        assert ev.min() >= -1e-9 * np.abs(ev).max()
+        assert np.sum(ev > 1e-9 * np.abs(ev).max()) <= 9           # rank <= 9 (image of G^T)
+        tr = np.tile(rng.normal(size=3), 4)                        # rigid translation
+        assert np.abs(Q[j] @ tr).max() < 1e-9 * np.abs(Q[j]).max()
+        # F-space image: G Q G^T = (G G^T) P (G G^T) with P the projected matrix; recover P
+        GGt = m.G[j] @ m.G[j].T
+        P = np.linalg.solve(GGt, np.linalg.solve(GGt, m.G[j] @ Q[j] @ m.G[j].T).T).T
+        assert np.abs(P - P.T).max() < 1e-9 * np.abs(P).max()
+        assert np.linalg.eigvalsh(P).min() >= -1e-9 * np.abs(P).max()
+        # Frobenius-nearest PSD matrix to -S[j]
+        dP = np.linalg.norm(-S[j] - P)
+        for _ in range(50):
+            Z = rng.normal(size=(9, int(rng.integers(1, 10))))
+            assert dP <= np.linalg.norm(-S[j] - Z @ Z.T) + 1e-12
+        for _ in range(50):                                        # nor any nearby PSD matrix P + e v v^T
+            v = rng.normal(size=9)
+            assert dP <= np.linalg.norm(-S[j] - P - 1e-2 * np.outer(v, v)) + 1e-12

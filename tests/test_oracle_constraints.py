@@ -109,20 +109,32 @@ def _unit_tet():
 
 
 def test_tet_rest_values():
+    """PAPER.md l.229 (reading R6): C_D = ||F||_F - sqrt 3 and C_H = det F - 1 both vanish at
+    rest (F = I), so U = 1/2 C^T alpha^-1 C (Eq. xpbdUenergy l.76) is zero there."""
     x, t = _unit_tet()
     Dminv, vol = cf.tet_rest(x, t)
     assert vol[0] == pytest.approx(1 / 6)
     G = cf.tet_G(Dminv)
     C, g, H = cf.tet(x[t], Dminv, G, "D")
-    assert C[0] == pytest.approx(np.sqrt(3), abs=1e-12)
-    gamma = np.array([1.25])
-    C, g, H = cf.tet(x[t], Dminv, G, "H", gamma)
-    assert C[0] == pytest.approx(1 - 1.25, abs=1e-12)
-    # F = 2I: C_D = sqrt(12), det = 8
+    assert C[0] == pytest.approx(0.0, abs=1e-12)
+    # grad C_D at F = I: dC/dF = I/sqrt3 -> vertex 1 gets column 0 of F: (1, 0, 0)/sqrt3
+    np.testing.assert_allclose(g[0].reshape(4, 3)[1], [1 / np.sqrt(3), 0, 0], atol=1e-12)
+    C, g, H = cf.tet(x[t], Dminv, G, "H")
+    assert C[0] == pytest.approx(0.0, abs=1e-12)
+    # grad C_H at F = I: cof(I) = I
+    np.testing.assert_allclose(g[0].reshape(4, 3)[2], [0, 1, 0], atol=1e-12)
+    # F = 2I: C_D = sqrt(12) - sqrt(3) = sqrt(3), det = 8
     C, *_ = cf.tet(2 * x[t], Dminv, G, "D")
-    assert C[0] == pytest.approx(np.sqrt(12), abs=1e-12)
-    C, *_ = cf.tet(2 * x[t], Dminv, G, "H", np.array([1.0]))
+    assert C[0] == pytest.approx(np.sqrt(3), abs=1e-12)
+    C, *_ = cf.tet(2 * x[t], Dminv, G, "H")
     assert C[0] == pytest.approx(7.0, abs=1e-12)
+    # pure shear F = [[1, 0.5, 0], [0, 1, 0], [0, 0, 1]]: det = 1, ||F||^2 = 3.25
+    xs = x.copy()
+    xs[2] = [0.5, 1.0, 0.0]
+    C, *_ = cf.tet(xs[t], Dminv, G, "H")
+    assert C[0] == pytest.approx(0.0, abs=1e-12)
+    C, *_ = cf.tet(xs[t], Dminv, G, "D")
+    assert C[0] == pytest.approx(np.sqrt(3.25) - np.sqrt(3), abs=1e-12)
 
 
 def test_regular_tet_volume():
@@ -138,11 +150,10 @@ def test_tet_fd_and_invariances(kind, trial):
     t = np.array([[0, 1, 2, 3]])
     Dminv, vol = cf.tet_rest(xr, t)
     G = cf.tet_G(Dminv)
-    gam = np.array([1.3])
     xs = xr + 0.2 * rng.normal(size=(4, 3))
-    f = lambda y: cf.tet(y.reshape(1, 4, 3), Dminv, G, kind, gam)[0][0]
-    gg = lambda y: cf.tet(y.reshape(1, 4, 3), Dminv, G, kind, gam)[1][0]
-    C, g, H = cf.tet(xs[None], Dminv, G, kind, gam)
+    f = lambda y: cf.tet(y.reshape(1, 4, 3), Dminv, G, kind)[0][0]
+    gg = lambda y: cf.tet(y.reshape(1, 4, 3), Dminv, G, kind)[1][0]
+    C, g, H = cf.tet(xs[None], Dminv, G, kind)
     assert rel(g[0], fd_jac(f, xs.ravel())) < 1e-7
     assert rel(H[0], fd_jac(gg, xs.ravel())) < 1e-6
     assert np.abs(H[0] - H[0].T).max() < 1e-10 * np.abs(H[0]).max()
