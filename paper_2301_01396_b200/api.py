@@ -139,6 +139,22 @@ class _Arg:
             self.mem = MEM_HOST
 
 
+def _out_arg(out, n: int, what: str) -> _Arg:
+    """Output buffer of a call that writes n floats: must be float32, contiguous and hold exactly n
+    elements (the library writes in place; a silently converted copy would hide the result)."""
+    if torch is not None and isinstance(out, torch.Tensor):
+        ok = out.dtype == torch.float32 and out.is_contiguous() and out.numel() == n
+    else:
+        ok = (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.flags.c_contiguous
+              and out.flags.writeable and out.size == n)
+    if not ok:
+        raise ValueError(f"{what}: `out` must be a contiguous writeable float32 buffer of {n} elements "
+                         f"(got {type(out).__name__} {getattr(out, 'dtype', None)} {tuple(getattr(out, 'shape', ()))})")
+    a = _Arg(out, np.float32)
+    assert a.ptr == (out.data_ptr() if not isinstance(out, np.ndarray) else out.ctypes.data)
+    return a
+
+
 def _host(a, dtype=np.float32):
     if a is None:
         return None
@@ -258,7 +274,7 @@ def dxpbd_forward(scene: DxScene, x0, v0, forces=None, num_frames: int = 1):
 def dxpbd_positions(scene: DxScene, frame: int, out=None):
     if out is None:
         out = np.zeros((scene.V, 3), np.float32)
-    a = _Arg(out, np.float32)
+    a = _out_arg(out, 3 * scene.V, "dxpbd_positions")
     _check(lib().dxpbd_positions(scene.handle, int(frame), a.ptr, a.mem, _stream(out)), "dxpbd_positions")
     return out
 
@@ -284,8 +300,8 @@ def dxpbd_grads(scene: DxScene, kind, out=None):
     shape = _grad_size(scene, kind)
     if out is None:
         out = np.zeros(shape, np.float32)
-    a = _Arg(out, np.float32)
     n = int(np.prod(shape))
+    a = _out_arg(out, n, "dxpbd_grads")
     _check(lib().dxpbd_grads(scene.handle, int(kind), a.ptr, n, a.mem, _stream(out)), "dxpbd_grads")
     return out
 
@@ -393,7 +409,7 @@ def dxpbd_group_forward(group: DxGroup, x0, v0, forces=None, num_frames: int = 1
 def dxpbd_group_positions(group: DxGroup, frame: int, out=None):
     if out is None:
         out = np.zeros((group.V, 3), np.float32)
-    a = _Arg(out, np.float32)
+    a = _out_arg(out, 3 * group.V, "dxpbd_group_positions")
     _check(lib().dxpbd_group_positions(group.handle, int(frame), a.ptr, a.mem, _stream(out)), "dxpbd_group_positions")
     return out
 
@@ -413,7 +429,7 @@ def dxpbd_group_grads(group: DxGroup, kind, out=None):
     shape = _grad_size(group, kind)
     if out is None:
         out = np.zeros(shape, np.float32)
-    a = _Arg(out, np.float32)
+    a = _out_arg(out, int(np.prod(shape)), "dxpbd_group_grads")
     _check(lib().dxpbd_group_grads(group.handle, int(kind), a.ptr, int(np.prod(shape)), a.mem, _stream(out)),
            "dxpbd_group_grads")
     return out

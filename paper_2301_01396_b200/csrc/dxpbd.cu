@@ -1006,7 +1006,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         DX_CHECK_CUDA(cudaMemcpyAsync(s->h_scal, s->cg_sc.p, sizeof(double) * (size_t)(maxit + 2) * 4, cudaMemcpyDeviceToHost, st));
         DX_CHECK_CUDA(cudaStreamSynchronize(st));
         double bb = s->h_scal[(size_t)(maxit + 1) * 4];
-        double tol2 = (double)s->cg_tol * s->cg_tol;
+        const double tol2 = (double)cs.tol2;   // the kernels' cg_done threshold, bit for bit
         if (bb == 0.0) { iters_out = 0; relres_out = 0.0; break; }
         for (int k = 0; k <= it; ++k) {
             double rr = s->h_scal[k * 4 + 2];

@@ -48,3 +48,21 @@ def test_sm100a_cubin():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", b.build()], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_out_buffer_validation():
+    """dxpbd_grads / dxpbd_positions write in place: a wrong-size, wrong-dtype or non-contiguous
+    `out` is rejected before the call (no silent copy, no write past the end)."""
+    import numpy as np
+    from paper_2301_01396_b200 import api
+    good = np.zeros((4, 3), np.float32)
+    assert api._out_arg(good, 12, "t").ptr == good.ctypes.data
+    for bad in (np.zeros((4, 3), np.float64), np.zeros((5, 3), np.float32), np.zeros((3, 8), np.float32)[:, ::2],
+                np.zeros((2, 3), np.float32)):
+        with pytest.raises(ValueError):
+            api._out_arg(bad, 12, "t")
+    import torch
+    with pytest.raises(ValueError):
+        api._out_arg(torch.zeros(13), 12, "t")
+    t = torch.zeros(12)
+    assert api._out_arg(t, 12, "t").ptr == t.data_ptr()
