@@ -78,12 +78,33 @@ def test_forces_keyframes_small():
 
 
 def test_garment_capsules_small():
-    """configs[3] shape at reduced size: tube over the 12-capsule body, shape gradients."""
-    s = f32(garment(n_around=20, n_along=14, frames=4))
+    """configs[3] shape at reduced size (20 x 14 tube), draped state, shape gradients."""
+    from tests.garment_case import garment_case
+    s = garment_case(20, 14, warm_frames=10, frames=4)
     grads = ("shape", "compliance")
     g = gpu_run(s, grads)
     o = oracle_run(s)
     _compare(g, o, ("shape", "compliance", "v0"))
+
+
+def test_garment_multitile_shape_gradient():
+    """configs[3] at 64 x 48 (several PCG tiles), started from the oracle's drape after 20 frames,
+    5 frames forward + adjoint with collisions active throughout; target = the oracle's drape under
+    the ground-truth shape vector.  Shape / compliance / initial-state gradients within 1e-3
+    relative L2, plus element-wise diagnostics."""
+    from tests.garment_case import contacts, garment_case
+    s = garment_case(64, 48, warm_frames=20, frames=5)
+    grads = ("shape", "compliance", "x0", "v0")
+    g = gpu_run(s, grads)
+    o = oracle_run(s)
+    for x in o["x"]:
+        assert contacts(s, x) >= 20                  # the garment rests on the body
+    assert np.linalg.norm(o["shape"]) > 0
+    _compare(g, o, grads)
+    for k in grads:
+        d = np.abs(np.asarray(g[k], float) - o[k]).max()
+        print(k, "max abs", d, "max |oracle|", np.abs(o[k]).max())
+        assert d <= 1e-2 * np.abs(o[k]).max(), k
 
 
 def test_host_buffers_e2e_matches_device():

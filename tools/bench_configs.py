@@ -22,10 +22,37 @@ CASES = [
 ]
 
 
+def garment_targets(s, t):
+    """configs[3] target: the drape produced by the ground-truth shape vector (BASELINE configs[3]),
+    simulated by the library itself (a performance input only; parity tests build it with the
+    oracle, tests/garment_case.py)."""
+    gt = s.replace(shape_beta=np.asarray(s.meta["shape_beta_gt"], np.float32).astype(np.float64))
+    sc = api.dxpbd_create(**api.scene_kwargs(gt), max_frames=s.frames)
+    api.dxpbd_forward(sc, t(s.x0), t(s.v0), None, s.frames)
+    x = api.dxpbd_positions(sc, s.frames)
+    del sc
+    return x[None]
+
+
+def capsule_contacts(s, x, tol=1e-3):
+    """(vertex, capsule) pairs within tol of the collision thickness, and the mean vertex height."""
+    r = s.cap_r0 + s.cap_rbasis @ s.shape_beta
+    L = s.cap_L0 + s.cap_lbasis @ s.shape_beta
+    n = 0
+    for k in range(len(r)):
+        c, a = s.cap_center[k], s.cap_axis[k]
+        tt = np.clip((x - c) @ a, -L[k] / 2, L[k] / 2)
+        n += int((np.linalg.norm(x - (c + tt[:, None] * a), axis=1) - r[k] < s.thickness + tol).sum())
+    return n
+
+
 def run(name, make, grads):
     s = as_float32_exact(make())
     dev = "cuda:0"
     t = lambda a: None if a is None else torch.as_tensor(np.asarray(a, np.float32), device=dev)  # noqa: E731
+    extra = {}
+    if s.name == "garment":
+        s = s.replace(targets=garment_targets(s, t))
     t0 = time.perf_counter()
     sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=s.frames, grad_flags=api.flags(*grads), cg_max_iter=2000)
     t_create = time.perf_counter() - t0
@@ -42,13 +69,19 @@ def run(name, make, grads):
     ev[2].record()
     torch.cuda.synchronize()
     st = api.dxpbd_stats(sc)
+    if s.name == "garment":
+        xl = api.dxpbd_positions(sc, s.frames).astype(np.float64)
+        extra = dict(mean_height_last_frame=float(xl[:, 1].mean()), min_height_last_frame=float(xl[:, 1].min()),
+                     capsule_contacts_last_frame=capsule_contacts(s, xl),
+                     rms_miss_to_target=float(np.sqrt(2 * loss / s.num_vertices)),
+                     shape_grad=api.dxpbd_grads(sc, "shape").tolist())
     N = s.frames * s.substeps
     fwd, tot = ev[0].elapsed_time(ev[1]), ev[0].elapsed_time(ev[2])
     line = dict(config=name, vertices=s.num_vertices, constraints=len(s.dist_idx), tets=len(s.tet_idx),
                 colliders=len(s.spheres) + len(s.cap_center), frames=s.frames, substeps=s.substeps, grads=list(grads),
                 ms_forward=fwd, ms_forward_adjoint=tot, ms_per_substep_fwd=fwd / N, ms_per_substep_fwd_adjoint=tot / N,
                 cg_iters_per_substep=st["cg_iters_total"] / max(st["solves"], 1), cg_iters_max=st["cg_iters_max"],
-                worst_relres=st["worst_relres"], tma_path=st["tma"], loss=loss, create_s=t_create)
+                worst_relres=st["worst_relres"], tma_path=st["tma"], loss=loss, create_s=t_create, **extra)
     print(json.dumps(line), flush=True)
     del sc
 
