@@ -27,9 +27,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "constraint solves/s & ms/step fwd+adjoint at ~26M DoF cloth; HBM GB/s vs peak"
-# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed `ncu --set full`
-# capture of the dominant kernel at configs[4] size (profiles/ncu/)
-TRAFFIC = {"cg_dist": 1.548254e9 + 0.299441e9}   # profiles/ncu/r01_k_cg_matvec_tma_v16.ncu-rep
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from an
+# `ncu --set full` capture, recorded with a hash of the CUDA sources it was taken on
+# (tools/ncu_traffic.py); reported only when the hash matches the sources being benchmarked
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "traffic.json")
 UNIT = "constraint solves/s"
 
 
@@ -122,15 +123,22 @@ def oracle_sample(ref_n: int, frames: int = 1):
     side = 10.0 * (ref_n - 1) / 2943.0
     s = as_float32_exact(large_cloth(n=ref_n, frames=frames, side=side, key_frames=(frames,)))
     m = OracleModel(s)
-    t0 = time.perf_counter()
-    xs = m.simulate(s.x0, s.v0, s.forces, frames)
-    t1 = time.perf_counter()
-    m.backward(xs, s.v0, s.forces)
-    t2 = time.perf_counter()
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):   # one host thread (the line's "cores": 1)
+        t0 = time.perf_counter()
+        xs = m.simulate(s.x0, s.v0, s.forces, frames)
+        t1 = time.perf_counter()
+        m.backward(xs, s.v0, s.forces)
+        t2 = time.perf_counter()
     solves = len(s.dist_idx) * s.iterations * s.substeps * frames
     return dict(solves=solves, t_fwd=t1 - t0, t_total=t2 - t0, E=len(s.dist_idx), V=s.num_vertices,
                 sample=f"{ref_n}x{ref_n} crop of configs[4], {frames} frame x {s.substeps} substeps, fwd+adjoint, "
                        f"fp64 oracle (numpy + scipy spsolve)")
+
+
+def _grid_constraints(n):
+    """Distance constraints of an n x n cloth grid (structural 2n(n-1), shear 2(n-1)^2, bending 2n(n-2))."""
+    return 2 * n * (n - 1) + 2 * (n - 1) ** 2 + 2 * n * (n - 2)
 
 
 def run_reference(a):
@@ -149,8 +157,8 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "large_cloth (configs[4]) bounded crop", "crop": f"{a.ref_n}x{a.ref_n}",
-                   "frames": 1, "substeps": 10, "iterations": 1},
+        "config": workload_config(a, a.n * a.n, _grid_constraints(a.n), [k for k in (10, 20, 30) if k <= a.frames]
+                                  or [a.frames], 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": res["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "t_max_s": tmax,
@@ -159,24 +167,69 @@ def run_reference(a):
 
 
 # ----------------------------------------------------------------------------- our arm
-# Algorithmic (compulsory) HBM bytes per launch of the kernel classes:
-# every array element the launch must read or write, counted once.
+# Algorithmic HBM bytes: the bytes the METHOD must move, every element once,
+# independent of this implementation's layout.  Layout overheads (halo re-reads, the cross-tile
+# block copies of the TMA matvec) are reported separately, never as algorithmic bytes.
 def algo_bytes(cls, st, units_per_launch=None):
-    E, V, NF, H = st["E"], st["V"], st["n_foreign"], st["halo_total"]
+    E, V = st["E"], st["V"]
     if cls == "dist_project":   # per constraint: idx 8 + rest 4 + alpha 4 + 2 x (32 B read + 32 B write) fp64 state
         return 144.0 * units_per_launch
-    if cls == "dist_replay":    # projection bytes + Q 16 + layout positions tpos/fpos 8 (+ the b-tile copy 16 per
-        # cross-tile constraint)
-        return (168.0 + 16.0 * NF / max(E, 1)) * units_per_launch
-    if cls == "cg_dist":        # TMA matvec: slot pair 4 + Q 16 per entry of the combined segments (own constraints
-        # and foreign copies), halo id 4 + slot 2 + (w 4, r 12, p_old 12) per halo entry, own w 4 + slot 2 + r 12 +
-        # p_old 12 + p_new 12 + q 12 and the deferred u += alpha p (u r/w 24)
-        return 20.0 * E + 20.0 * NF + 34.0 * H + 78.0 * V
+    if cls == "dist_replay":    # projection bytes + the block Q written (16)
+        return 160.0 * units_per_launch
+    if cls == "cg_dist":        # PCG matvec of q = (M + Sum_j P_j^T Q_j P_j) p fused with the p update and the
+        # deferred u += alpha p: per constraint its block Q (16) + endpoint pair (4, 16-bit tile slots); per vertex
+        # w 4 + slot 2 + r 12 + p_old 12 + p_new 12 + q 12 + u r/w 24 = 78
+        return 20.0 * E + 78.0 * V
     if cls == "cg_update":      # r r/w 24, q 12, w 4 (u is updated in the next matvec)
         return 40.0 * V
     if cls == "predict":        # x_n 32, x_{n-1} 32, f 12, out 32
         return 108.0 * V
     return None
+
+
+def layout_overhead_bytes(cls, st):
+    """Bytes per launch this layout moves beyond the method's: the TMA matvec re-reads halo vertices of
+    neighbouring tiles (id 4 + slot 2 + w 4 + r 12 + p_old 12 = 34 B per halo entry) and streams a copy of
+    each cross-tile constraint in the b-endpoint's tile (20 B)."""
+    if cls == "cg_dist":
+        return 20.0 * st["n_foreign"] + 34.0 * st["halo_total"]
+    return 0.0
+
+
+def unique_step_bytes(st, S, M, E, V, cg_mv, cg_it):
+    """Compulsory HBM bytes of one step (forward + adjoint) counted on UNIQUE data: per forward substep the
+    state x_n, x_{n-1} (64 B/V), forces (12 B/V) and the checkpoint write (32 B/V) once, the constraint data
+    (idx 8 + rest 4 + alpha 4 = 16 B/E) once -- however many color sweeps re-read them; cached substeps also
+    write their blocks (16 B/E); per replayed substep the same reads and the block write (16 B/E); per
+    substep the rhs (one matvec + b, r0, u0, p0 and the extrapolation inputs: 60 B/V), the final u update
+    (36 B/V) and the adjoint accumulation (40 B/V); per PCG iteration one matvec and one update."""
+    mv = algo_bytes("cg_dist", st)
+    fwd = S * (108.0 * V + 16.0 * E) + M * 16.0 * E
+    rep = (S - M) * (76.0 * V + 32.0 * E)
+    pcg = S * (mv + 60.0 * V + 36.0 * V + 40.0 * V) + cg_mv * mv + cg_it * algo_bytes("cg_update", st)
+    return fwd + rep + pcg
+
+
+def src_hash():
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2301_01396_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        h.update(open(os.path.join(d, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def load_traffic(kernel):
+    try:
+        t = json.load(open(TRAFFIC_JSON))
+    except Exception:
+        return None, "no capture (profiles/traffic.json)"
+    e = t.get("kernels", {}).get(kernel)
+    if not e:
+        return None, f"{kernel} not in profiles/traffic.json"
+    if t.get("src_sha") != src_hash():
+        return None, f"capture {t.get('capture')} taken on other sources ({t.get('src_sha')})"
+    return e["dram_bytes_per_launch"], t.get("capture")
 
 
 def run_partitioned(a):
@@ -302,10 +355,9 @@ def run_ours(a):
         step()
     torch.cuda.synchronize()
     par.barrier()
+    # ---- timed region: profiler OFF (kernel-class times come from a separate profiled step below)
     clocks = Clocks(local)
     clocks.start()
-    if not a.no_profile:
-        api.dxpbd_profile(sc, True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     launches, cg_iters, cg_mv = 0, 0, 0
@@ -324,13 +376,26 @@ def run_ours(a):
     clk = clocks.stop()
     t_steps = [ev[i][0].elapsed_time(ev[i][2]) for i in range(a.steps)]
     t_fwds = [ev[i][0].elapsed_time(ev[i][1]) for i in range(a.steps)]
-    ktimes = api.dxpbd_kernel_times(sc) if not a.no_profile else {}
-    api.dxpbd_profile(sc, False)
     total_ms = par.reduce_max(sum(t_steps), device=dev)
     ms_per_step = total_ms / a.steps
     substeps_total = a.frames * a.substeps
     solves_per_step = E * a.iterations * substeps_total
     value = par.job_throughput(solves_per_step, ms_per_step, world)
+
+    # ---- one profiled step (events around every launch, on the stream each kernel runs on)
+    ktimes, prof_ms, prof_mv, prof_it = {}, None, 0, 0
+    if not a.no_profile:
+        api.dxpbd_profile(sc, True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        prof_ms = e0.elapsed_time(e1)
+        ktimes = api.dxpbd_kernel_times(sc)
+        api.dxpbd_profile(sc, False)
+        pst = api.dxpbd_stats(sc)
+        prof_mv, prof_it = int(pst["cg_matvecs"]), int(pst["cg_iters_total"])
 
     # ---- e2e through the public API with pinned host buffers (copies inside the timed region)
     e2e = None
@@ -356,9 +421,11 @@ def run_ours(a):
         e2e = {"value": par.job_throughput(solves_per_step, e2e_ms, world), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
-    # ---- roofline of the dominant kernel class
+    # ---- roofline of the dominant kernel class (from the profiled step)
     peaks = load_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    sst = api.dxpbd_stats(sc)
     roof = None
     if ktimes:
         # the replay runs on a low-priority stream overlapping the PCG, so its
@@ -367,44 +434,38 @@ def run_ours(a):
         crit = {k: v for k, v in ktimes.items() if not k.endswith("_replay") and k != "predict"}
         dom = max(crit or ktimes, key=lambda k: (crit or ktimes)[k][0])
         ms, cnt = ktimes[dom]
-        sst = api.dxpbd_stats(sc)
-        # color launches: constraints of one launch on average
-        per_launch_units = E * a.iterations * substeps_total / max(cnt / a.steps, 1)
+        per_launch_units = E * a.iterations * substeps_total / max(cnt, 1)
         b = algo_bytes(dom, sst, per_launch_units)
-        # PCG kernels: the host polls convergence every 8 iterations, so launches after convergence
-        # exit at once; only working launches (= PCG iterations) count, their time stays in ms
-        # (conservative)
-        work = {"cg_dist": cg_mv, "cg_update": cg_iters}.get(dom, 0) or cnt
+        # PCG kernels: launches after convergence (before the host's poll sees it) exit at once; only
+        # working launches (= matvecs / iterations) count, their time stays in ms (conservative)
+        work = {"cg_dist": prof_mv, "cg_update": prof_it}.get(dom, 0) or cnt
         avg_ms = ms / work
         ach = (b / (avg_ms / 1e3)) / 1e9 if b else None
         share = ms / sum(v[0] for v in crit.values()) if crit else ms / sum(v[0] for v in ktimes.values())
+        traffic, traffic_src = load_traffic(dom)
+        ovh = layout_overhead_bytes(dom, sst)
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": TRAFFIC.get(dom), "kernel": dom,
-                "algorithmic_bytes_per_launch": b,
+                "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": dom, "algorithmic_bytes_per_launch": b,
+                "algorithmic_bytes": "20 E + 78 V (DESIGN.md Kernels)" if dom == "cg_dist" else "DESIGN.md Kernels",
+                "layout_overhead_bytes_per_launch": ovh,
+                "frac_incl_layout_overhead": ((b + ovh) / (avg_ms / 1e3) / 1e9 / peak) if b else None,
                 "avg_launch_ms": avg_ms, "launches": cnt, "working_launches": work, "share_of_kernel_time": share,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+                "timing": "CUDA events around every launch of one separate profiled step (headline unprofiled)",
+                "profiled_step_ms": prof_ms, "peak_source": peak_src}
 
-    # ---- whole-step roofline: compulsory bytes of every kernel class of one step (forward + adjoint)
-    # over the step time; rhs ~ one matvec + 36 B/vertex, adjoint ~ 40 B/vertex
+    # ---- whole-step roofline on unique bytes (each state / constraint element once per sweep)
     step_roof = None
-    sst = api.dxpbd_stats(sc)
     if sst["tma"]:
-        S = substeps_total
-        mv = algo_bytes("cg_dist", sst)
-        # forward: predict + projection per substep, plus the block writes (Q + copy + layout indices) of the
-        # substeps cached for the backward; backward: predict + replay per substep not cached, rhs (~ one
-        # matvec + b, r0, u0, p0 and the extrapolation inputs: 60 B/vertex), the final u += alpha p (36 B/vertex),
-        # adjoint accumulation (~40 B/vertex) per substep, and the PCG matvecs / updates
         M = sst.get("cached_substeps", 0)
-        NF = sst["n_foreign"]
-        per_step = (S * (algo_bytes("predict", sst) + algo_bytes("dist_project", sst, E * a.iterations))
-                    + M * (16.0 * (E + NF) + 8.0 * E)
-                    + (S - M) * (algo_bytes("predict", sst) + algo_bytes("dist_replay", sst, E * a.iterations))
-                    + S * (mv + 60.0 * V + 36.0 * V + 40.0 * V)
-                    + (cg_mv / a.steps) * mv + (cg_iters / a.steps) * algo_bytes("cg_update", sst))
+        per_step = unique_step_bytes(sst, substeps_total, M, E, V, cg_mv / a.steps, cg_iters / a.steps)
         ach = per_step / (ms_per_step / 1e3) / 1e9
         step_roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "algorithmic_bytes_per_step": per_step, "substeps_with_cached_blocks": M}
+                     "algorithmic_bytes_per_step": per_step, "substeps_with_cached_blocks": M,
+                     "counting": "unique bytes: state and constraint data once per substep (not per color)"}
+        fwd_ms = (sum(t_fwds) / a.steps)
+        fwd_bytes = substeps_total * (108.0 * V + 16.0 * E) + M * 16.0 * E
+        step_roof["forward_frac"] = fwd_bytes / (fwd_ms / 1e3) / 1e9 / peak
 
     # ---- CPU baseline (oracle on a bounded crop, rank 0 at N = 1 only)
     cpu = None
@@ -419,23 +480,29 @@ def run_ours(a):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "precision": "fp32 arithmetic, fp64 position state (DESIGN.md Precision)",
             "data": "synthetic",
-            "config": {"workload": f"large_cloth {a.n}x{a.n} (BASELINE configs[4])" if a.n == 2944 else
-                       f"large_cloth {a.n}x{a.n} (reduced)", "vertices": V, "dof": 3 * V, "constraints": E,
-                       "frames": a.frames, "substeps": a.substeps, "iterations": a.iterations,
-                       "keyframes": kf.tolist(), "grads": "per-frame per-vertex forces",
-                       "cg_tol": a.cg_tol, "l2": "inputs larger than L2 (positions 277 MB fp64 state per GPU)",
-                       "parallelism": f"independent scene per GPU x{world}"},
+            "config": workload_config(a, V, E, kf, world),
             "ms_per_substep_fwd": (sum(t_fwds) / a.steps) / substeps_total,
             "ms_per_substep_fwd_adjoint": ms_per_step / substeps_total,
             "cg_iters_per_substep": cg_iters / max(1, a.steps * substeps_total),
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "create_s": t_create, "loss": loss,
-            "kernel_ms_per_step": {k: v[0] / a.steps for k, v in ktimes.items()},
-            "kernel_ms_note": "event-timed per class; the replay classes (dist_replay and the replay's predict) run "
-                              "on a low-priority stream concurrently with the PCG, so their times include waiting",
+            "kernel_ms_profiled_step": {k: v[0] for k, v in ktimes.items()},
+            "kernel_ms_note": "one profiled step after the timed region; the replay classes (dist_replay and the "
+                              "replay's predict) run on a low-priority stream concurrently with the PCG, so their "
+                              "times include waiting",
+            "src_sha": src_hash(),
         }
         print(json.dumps(line), flush=True)
     par.shutdown()
+
+
+def workload_config(a, V, E, kf, world):
+    return {"workload": f"large_cloth {a.n}x{a.n} (BASELINE configs[4])" if a.n == 2944 else
+            f"large_cloth {a.n}x{a.n} (reduced)", "vertices": V, "dof": 3 * V, "constraints": E,
+            "frames": a.frames, "substeps": a.substeps, "iterations": a.iterations,
+            "keyframes": [int(k) for k in kf], "grads": "per-frame per-vertex forces",
+            "cg_tol": a.cg_tol, "l2": "inputs larger than L2 (positions 277 MB fp64 state per GPU)",
+            "parallelism": f"independent scene per GPU x{world}"}
 
 
 def main():
