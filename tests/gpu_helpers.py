@@ -38,11 +38,11 @@ def gpu_run(scene, grads=(), frames=None, pd=1, cg_tol=1e-6, cg_max_iter=1000, d
     return out
 
 
-def oracle_run(scene, frames=None, pd=True, backward=True):
+def oracle_run(scene, frames=None, pd=True, backward=True, solver="direct"):
     from oracle import OracleModel
     s = scene
     frames = s.frames if frames is None else frames
-    m = OracleModel(s, pd_projection=pd)
+    m = OracleModel(s, pd_projection=pd, solver=solver)
     xs = m.simulate(s.x0, s.v0, s.forces, frames)
     out = dict(model=m, x=[xs[f * s.substeps] for f in range(frames + 1)])
     if backward:

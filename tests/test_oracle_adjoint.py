@@ -331,6 +331,31 @@ def test_filtered_solve():
     np.testing.assert_allclose(m.solve(Z, r)[m.free], (m.w[:, None] * r)[m.free], rtol=1e-13)
 
 
+def test_cg_solver_matches_direct():
+    """solver="cg" (l.201 "PCG ... preferred") reaches the direct solve's solution: the same filtered
+    system residual bound and the same gradients, on cloth with forces and keyframes."""
+    from synth import large_cloth
+    s = large_cloth(n=12, frames=2, substeps=3, side=0.05, key_frames=(1, 2))
+    ga = []
+    for solver in ("direct", "cg"):
+        m = OracleModel(s, solver=solver)
+        xs = m.simulate(s.x0, s.v0, s.forces, 2)
+        phi, g = m.backward(xs, s.v0, s.forces, key_frames=np.array([1, 2]), targets=s.targets)
+        ga.append(g)
+        if solver == "cg":
+            _, _, rec = m.step(xs[0], s.v0, s.forces[0], record=True)
+            Q = m.blocks(rec)
+            r = rng.normal(size=(m.V, 3))
+            y = m.solve(Q, r)
+            assert np.all(y[~m.free] == 0.0)
+            A = m.system_matrix(Q)
+            fdof = np.repeat(m.free, 3)
+            res = A[fdof][:, fdof] @ y.ravel()[fdof] - r.ravel()[fdof]
+            assert np.linalg.norm(res) <= 1e-12 * np.linalg.norm(r.ravel()[fdof])
+    for k in ("forces", "x0", "v0", "compliance"):
+        np.testing.assert_allclose(ga[1][k], ga[0][k], rtol=0, atol=1e-10 * np.abs(ga[0][k]).max())
+
+
 def test_projected_system_is_spd():
     s = tiny_cloth(n=6, frames=1, substeps=1)
     m = OracleModel(s)
