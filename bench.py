@@ -486,6 +486,7 @@ def run_ours(a):
             "cg_iters_per_substep": cg_iters / max(1, a.steps * substeps_total),
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "create_s": t_create, "loss": loss,
+            "wave": {k: sst.get(k) for k in ("wave_tiles", "wave_items", "wave_lag", "wave_max_neighbours")},
             "kernel_ms_profiled_step": {k: v[0] for k, v in ktimes.items()},
             "kernel_ms_note": "one profiled step after the timed region; the replay classes (dist_replay and the "
                               "replay's predict) run on a low-priority stream concurrently with the PCG, so their "

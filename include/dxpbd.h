@@ -144,14 +144,16 @@ int dxpbd_set_params(dxpbd_scene *scene, int32_t kind, const float *data, int64_
 int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out_len,
                    int32_t *num_colors);
 
-/* Statistics into HOST out[0..n), n <= 16:
+/* Statistics into HOST out[0..n), n <= 20:
  *  0: total PCG iterations of the last backward, 1: max PCG iterations of one solve,
  *  2: kernel launches of the last forward, 3: of the last backward, 4: substeps solved,
  *  5: worst final relative residual, 6: last loss, 7: foreign constraint entries (tiled PCG),
  *  8: halo slots summed over tiles, 9: E, 10: V, 11: T, 12: vertex tiles, 13: TMA path on,
  *  14: PCG matvec launches of the last backward that did work (iterations, plus one start
  *      matvec per solve for the single-reduction PCG), 15: substeps of the last backward whose
- *      derivative blocks came from the forward's cache (no replay). */
+ *      derivative blocks came from the forward's cache (no replay),
+ *  16: wave tiles of the wavefront sweep (0: per-color launches), 17: its work items per substep,
+ *  18: its ticket lag L (bandwidth of the wave-tile order + 1), 19: most neighbours of a wave tile. */
 int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
 
 /* ---- Vertex-partitioned domain decomposition -------------------------

@@ -21,6 +21,7 @@
 #include "../../include/dxpbd.h"
 #include "kernels.cuh"
 #include "tet_kernels.cuh"
+#include "wave.cuh"
 
 using namespace dx;
 
@@ -305,12 +306,18 @@ static inline uint64_t spread3(uint64_t x) {
     x = (x | x << 2) & 0x1249249249249249ull;
     return x;
 }
-void morton_order(const float *x, int V, std::vector<int32_t> &perm) {
+// The quantization cell is the mesh's short edge length h (10th percentile of a sample of rest
+// lengths), so a regular grid maps onto the integer lattice and every run of 2^k consecutive Morton
+// codes is an aligned lattice block: tiles are compact rectangles / boxes (32 x 16 at kTileV = 512 on
+// a cloth grid), which minimises tile halos and cross-tile constraints.  A cell of extent / 2^21
+// (the key's resolution) when h is unknown or smaller.
+void morton_order(const float *x, int V, double h, std::vector<int32_t> &perm) {
     float lo[3] = {x[0], x[1], x[2]}, hi[3] = {x[0], x[1], x[2]};
     for (int i = 0; i < V; ++i)
         for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], x[3 * i + k]); hi[k] = std::max(hi[k], x[3 * i + k]); }
     float ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
-    double sc = ext > 0 ? 2097151.0 / ext : 0.0;
+    const double cell = std::max(h, (double)ext / 2097151.0);
+    double sc = cell > 0 ? 1.0 / cell : 0.0;
     std::vector<std::pair<uint64_t, int32_t>> key(V);
     for (int i = 0; i < V; ++i) {
         uint64_t q[3];
@@ -522,6 +529,20 @@ struct dxpbd_scene {
     size_t qc_cper = 0;       // floats per cached substep in qccache
     int qc_first = 0, qc_count = 0;
     bool qcache_on = true;
+    // wavefront sweep (wave.cuh): predict + all distance colors of a K = 1 substep in one launch
+    bool wave_on = false;            // opt-in (DXPBD_WAVE=1): measured slower than the per-color launches
+    bool wave_fwd = true, wave_rep = true;   // per pass (DXPBD_WAVE_FWD / DXPBD_WAVE_REP)
+    int wave_g = 4;                  // base tiles per wave tile (DXPBD_WAVE_G)
+    int wave_grid_fwd = 0;           // forward grid (0: persistent, resident CTAs of every SM; < 0: one item per CTA)
+    int wave_grid_rep = -1;          // replay grid (one item per CTA: shares the GPU with the PCG)
+    int wave_lag = -1;               // extra ticket lag (DXPBD_WAVE_LAG; < 0: resident CTAs of the GPU)
+    int wave_ntw = 0, wave_nitems = 0, wave_L = 0, wave_maxnbr = 0;
+    DBuf<int4> wave_items;           // per ticket {wave tile, phase, first constraint, count}
+    DBuf<int2> wave_nrange;          // per ticket: neighbour range in wave_nbr
+    DBuf<int> wave_nbr;
+    DBuf<unsigned> wave_flags;       // [2][ntw]: forward, replay
+    DBuf<int> wave_ctr;              // [2] ticket counters
+    unsigned wave_base[2] = {0u, 0u};
     // colliders
     DBuf<float> sph, cap_c, cap_a, cap_r0, cap_L0, cap_Rb, cap_Lb, beta;
     DBuf<Collider> cols;
@@ -571,7 +592,7 @@ struct dxpbd_scene {
     bool have_grads = false;
 
     // stats
-    double stats[16] = {0};
+    double stats[20] = {0};
     // opt-in event profiler
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -626,20 +647,204 @@ void apply_shape(dxpbd_scene *s, cudaStream_t st) {
 
 inline double4 *state(dxpbd_scene *s, int n) { return s->ckpt.p + (size_t)n * s->V; }
 
+// ------------------------------------------------------------------ wavefront plan (create time)
+// Wave tile w = base tiles [w g, w g + g).  Neighbours: two wave tiles are neighbours when their
+// items touch a common vertex (a tile's items touch its own vertices -- prediction -- and both
+// endpoints of the constraints it owns).  Order pi: Cuthill-McKee BFS of the neighbour graph
+// (restarted per component), L = 1 + max |pi(w) - pi(w')| over neighbours; tickets in the order of
+// key = pi(w) + L p (wave.cuh: every dependency holds a smaller ticket).
+void build_wave_plan(dxpbd_scene *s, const std::vector<int> &seg, const std::vector<int2> &ab, const float *xrest,
+                     cudaStream_t st) {
+    const int V = s->V, nt = s->ntiles, nc = s->n_dist_colors, g = std::max(1, s->wave_g);
+    const int W = g * kTileV, ntw = (nt + g - 1) / g;
+    constexpr int KIN = 6;
+    std::vector<uint32_t> own((size_t)KIN * V);
+    std::vector<uint8_t> cnt(V, 0);
+    bool overflow = false;
+    auto add = [&](int v, uint32_t w) {
+        uint32_t *o = own.data() + (size_t)KIN * v;
+        for (int k = 0; k < cnt[v]; ++k)
+            if (o[k] == w) return;
+        if (cnt[v] == KIN) { overflow = true; return; }
+        o[cnt[v]++] = w;
+    };
+    for (int v = 0; v < V; ++v) add(v, (uint32_t)(v / W));
+    for (size_t q = 0; q < ab.size(); ++q) {
+        const uint32_t w = (uint32_t)(ab[q].x / W);
+        add(ab[q].x, w);
+        add(ab[q].y, w);
+    }
+    if (overflow) { s->wave_on = false; return; }   // very irregular meshes: per-color launches
+    std::vector<std::vector<int>> nb(ntw);
+    for (int w = 0; w < ntw; ++w) nb[w].push_back(w);
+    for (int v = 0; v < V; ++v) {
+        const uint32_t *o = own.data() + (size_t)KIN * v;
+        for (int a = 0; a < cnt[v]; ++a)
+            for (int b = 0; b < cnt[v]; ++b)
+                if (a != b) nb[o[a]].push_back((int)o[b]);
+    }
+    std::vector<uint32_t>().swap(own);
+    int maxn = 0;
+    for (auto &l : nb) {
+        std::sort(l.begin(), l.end());
+        l.erase(std::unique(l.begin(), l.end()), l.end());
+        maxn = std::max(maxn, (int)l.size());
+    }
+    // Two orders of the wave tiles, the one with the smaller bandwidth b is kept: (1) by centroid along
+    // the longest bounding-box axis of the rest shape, in rows across the second-longest (sheets and
+    // blocks), (2) Cuthill-McKee BFS.  The band of tiles live between a tile's first and last phase is
+    // ~P b tiles, so b sets the L2 working set.
+    auto bandwidth = [&](const std::vector<int> &pi) {
+        int b = 0;
+        for (int w = 0; w < ntw; ++w)
+            for (int v : nb[w]) b = std::max(b, std::abs(pi[w] - pi[v]));
+        return b;
+    };
+    std::vector<int> order_geo(ntw);
+    {
+        std::vector<double> cen((size_t)3 * ntw, 0.0);
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        for (int v = 0; v < V; ++v) {
+            const float *xr = xrest + (size_t)3 * s->vperm_h[v];
+            for (int k = 0; k < 3; ++k) {
+                cen[(size_t)3 * (v / W) + k] += xr[k];
+                lo[k] = std::min(lo[k], (double)xr[k]);
+                hi[k] = std::max(hi[k], (double)xr[k]);
+            }
+        }
+        int ax[3] = {0, 1, 2};
+        std::sort(ax, ax + 3, [&](int a, int b) { return hi[a] - lo[a] > hi[b] - lo[b]; });
+        const double ext1 = std::max(hi[ax[1]] - lo[ax[1]], 1e-30), ext0 = std::max(hi[ax[0]] - lo[ax[0]], 1e-30);
+        const double cell = std::sqrt(ext0 * ext1 / std::max(1, ntw));   // about one wave tile's extent
+        std::vector<std::pair<long long, double>> key(ntw);
+        for (int w = 0; w < ntw; ++w) {
+            const int nv = std::min(V, (w + 1) * W) - w * W;
+            const double c0 = cen[(size_t)3 * w + ax[0]] / nv, c1 = cen[(size_t)3 * w + ax[1]] / nv;
+            key[w] = {(long long)std::floor((c1 - lo[ax[1]]) / cell), c0};
+        }
+        for (int w = 0; w < ntw; ++w) order_geo[w] = w;
+        std::sort(order_geo.begin(), order_geo.end(), [&](int a, int b) { return key[a] < key[b] || (key[a] == key[b] && a < b); });
+    }
+    std::vector<int> order;
+    order.reserve(ntw);
+    std::vector<char> seen(ntw, 0);
+    for (int r = 0; r < ntw; ++r) {
+        if (seen[r]) continue;
+        size_t head = order.size();
+        order.push_back(r);
+        seen[r] = 1;
+        while (head < order.size()) {
+            const int u = order[head++];
+            std::vector<int> nx;
+            for (int v : nb[u])
+                if (!seen[v]) { seen[v] = 1; nx.push_back(v); }
+            std::sort(nx.begin(), nx.end(), [&](int x, int y) { return nb[x].size() < nb[y].size() || (nb[x].size() == nb[y].size() && x < y); });
+            order.insert(order.end(), nx.begin(), nx.end());
+        }
+    }
+    std::vector<int> pi(ntw), pig(ntw);
+    for (int k = 0; k < ntw; ++k) pi[order[k]] = k;
+    for (int k = 0; k < ntw; ++k) pig[order_geo[k]] = k;
+    int bw = bandwidth(pi);
+    const int bwg = bandwidth(pig);
+    if (bwg <= bw) { order.swap(order_geo); pi.swap(pig); bw = bwg; }
+    const int P = 1 + nc;
+    int L = 1 + bw;
+    {   // + the in-flight window in keys (resident CTAs / items per key), so that a dependency is
+        // normally finished when its dependant is dispatched
+        int occ = 0, nsm = 0;
+        DX_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_wave<2, 2, false, true>, kBlock, 0));
+        DX_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device));
+        L += s->wave_lag >= 0 ? s->wave_lag : (occ * nsm + P - 1) / P;
+    }
+    std::vector<int> off(ntw + 1, 0), flat;
+    for (int w = 0; w < ntw; ++w) off[w + 1] = off[w] + (int)nb[w].size();
+    flat.reserve(off[ntw]);
+    for (auto &l : nb) flat.insert(flat.end(), l.begin(), l.end());
+    std::vector<int4> items;
+    std::vector<int2> nrange;
+    items.reserve((size_t)ntw * P);
+    nrange.reserve((size_t)ntw * P);
+    for (int64_t key = 0; key < (int64_t)ntw + (int64_t)L * (P - 1); ++key)
+        for (int p = P - 1; p >= 0; --p) {
+            const int64_t k = key - (int64_t)L * p;
+            if (k < 0 || k >= ntw) continue;
+            const int w = order[k];
+            int b = 0, c = 0;
+            if (p > 0) {
+                const int *sg = seg.data() + (size_t)(p - 1) * (nt + 1);
+                b = sg[w * g];
+                c = sg[std::min(nt, w * g + g)] - b;
+            }
+            items.push_back(make_int4(w, p, b, c));
+            nrange.push_back(make_int2(off[w], off[w + 1]));
+        }
+    s->wave_ntw = ntw;
+    s->wave_nitems = (int)items.size();
+    s->wave_L = L;
+    s->wave_maxnbr = maxn;
+    s->wave_items.alloc(items.size());
+    upload(s->wave_items.p, items.data(), sizeof(int4) * items.size(), DXPBD_MEM_HOST, st);
+    s->wave_nrange.alloc(nrange.size());
+    upload(s->wave_nrange.p, nrange.data(), sizeof(int2) * nrange.size(), DXPBD_MEM_HOST, st);
+    s->wave_nbr.alloc(flat.size());
+    upload(s->wave_nbr.p, flat.data(), sizeof(int) * flat.size(), DXPBD_MEM_HOST, st);
+    s->wave_flags.alloc((size_t)2 * ntw);
+    DX_CHECK_CUDA(cudaMemsetAsync(s->wave_flags.p, 0, sizeof(unsigned) * 2 * ntw, st));
+    s->wave_ctr.alloc(2);
+    DX_CHECK_CUDA(cudaMemsetAsync(s->wave_ctr.p, 0, sizeof(int) * 2, st));
+    DX_CHECK_CUDA(cudaStreamSynchronize(st));
+}
+
+// One wavefront launch over the substep (k = 0: forward, 1: replay); REPLAY also stores the blocks.
+template <bool REPLAY, bool WRITE_LAST_X>
+void launch_wave(dxpbd_scene *s, int k, int grid, const WavePredict &pr, const WaveDist &dd, double4 *x, cudaStream_t st) {
+    WavePlan w{s->wave_ntw, s->wave_g * kTileV, s->wave_nitems, s->wave_items.p, s->wave_nrange.p, s->wave_nbr.p,
+               s->wave_flags.p + (size_t)k * s->wave_ntw, s->wave_ctr.p + k};
+    DX_CHECK_CUDA(cudaMemsetAsync(s->wave_ctr.p + k, 0, sizeof(int), st));
+    auto kern = k_wave<2, 2, REPLAY, WRITE_LAST_X>;
+    if (grid < 0) grid = s->wave_nitems;
+    if (grid == 0) {
+        int occ = 0, nsm = 0;
+        DX_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0));
+        DX_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device));
+        grid = std::max(1, occ * nsm);
+    }
+    kern<<<std::min(grid, s->wave_nitems), kBlock, 0, st>>>(w, s->wave_base[k], s->V, s->n_dist_colors, pr, dd, x);
+    DX_CHECK_CUDA(cudaGetLastError());
+    s->wave_base[k] += (unsigned)(1 + s->n_dist_colors);
+}
+
 // ------------------------------------------------------------------ one forward substep
 int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int V = s->V;
     const int frame = n / s->substeps;
     double4 *xo = state(s, n + 1);
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
-    LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
-                                                                   s->dtd, 1.0 / s->dtd, s->gravity, xo));
-    int launches = 1;
     const float inv_dt2 = s->inv_dt * s->inv_dt;
     const int K = s->iterations;
+    int launches = 1;
+    bool wave = s->wave_on && s->wave_fwd && s->wave_nitems > 0 && K == 1;
+    const bool cached = s->qc_count && n >= s->qc_first;
+    if (wave) {
+        // predict + every distance color in one time-skewed launch (wave.cuh); on cached substeps the
+        // replay variant also stores Q_n (same iterates bit for bit)
+        WavePredict pr{state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f, s->dtd, 1.0 / s->dtd, s->gravity};
+        if (cached) {
+            float4 *slot = s->qcache.p + (size_t)(n - s->qc_first) * s->d_Qt.n;
+            WaveDist dd{s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->E, slot, slot, nullptr, s->d_tpos.p, s->d_fpos.p};
+            LAUNCH(DXPBD_K_DIST_PROJECT, (launch_wave<true, true>(s, 0, s->wave_grid_fwd, pr, dd, xo, st)));
+        } else {
+            WaveDist dd{s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->E, nullptr, nullptr, nullptr, nullptr, nullptr};
+            LAUNCH(DXPBD_K_DIST_PROJECT, (launch_wave<false, true>(s, 0, s->wave_grid_fwd, pr, dd, xo, st)));
+        }
+    } else {
+        LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
+                                                                       s->dtd, 1.0 / s->dtd, s->gravity, xo));
+    }
     for (int k = 0; k < K; ++k) {
         const bool rd = k > 0, wr = k < K - 1;
-        for (int c = 0; c < s->n_dist_colors; ++c) {
+        for (int c = 0; c < (wave ? 0 : s->n_dist_colors); ++c) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
             if (!rd && !wr && s->qc_count && n >= s->qc_first) {
@@ -699,18 +904,30 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int frame = n / s->substeps;
     const float *f = s->have_forces ? s->forces.p + (size_t)frame * V * 3 : nullptr;
     double4 *x = s->xr.p;
-    LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
-                                                                   s->dtd, 1.0 / s->dtd, s->gravity, x));
     int launches = 1;
     const float inv_dt2 = s->inv_dt * s->inv_dt;
     const int K = s->iterations;
     const bool want_e = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
+    const bool wave = s->wave_on && s->wave_rep && s->wave_nitems > 0 && K == 1 && s->qf == 1;
+    if (wave) {
+        WavePredict pr{state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f, s->dtd, 1.0 / s->dtd, s->gravity};
+        float4 *Q = s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p);
+        WaveDist dd{s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, E, Q, qtw, want_e ? s->ed.p : nullptr,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr};
+        if (!s->T && !s->NC)
+            LAUNCH(DXPBD_K_DIST_REPLAY, (launch_wave<true, false>(s, 1, s->wave_grid_rep, pr, dd, x, st)));
+        else
+            LAUNCH(DXPBD_K_DIST_REPLAY, (launch_wave<true, true>(s, 1, s->wave_grid_rep, pr, dd, x, st)));
+    } else {
+        LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
+                                                                       s->dtd, 1.0 / s->dtd, s->gravity, x));
+    }
     DistScratch ds{s->sc_lam.p, s->sc_sig.p, s->sc_B.p, s->sc_T.p, s->sc_e.p};
     ContactScratch cs{s->cc_lam.p, s->cc_T.p, s->cc_sig.p, s->cc_B.p, s->cc_e.p};
     const bool want_ce = (s->grad_flags & ((1u << DXPBD_GRAD_SHAPE) | (1u << DXPBD_GRAD_SPHERE))) != 0;
     for (int k = 0; k < K; ++k) {
         const bool first = k == 0, last = k == K - 1;
-        for (int c = 0; c < s->n_dist_colors; ++c) {
+        for (int c = 0; c < (wave ? 0 : s->n_dist_colors); ++c) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
             float *eo = want_e ? s->ed.p : nullptr;
@@ -1121,11 +1338,38 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_OVERLAP")) s->overlap = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_QCACHE")) s->qcache_on = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_POLL_EXTRA")) s->poll_extra = atoi(ev);
+    if (const char *ev = getenv("DXPBD_WAVE")) s->wave_on = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_WAVE_G")) s->wave_g = std::max(1, atoi(ev));
+    if (const char *ev = getenv("DXPBD_WAVE_FWD")) s->wave_fwd = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_WAVE_REP")) s->wave_rep = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_WAVE_LAG")) s->wave_lag = atoi(ev);
+
+    if (const char *ev = getenv("DXPBD_WAVE_GRID_FWD")) s->wave_grid_fwd = atoi(ev);
+    if (const char *ev = getenv("DXPBD_WAVE_GRID_REP")) s->wave_grid_rep = atoi(ev);
 
     cudaStream_t st = 0;
 
     // vertex order: Morton order of the rest positions (host, create time)
-    morton_order(d->x_rest, V, s->vperm_h);
+    {   // short edge length: 10th percentile over a sample of distance-constraint (else tet) edges (on a
+        // cloth grid the structural spacing, not the shear / bending lengths)
+        std::vector<double> len;
+        auto edge = [&](int a, int b) {
+            double q = 0;
+            for (int k = 0; k < 3; ++k) { const double u = (double)d->x_rest[3 * a + k] - d->x_rest[3 * b + k]; q += u * u; }
+            if (q > 0) len.push_back(std::sqrt(q));
+        };
+        const int64_t ne = d->num_dist, nte = d->num_tets;
+        for (int64_t j = 0; j < ne; j += std::max<int64_t>(1, ne / 65536)) edge(d->dist_idx[2 * j], d->dist_idx[2 * j + 1]);
+        if (len.empty())
+            for (int64_t j = 0; j < nte; j += std::max<int64_t>(1, nte / 65536)) edge(d->tet_idx[4 * j], d->tet_idx[4 * j + 1]);
+        double h = 0;
+        if (!len.empty()) {
+            std::nth_element(len.begin(), len.begin() + len.size() / 10, len.end());
+            h = len[len.size() / 10];
+        }
+        if (const char *ev = getenv("DXPBD_MORTON_CELL")) h = atof(ev);   // 0: the extent / 2^21 cell (A/B)
+        morton_order(d->x_rest, V, h, s->vperm_h);
+    }
     std::vector<int32_t> vinv(V);
     for (int i = 0; i < V; ++i) vinv[s->vperm_h[i]] = i;
     s->vperm.alloc(V);
@@ -1195,6 +1439,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         for (int q = 0; q < E; ++q) ab_sorted[q] = ab[s->dist_perm_h[q]];
         s->d_seg.alloc(seg.size());
         upload(s->d_seg.p, seg.data(), sizeof(int) * seg.size(), DXPBD_MEM_HOST, st);
+        if (s->wave_on && s->iterations == 1 && !g_keep_host) build_wave_plan(s, seg, ab_sorted, d->x_rest, st);
         // foreign lists: constraints whose b lies in another tile than a, keyed (color, tile(b))
         {
             std::vector<int64_t> fc(nkeys + 1, 0);
@@ -1839,7 +2084,12 @@ int dxpbd_stats(dxpbd_scene *s, double *out, int32_t n) {
     s->stats[11] = (double)s->T;
     s->stats[12] = (double)s->ntiles;
     s->stats[13] = s->use_tma ? 1.0 : 0.0;
-    for (int k = 0; k < n && k < 16; ++k) out[k] = s->stats[k];
+    const bool wave = s->wave_on && s->wave_nitems > 0;
+    s->stats[16] = wave ? s->wave_ntw : 0;
+    s->stats[17] = wave ? s->wave_nitems : 0;
+    s->stats[18] = wave ? s->wave_L : 0;
+    s->stats[19] = wave ? s->wave_maxnbr : 0;
+    for (int k = 0; k < n && k < 20; ++k) out[k] = s->stats[k];
     DX_API_END
 }
 

@@ -24,11 +24,9 @@ struct Collider {
 // x~ = x_n + dt v_n + dt^2 (g + w f)  for free vertices, x~ = x_n for pinned ones
 // (Eq. xpbdUpdateRule l.91, R2).  v_n = (x_n - x_{n-1}) / dt exactly as the forward
 // defines it (R9), or v0 at n = 0.  Writes x~ (w = inverse mass) into out.
-__global__ void k_predict(int V, const double4 *__restrict__ xn, const double4 *__restrict__ xprev,
-                          const float4 *__restrict__ v0, const float *__restrict__ f, double dt,
-                          double inv_dt, float3 g, double4 *__restrict__ out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= V) return;
+DX_INLINE double4 predict_one(int i, const double4 *__restrict__ xn, const double4 *__restrict__ xprev,
+                              const float4 *__restrict__ v0, const float *__restrict__ f, double dt, double inv_dt,
+                              float3 g) {
     double4 x = xn[i];
     double3 v;
     if (xprev) {
@@ -49,7 +47,14 @@ __global__ void k_predict(int V, const double4 *__restrict__ xn, const double4 *
         o.y = __fma_rn(dt2, acc.y, __fma_rn(dt, v.y, x.y));
         o.z = __fma_rn(dt2, acc.z, __fma_rn(dt, v.z, x.z));
     }
-    out[i] = o;
+    return o;
+}
+__global__ void k_predict(int V, const double4 *__restrict__ xn, const double4 *__restrict__ xprev,
+                          const float4 *__restrict__ v0, const float *__restrict__ f, double dt,
+                          double inv_dt, float3 g, double4 *__restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= V) return;
+    out[i] = predict_one(i, xn, xprev, v0, f, dt, inv_dt, g);
 }
 
 // ============================================================================ distance

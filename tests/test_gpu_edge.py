@@ -210,3 +210,50 @@ def test_garment_block_cache_and_overlap_match_serial(monkeypatch, switch):
     for k in ("x0", "v0"):
         np.testing.assert_array_equal(ga[k], gb[k])
     np.testing.assert_allclose(ga["shape"], gb["shape"], rtol=1e-12, atol=1e-30)
+
+
+def _run_all(s, grads, frames):
+    api = _api()
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=frames, grad_flags=api.flags(*grads))
+    api.dxpbd_forward(sc, s.x0, s.v0, None if s.forces is None else s.forces[:frames], frames)
+    xs = [api.dxpbd_positions(sc, f) for f in range(frames + 1)]
+    kf = [k for k in np.asarray(s.key_frames).tolist() if k <= frames]
+    loss = api.dxpbd_backward(sc, kf, s.targets[: len(kf)])
+    return xs, loss, {k: api.dxpbd_grads(sc, k) for k in grads}, api.dxpbd_stats(sc)
+
+
+def _wave_cases():
+    from tests.garment_case import garment_case
+    return [
+        ("large96", lambda: f32(large_cloth(n=96, frames=2, substeps=3, side=10.0 * 95 / 2943.0, key_frames=(2,))
+                                .replace(frame_dt=3 / 600)), ("forces", "x0", "v0")),
+        ("tiny", lambda: f32(tiny_cloth(frames=3)), ("compliance", "v0", "x0")),
+        ("sphere", lambda: f32(medium_cloth(n=48, frames=3)), ("compliance", "x0", "v0")),
+        ("garment", lambda: garment_case(64, 48, warm_frames=10, frames=2), ("x0", "v0")),
+    ]
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_wave_sweep_bit_identical(monkeypatch, case):
+    """The wavefront sweep (prediction + every distance color of a substep in one launch, wave.cuh)
+    reproduces the per-color launches bit for bit: positions of every frame, the loss and every
+    gradient (its replay variant writes the same blocks), for several wave-tile sizes and for a
+    persistent and a one-item-per-CTA grid."""
+    name, mk, grads = _wave_cases()[case]
+    s = mk()
+    frames = s.frames
+    monkeypatch.setenv("DXPBD_WAVE", "0")
+    xa, la, ga, sa = _run_all(s, grads, frames)
+    assert sa["wave_tiles"] == 0
+    monkeypatch.setenv("DXPBD_WAVE", "1")
+    for g, gf, gr in ((2, 0, -1), (1, -1, 0), (4, 7, 3)):
+        monkeypatch.setenv("DXPBD_WAVE_G", str(g))
+        monkeypatch.setenv("DXPBD_WAVE_GRID_FWD", str(gf))
+        monkeypatch.setenv("DXPBD_WAVE_GRID_REP", str(gr))
+        xb, lb, gb, sb = _run_all(s, grads, frames)
+        assert sb["wave_tiles"] > 0, name
+        for f in range(frames + 1):
+            np.testing.assert_array_equal(xa[f], xb[f], err_msg=f"{name} g={g} frame {f}")
+        assert la == lb, (name, g)
+        for k in grads:
+            np.testing.assert_array_equal(ga[k], gb[k], err_msg=f"{name} g={g} {k}")
