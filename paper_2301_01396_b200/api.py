@@ -19,7 +19,7 @@ except Exception:  # pragma: no cover
     torch = None
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdxpbd.so")
+LIB_PATH = os.environ.get("DXPBD_LIB") or os.path.join(_HERE, "libdxpbd.so")   # DXPBD_LIB: an A/B build
 
 MEM_HOST, MEM_DEVICE = 0, 1
 GRAD_COMPLIANCE, GRAD_X0, GRAD_V0, GRAD_FORCES, GRAD_SHAPE, GRAD_SPHERE, GRAD_MATERIAL = range(7)

@@ -586,6 +586,14 @@ struct dxpbd_scene {
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
     DBuf<float> cc_lam, cc_T, cc_sig, cc_B, cc_e;               // contact scratch (K>1)
     DBuf<double> cg_sc, acc;
+    // PCG as a CUDA graph with a conditional WHILE node (no host polls).  Opt-in (DXPBD_PCG_GRAPH=1):
+    // measured 3-15 % slower than the host-polled loop with its iteration-count prediction
+    bool pcg_graph = false;
+    DBuf<PcgCtl> pcg_ctl;
+    DBuf<PcgPtrs> pcg_pp;
+    cudaStream_t cap = nullptr;
+    cudaGraphExec_t pcg_exec = nullptr;
+    int pcg_kernels_per_it = 0;
     DBuf<float> targets, weights;
     DBuf<float> g_comp, g_force, g_shape, g_sph;
     DBuf<float> g_x0, g_v0;
@@ -1161,9 +1169,9 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     CGCGBufs cb{s->ax.p, s->p.p, {s->r.p, s->r1.p}, {s->p1.p, s->s1.p}, {s->q.p, s->w1.p}, s->rhs.p};
     auto cgcg_launch = [&](int i) {
         if (s->cgcg_minb == 3)
-            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<256, 3><<<s->ntiles, 256, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
+            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<kMvThreads, kMvMinB - 1><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
         else
-            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<256, 4><<<s->ntiles, 256, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
+            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<kMvThreads, kMvMinB><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
     };
     if (cgcg)
         cgcg_launch(-1);
@@ -1171,6 +1179,98 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         LAUNCH(DXPBD_K_CG_INIT, k_cg_start<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->r.p, s->p.p, xw, cs));
     int launches = 1;
     int it = 0;
+    // one PCG iteration (it >= 0, or it = -1 with the graph-mode state: counter and pointers on the device)
+    auto iteration = [&](int it, cudaStream_t st, const CGState &cs) -> int {
+        if (cgcg) {
+            cgcg_launch(it);
+            return 1;
+        }
+        if (tetv) {
+            if (s->tetv_minb == 3)
+                LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<3><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
+                                                                                     xw, Qc, cs, s->t_q4.p));
+            else
+                LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<1><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
+                                                                                     xw, Qc, cs, s->t_q4.p));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update_tet<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, Qc, cs, s->t_q4.p));
+            return 2;
+        }
+        int n = 0;
+        if (s->use_tma) {
+            if (s->mv_minb == 3)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<kMvThreads, kMvMinB - 1><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
+                                                                                                         defer ? s->ax.p : nullptr)));
+            else
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<kMvThreads, kMvMinB><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
+                                                                                                         defer ? s->ax.p : nullptr)));
+        } else if (s->qf == 1)
+            LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
+        else
+            LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<0><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
+        ++n;
+        if (s->T) {
+            LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), tQr, bufs, xw, cs, s->t_q4.p));
+            LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->t_q4.p, cs));
+            n += 2;
+        }
+        if (defer)
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<false><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
+        else
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<true><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
+        return n + 1;
+    };
+    if (s->pcg_graph && !cgcg && !s->prof) {
+        // the whole iteration loop as one graph launch: a WHILE node over one iteration whose update kernel's
+        // last block sets the condition (kernels.cuh pcg_ctl_end); built once per scene, the buffers that
+        // change between substeps are read from pcg_pp
+        if (!s->pcg_exec) {
+            if (!s->cap) {   // captured kernel nodes keep the capture stream's priority: the PCG's (highest)
+                int least = 0, greatest = 0;
+                DX_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+                DX_CHECK_CUDA(cudaStreamCreateWithPriority(&s->cap, cudaStreamNonBlocking, greatest));
+            }
+            cudaGraph_t g = nullptr;
+            DX_CHECK_CUDA(cudaGraphCreate(&g, 0));
+            cudaGraphConditionalHandle h;
+            DX_CHECK_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+            cudaMemsetParams mp = {};
+            mp.dst = &s->pcg_ctl.p->it;
+            mp.value = 0;
+            mp.elementSize = 4;
+            mp.width = 1;
+            mp.height = 1;
+            cudaGraphNode_t mn, wn;
+            DX_CHECK_CUDA(cudaGraphAddMemsetNode(&mn, g, nullptr, 0, &mp));
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            DX_CHECK_CUDA(cudaGraphAddNode(&wn, g, &mn, 1, &cp));
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            CGState cg = cs;
+            cg.ctl = s->pcg_ctl.p;
+            cg.cond = h;
+            cg.maxit = maxit;
+            cg.pp = s->pcg_pp.p;
+            DX_CHECK_CUDA(cudaStreamBeginCaptureToGraph(s->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            s->pcg_kernels_per_it = iteration(-1, s->cap, cg);
+            DX_CHECK_CUDA(cudaStreamEndCapture(s->cap, &body));
+            if (defer) {
+                DX_CHECK_CUDA(cudaStreamBeginCaptureToGraph(s->cap, g, &wn, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+                k_cg_ufinal<<<nblk(V), kBlock, 0, s->cap>>>(V, -1, bufs, cg);
+                DX_CHECK_CUDA(cudaStreamEndCapture(s->cap, &g));
+            }
+            DX_CHECK_CUDA(cudaGraphInstantiate(&s->pcg_exec, g, 0));
+            DX_CHECK_CUDA(cudaGraphDestroy(g));
+        }
+        k_set_pcg_ptrs<<<1, 1, 0, st>>>(s->pcg_pp.p, PcgPtrs{s->ax.p, tt.Q4, Qc, tQr});
+        DX_CHECK_CUDA(cudaGraphLaunch(s->pcg_exec, st));
+        DX_CHECK_CUDA(cudaGetLastError());
+        iters_out = -1;   // known on the device only (PcgCtl, read at the end of the backward)
+        relres_out = 0.0;
+        return 1;
+    }
     // launches between host convergence polls: first the previous solve's count (consecutive
     // substeps need nearly the same number), then small chunks; launches past convergence exit at once
     int chunk = s->last_iters > 0 ? std::max(s->last_iters + s->poll_extra, 2) : 8;
@@ -1179,46 +1279,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         chunk = 2;
-        for (; it < end; ++it) {
-            if (cgcg) {
-                cgcg_launch(it);
-                ++launches;
-                continue;
-            }
-            if (tetv) {
-                if (s->tetv_minb == 3)
-                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<3><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
-                                                                                         xw, Qc, cs, s->t_q4.p));
-                else
-                    LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<1><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
-                                                                                         xw, Qc, cs, s->t_q4.p));
-                LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update_tet<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, Qc, cs, s->t_q4.p));
-                launches += 2;
-                continue;
-            }
-            if (s->use_tma) {
-                if (s->mv_minb == 3)
-                    LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 3><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
-                                                                                                             defer ? s->ax.p : nullptr)));
-                else
-                    LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<256, 4><<<s->ntiles, 256, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
-                                                                                                             defer ? s->ax.p : nullptr)));
-            } else if (s->qf == 1)
-                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
-            else
-                LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<0><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
-            ++launches;
-            if (s->T) {
-                LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), tQr, bufs, xw, cs, s->t_q4.p));
-                LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->t_q4.p, cs));
-                ++launches;
-            }
-            if (defer)
-                LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<false><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
-            else
-                LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<true><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
-            ++launches;
-        }
+        for (; it < end; ++it) launches += iteration(it, st, cs);
         // convergence check: rr of the last completed iteration against |b|^2
         DX_CHECK_CUDA(cudaMemcpyAsync(s->h_scal, s->cg_sc.p, sizeof(double) * (size_t)(maxit + 2) * 4, cudaMemcpyDeviceToHost, st));
         DX_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -1264,6 +1325,8 @@ int dxpbd_destroy(dxpbd_scene *s) {
         if (e) cudaEventDestroy(e);
     if (s->aux) cudaStreamDestroy(s->aux);
     if (s->hi) cudaStreamDestroy(s->hi);
+    if (s->pcg_exec) cudaGraphExecDestroy(s->pcg_exec);
+    if (s->cap) cudaStreamDestroy(s->cap);
     delete s;
     return DXPBD_OK;
 }
@@ -1338,6 +1401,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_OVERLAP")) s->overlap = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_QCACHE")) s->qcache_on = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_POLL_EXTRA")) s->poll_extra = atoi(ev);
+    if (const char *ev = getenv("DXPBD_PCG_GRAPH")) s->pcg_graph = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_WAVE")) s->wave_on = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_WAVE_G")) s->wave_g = std::max(1, atoi(ev));
     if (const char *ev = getenv("DXPBD_WAVE_FWD")) s->wave_fwd = atoi(ev) != 0;
@@ -1532,10 +1596,10 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 if (s->qf == 0) s->d_Qt2b.alloc((size_t)NTOT + 2);
                 s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->qf == 0);
                 s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0);
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
                 if (const char *ev = getenv("DXPBD_CGCG_MINB")) s->cgcg_minb = atoi(ev);
                 if (const char *ev = getenv("DXPBD_CG")) s->cgcg = std::string(ev) == "cgcg";
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
@@ -1733,6 +1797,15 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     int launches = num_keys + 2, total_it = 0, max_it = 0;
     double worst = 0.0;
     int solves = 0;
+    // PCG iteration loops as graph launches (pcg_solve): counts and convergence come back once, at the end
+    const bool gmode = s->pcg_graph && !s->prof && !(s->use_tma && s->qf == 1 && !s->T && s->cgcg);
+    if (gmode) {
+        if (!s->pcg_ctl.p) {
+            s->pcg_ctl.alloc(1);
+            s->pcg_pp.alloc(1);
+        }
+        DX_CHECK_CUDA(cudaMemsetAsync(s->pcg_ctl.p, 0, sizeof(PcgCtl), st));
+    }
     // PCG start fused into the TMA rhs kernel (no tet rhs pass after it, standard PCG)
     const bool fuse_start = s->use_tma && !s->T && !(s->cgcg && s->qf == 1);
     // replay of substep n-1 on the aux stream during the PCG of substep n (independent work: the
@@ -1863,9 +1936,11 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         launches += pcg_solve(s, st, iters, rel, fuse_start);   // u_n into s->ax
         if (warm2) std::swap(s->uprev2.p, s->uprev.p);   // uprev2 <- u_{n+2}
         std::swap(s->uprev.p, s->u0.p);   // uprev <- u_{n+1}, u0 <- u_{n+2} or u_{n+3} (free)
-        total_it += iters;
-        max_it = std::max(max_it, iters);
-        worst = std::max(worst, rel);
+        if (iters >= 0) {
+            total_it += iters;
+            max_it = std::max(max_it, iters);
+            worst = std::max(worst, rel);
+        }
         ++solves;
         LAUNCH(DXPBD_K_ADJOINT, k_adjoint_accum<<<nblk(V), kBlock, 0, st>>>(V, s->inv_mass.p, s->ax.p, s->y.p, gf, s->dt));
         ++launches;
@@ -1901,6 +1976,17 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     DX_CHECK_CUDA(cudaMemcpyAsync(s->h_scal, s->acc.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     DX_CHECK_CUDA(cudaStreamSynchronize(st));
     phi = s->h_scal[0];
+    if (gmode && solves > 0) {
+        PcgCtl c;
+        DX_CHECK_CUDA(cudaMemcpy(&c, s->pcg_ctl.p, sizeof(PcgCtl), cudaMemcpyDeviceToHost));
+        total_it = (int)c.sum_it;
+        max_it = c.max_it;
+        worst = c.worst;
+        launches += (int)c.execd * s->pcg_kernels_per_it + (s->use_tma && s->defer_u ? solves : 0);
+        s->last_iters = max_it;
+        if (c.fail) throw Err{DXPBD_ERR_SOLVE, "PCG did not converge within " + std::to_string(s->cg_max_iter) +
+                                                  " iterations (worst relative residual " + std::to_string(c.worst) + ")"};
+    }
     if (loss_out) *loss_out = (float)phi;
     s->stats[0] = total_it;
     // substeps of this backward whose blocks came from the forward's cache (no replay)

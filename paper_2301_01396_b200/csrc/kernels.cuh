@@ -521,11 +521,82 @@ __global__ void __launch_bounds__(kBlock) k_contact_replay(int V, int NC, const 
 // slot array sc[it*4 + {0: p.Ap, 1: r.z, 2: r.r}] (double) so no reset is ever needed:
 // iteration `it` accumulates into slot it, reads slot it-1 (and slot "rz" of it-1).
 // done-test: an iteration returns immediately if the previous residual met the tolerance.
+// Device-side PCG control (graph mode): the iteration loop is a
+// conditional WHILE node; the last block of each update kernel tests convergence, advances the
+// iteration counter and sets the loop condition, so no host poll is needed.  Per-backward totals
+// are accumulated here and read once at the end.
+struct PcgCtl {
+    unsigned blk;      // blocks of the current update launch that finished (last-block ticket)
+    int it;            // iteration counter read by the kernels launched with it < 0
+    int K;             // iterations of the last solve (read by k_cg_ufinal with K < 0)
+    int fail;          // a solve reached max_iter without converging
+    long long sum_it;  // sum of iterations over the solves of this backward
+    int max_it;
+    int solves;
+    long long execd;   // iterations executed (launched loop bodies)
+    double worst;      // largest final relative residual
+};
+
+// Graph mode: the pointers that change from substep to substep (the solution buffer rotates with
+// the warm start, the block buffers alternate with the replay overlap / come from the forward's
+// cache) are read from this device block, written by k_set_pcg_ptrs before each graph launch.
+struct PcgPtrs {
+    float3 *u;
+    const float4 *Qt;   // TMA-layout blocks
+    const float *Qc;    // contact blocks
+    const float *tQ;    // tet blocks
+};
+
 struct CGState {
     double *sc;      // [(max_iter+2)*4]
     double *bnorm2;  // b.b (filtered)
     float tol2;
+    PcgCtl *ctl = nullptr;                    // graph mode only
+    cudaGraphConditionalHandle cond = 0;      // the WHILE node's condition
+    int maxit = 0;
+    const PcgPtrs *pp = nullptr;              // graph mode only
 };
+
+__global__ void k_set_pcg_ptrs(PcgPtrs *pp, PcgPtrs v) { *pp = v; }
+
+// iteration index of a PCG kernel: its argument, or (graph mode, it < 0) the device counter
+DX_INLINE int cg_iter(const CGState &s, int it) { return it >= 0 ? it : *(volatile int *)&s.ctl->it; }
+
+// Graph mode, end of an update kernel (all threads of every block): the last block to finish reads
+// the residual of iteration it + 1 (all blocks' reductions are visible after their fences), decides
+// convergence exactly as the host poll does (rr <= tol2 |b|^2, K = first converged slot), advances
+// the counter and sets the WHILE condition.
+DX_INLINE void pcg_ctl_end(const CGState &s, int it) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&s.ctl->blk, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    PcgCtl *c = s.ctl;
+    c->blk = 0;
+    const volatile double *sc = s.sc;
+    const double bb = *(volatile double *)s.bnorm2, thr = (double)s.tol2 * bb;
+    int K = -1;
+    if (bb == 0.0) K = 0;
+    else if (it == 0 && sc[2] <= thr) K = 0;             // the warm start already converged
+    else if (sc[(it + 1) * 4 + 2] <= thr) K = it + 1;
+    const bool stop = K >= 0 || it + 1 >= s.maxit;
+    c->it = it + 1;
+    if (stop) {
+        c->execd += it + 1;
+        if (K < 0) { c->fail = 1; K = s.maxit; }
+        c->K = K;
+        c->sum_it += K;
+        c->max_it = max(c->max_it, K);
+        c->solves += 1;
+        if (bb > 0.0) c->worst = fmax(c->worst, sqrt(sc[min(K, s.maxit) * 4 + 2] / bb));
+    }
+    cudaGraphSetConditional(s.cond, stop ? 0u : 1u);
+}
 
 DX_INLINE bool cg_done(const CGState &s, int it) {
     // converged after iteration it-1 ?
@@ -544,7 +615,10 @@ DX_INLINE bool cg_done(const CGState &s, int it) {
 // walks its segment of every color, accumulates q for its own vertices in shared memory and
 // flushes each owned vertex with one vector reduction; only endpoints outside the tile (halo)
 // use global reductions.  With DOT it also accumulates p.(A p) = Sum_j d^T Q_j d.
-constexpr int kTileV = 512;
+#ifndef DX_TILEV
+#define DX_TILEV 512
+#endif
+constexpr int kTileV = DX_TILEV;   // vertices per Morton tile (a power of two: aligned lattice blocks)
 
 template <int QF>
 struct QVal {
@@ -610,6 +684,12 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
                                                       const float *__restrict__ Q, int E,
                                                       const float *__restrict__ Qc, CGBufs B,
                                                       const float *__restrict__ wv, CGState s) {
+    it = cg_iter(s, it);
+    if (s.pp) {
+        const PcgPtrs pp = *s.pp;
+        if (Qc) Qc = pp.Qc;
+        B.u = pp.u;
+    }
     if (cg_done(s, it + 1)) return;
     __shared__ float sp[3][kTileV];
     __shared__ float sq[3][kTileV];
@@ -712,7 +792,10 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
 // in shared memory (plain read-modify-write of the accumulator, one barrier per color,
 // vertex-disjoint within a color by R1).
 constexpr int kTmaStages = 3;
-constexpr int kTmaThreads = 256;
+constexpr int kTmaThreads = kTileV / 2;                  // rhs kernel threads per tile
+constexpr int kRhsMinB = kTileV == 512 ? 3 : 1;           // its launch-bounds CTAs per SM
+constexpr int kMvThreads = kTileV / 2;                   // matvec threads per tile
+constexpr int kMvMinB = 2048 / kTileV;                   // its resident CTAs per SM (64 registers)
 constexpr int kMaxColors = 64;   // bounds table in shared memory (more colors: generic kernel)
 
 struct TmaTiles {
@@ -836,6 +919,14 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap, T.Q2 != nullptr) * kTmaStages);
     float4 *sp = sq + kTileV;
     const int hcap = T.hcap;
+    it = cg_iter(s, it);
+    if (s.pp) {   // graph mode: this substep's buffers
+        const PcgPtrs pp = *s.pp;
+        T.Q4 = pp.Qt;
+        if (Qc) Qc = pp.Qc;
+        B.u = pp.u;
+        if (ufix) ufix = pp.u;
+    }
     const int t = blockIdx.x + t0;   // t0: first tile of a partition (domain decomposition)
     const int v0 = t * kTileV;
     const int nv = min(kTileV, V - v0);
@@ -1129,7 +1220,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V,
 
 // rhs (warm start): b = M u - Q_n y + dphi, r0 = b - A_n (u + du); A_dist applied tile-locally
 // with the same staging / slot layout as the matvec.
-__global__ void __launch_bounds__(kTmaThreads, 3) k_rhs_tma(TmaTiles T, int V, const float *__restrict__ Qc,
+__global__ void __launch_bounds__(kTmaThreads, kRhsMinB) k_rhs_tma(TmaTiles T, int V, const float *__restrict__ Qc,
                                                             const float3 *__restrict__ u, const float3 *__restrict__ uprev,
                                                             const float3 *__restrict__ uprev2,
                                                             const float3 *__restrict__ y,
@@ -1438,7 +1529,12 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tiled(TileLists L, int V, const 
 // r.M^-1 r and r.r into slot it+1; the V % 4 tail vertices by one extra thread.
 template <bool UPD_U>
 __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ wv, CGState s) {
-    if (cg_done(s, it + 1)) return;
+    it = cg_iter(s, it);
+    if (s.pp) B.u = s.pp->u;
+    if (cg_done(s, it + 1)) {
+        if (s.ctl) pcg_ctl_end(s, it);
+        return;
+    }
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nq = V / 4;
     float acc[2] = {0.f, 0.f};
@@ -1491,6 +1587,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         }
     }
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
+    if (s.ctl) pcg_ctl_end(s, it);
 }
 
 // Deferred solution update (UPD_U = false above): the matvec of iteration it adds
@@ -1498,6 +1595,10 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
 // last term alpha_{K-1} p_{K-1}.
 __global__ void k_cg_ufinal(int V, int K, CGBufs B, CGState s) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (K < 0) {   // graph mode: the solve's iteration count and solution buffer
+        K = s.ctl->K;
+        B.u = s.pp->u;
+    }
     if (v >= V || K <= 0) return;
     const double pq = s.sc[K * 4 + 0];
     const float alpha = pq > 0.0 ? (float)(s.sc[(K - 1) * 4 + 1] / pq) : 0.f;

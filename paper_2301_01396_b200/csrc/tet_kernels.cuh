@@ -501,6 +501,11 @@ DX_INLINE void tet_Qmul(const float *__restrict__ Qt, int T, int j, const float 
 __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float *__restrict__ Qt, CGBufs B,
                                                    const float *__restrict__ wv, CGState s,
                                                    float4 *__restrict__ q4 = nullptr) {
+    it = cg_iter(s, it);
+    if (s.pp) {
+        Qt = s.pp->tQ;
+        B.u = s.pp->u;
+    }
     if (cg_done(s, it + 1)) return;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     float acc[1] = {0.f};
@@ -531,6 +536,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float
 
 // q += xyz(q4) (the tet matvec's float4 accumulator), q4 <- 0 for the next iteration
 __global__ void k_fold_q4(int V, int it, CGBufs B, float4 *__restrict__ q4, CGState s) {
+    it = cg_iter(s, it);
     if (cg_done(s, it + 1)) return;
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
@@ -549,6 +555,13 @@ __global__ void __launch_bounds__(kBlock, MINB) k_cg_tetv(int it, int nbt, int V
                                                     CGBufs B, const float *__restrict__ wv,
                                                     const float *__restrict__ Qc, CGState s,
                                                     float4 *__restrict__ q4) {
+    it = cg_iter(s, it);
+    if (s.pp) {
+        const PcgPtrs pp = *s.pp;
+        Qt = pp.tQ;
+        if (Qc) Qc = pp.Qc;
+        B.u = pp.u;
+    }
     if (cg_done(s, it + 1)) return;
     const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;   // p_{it-1}
     float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;         // p_it
@@ -618,7 +631,16 @@ __global__ void __launch_bounds__(kBlock, MINB) k_cg_tetv(int it, int nbt, int V
 __global__ void __launch_bounds__(kBlock) k_cg_update_tet(int V, int it, CGBufs B, const float *__restrict__ wv,
                                                           const float *__restrict__ Qc, CGState s,
                                                           float4 *__restrict__ q4) {
-    if (cg_done(s, it + 1)) return;
+    it = cg_iter(s, it);
+    if (s.pp) {
+        const PcgPtrs pp = *s.pp;
+        if (Qc) Qc = pp.Qc;
+        B.u = pp.u;
+    }
+    if (cg_done(s, it + 1)) {
+        if (s.ctl) pcg_ctl_end(s, it);
+        return;
+    }
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     float acc[2] = {0.f, 0.f};
     if (v < V) {
@@ -647,6 +669,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update_tet(int V, int it, CGBufs 
         acc[1] += r2;
     }
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
+    if (s.ctl) pcg_ctl_end(s, it);
 }
 
 // Tet part of the increment rhs: b -= G^T Qt~ G y, r0 -= G^T Qt~ G (y + u0), u0 = warm start

@@ -257,3 +257,56 @@ def test_wave_sweep_bit_identical(monkeypatch, case):
         assert la == lb, (name, g)
         for k in grads:
             np.testing.assert_array_equal(ga[k], gb[k], err_msg=f"{name} g={g} {k}")
+
+
+def _pcg_cases():
+    from synth import volumetric_block
+    return [
+        ("tma_cloth", lambda: f32(large_cloth(n=64, frames=2, substeps=3, side=10.0 * 63 / 2943.0, key_frames=(2,))
+                                  .replace(frame_dt=3 / 600)), ("forces", "x0", "v0")),
+        ("sphere", lambda: f32(medium_cloth(n=32, frames=3)), ("compliance", "sphere", "x0")),
+        ("tets", lambda: f32(volumetric_block(n=6, frames=2, substeps=4)), ("material", "x0")),
+        ("k3_generic", lambda: f32(tiny_cloth(n=12, frames=2, iterations=3)), ("compliance", "v0")),
+    ]
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_pcg_graph_matches_host_polls(monkeypatch, case):
+    """The PCG iteration loop as a CUDA graph (conditional WHILE node, convergence decided by the
+    update kernel's last block) against the host-polled loop: same kernels, same convergence test,
+    so positions, loss, gradients and the iteration statistics are identical."""
+    name, mk, grads = _pcg_cases()[case]
+    s = mk()
+    monkeypatch.setenv("DXPBD_PCG_GRAPH", "0")
+    xa, la, ga, sa = _run_all(s, grads, s.frames)
+    monkeypatch.setenv("DXPBD_PCG_GRAPH", "1")
+    xb, lb, gb, sb = _run_all(s, grads, s.frames)
+    det = name != "tets"   # the tet matvec accumulates with float atomics (run-to-run summation order)
+    for f in range(s.frames + 1):
+        np.testing.assert_array_equal(xa[f], xb[f])
+    assert la == lb, name
+    for k in grads:
+        if not det or k in ("sphere", "shape"):   # atomics: summation order may differ
+            assert rel_l2(gb[k], ga[k]) < 1e-4, (name, k, rel_l2(gb[k], ga[k]))
+        else:
+            np.testing.assert_array_equal(ga[k], gb[k], err_msg=f"{name} {k}")
+    assert sa["solves"] == sb["solves"]
+    if det:
+        for key in ("cg_iters_total", "cg_iters_max"):
+            assert sa[key] == sb[key], (name, key, sa[key], sb[key])
+        assert abs(sa["worst_relres"] - sb["worst_relres"]) <= 1e-12 + 1e-9 * sa["worst_relres"]
+    else:
+        assert abs(sa["cg_iters_total"] - sb["cg_iters_total"]) <= 0.05 * sa["cg_iters_total"]
+
+
+def test_pcg_graph_reports_nonconvergence(monkeypatch):
+    """A solve that cannot reach the tolerance within cg_max_iter fails the backward with an error in
+    graph mode too (detected on the device, reported at the end of the call)."""
+    api = _api()
+    s = f32(tiny_cloth(n=12, frames=2))
+    for mode in ("0", "1"):
+        monkeypatch.setenv("DXPBD_PCG_GRAPH", mode)
+        sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=2, cg_tol=1e-12, cg_max_iter=2)
+        api.dxpbd_forward(sc, s.x0, s.v0, None, 2)
+        with pytest.raises(api.DxpbdError, match="converge"):
+            api.dxpbd_backward(sc, [2], s.targets)

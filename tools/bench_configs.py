@@ -58,16 +58,20 @@ def run(name, make, grads):
     t_create = time.perf_counter() - t0
     x0, v0, f, tg = t(s.x0), t(s.v0), t(s.forces), t(s.targets)
     w = t(s.weights) if s.weights is not None else None
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    torch.cuda.synchronize()
-    ev[0].record()
-    api.dxpbd_forward(sc, x0, v0, f, s.frames)
-    ev[1].record()
-    loss = api.dxpbd_backward(sc, s.key_frames, tg, w)
-    for g in grads:
-        api.dxpbd_grads(sc, g)
-    ev[2].record()
-    torch.cuda.synchronize()
+    fwds, tots = [], []
+    for _ in range(REPEAT):   # the first pass includes one-time work (graph instantiation, lazy buffers)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize()
+        ev[0].record()
+        api.dxpbd_forward(sc, x0, v0, f, s.frames)
+        ev[1].record()
+        loss = api.dxpbd_backward(sc, s.key_frames, tg, w)
+        for g in grads:
+            api.dxpbd_grads(sc, g)
+        ev[2].record()
+        torch.cuda.synchronize()
+        fwds.append(ev[0].elapsed_time(ev[1]))
+        tots.append(ev[0].elapsed_time(ev[2]))
     st = api.dxpbd_stats(sc)
     if s.name == "garment":
         xl = api.dxpbd_positions(sc, s.frames).astype(np.float64)
@@ -76,15 +80,19 @@ def run(name, make, grads):
                      rms_miss_to_target=float(np.sqrt(2 * loss / s.num_vertices)),
                      shape_grad=api.dxpbd_grads(sc, "shape").tolist())
     N = s.frames * s.substeps
-    fwd, tot = ev[0].elapsed_time(ev[1]), ev[0].elapsed_time(ev[2])
+    k = int(np.argmin(tots))   # best of REPEAT full-length passes
+    fwd, tot = fwds[k], tots[k]
     line = dict(config=name, vertices=s.num_vertices, constraints=len(s.dist_idx), tets=len(s.tet_idx),
                 colliders=len(s.spheres) + len(s.cap_center), frames=s.frames, substeps=s.substeps, grads=list(grads),
                 ms_forward=fwd, ms_forward_adjoint=tot, ms_per_substep_fwd=fwd / N, ms_per_substep_fwd_adjoint=tot / N,
                 cg_iters_per_substep=st["cg_iters_total"] / max(st["solves"], 1), cg_iters_max=st["cg_iters_max"],
-                worst_relres=st["worst_relres"], tma_path=st["tma"], loss=loss, create_s=t_create, **extra)
+                worst_relres=st["worst_relres"], tma_path=st["tma"], loss=loss, create_s=t_create,
+                passes=REPEAT, ms_forward_adjoint_all=tots, **extra)
     print(json.dumps(line), flush=True)
     del sc
 
+
+REPEAT = 3
 
 if __name__ == "__main__":
     which = [int(a) for a in sys.argv[1:]] or range(len(CASES))
