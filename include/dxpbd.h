@@ -100,6 +100,18 @@ typedef struct dxpbd_scene_desc {
     float cg_tol;                    /* relative residual of the filtered PCG (e.g. 1e-6)   */
     int32_t cg_max_iter;             /* PCG iteration cap per substep                       */
     int32_t device;                  /* CUDA device ordinal                                 */
+
+    /* batch of independent scenes in one handle (north_star (4) "batches of independent scenes"):
+     * vertex_scene[v] in [0, num_scenes) tags every vertex; every distance constraint / tet must
+     * lie within one scene (else DXPBD_ERR_ARG); collider_scene[c] (spheres then capsules) is the
+     * scene a collider acts on, or -1 for all scenes.  NULL vertex_scene = one scene (then
+     * collider_scene is ignored).  The scenes share the time stepping, the PCG solve per substep
+     * (block-diagonal system, one global relative-residual test) and the loss sum; gradients are
+     * per vertex / constraint / collider, so they separate by scene.  Internal vertex order is
+     * (scene, Morton), so tiles rarely straddle scenes.                                       */
+    int32_t num_scenes;
+    const int32_t *vertex_scene;     /* [V] or NULL                                         */
+    const int32_t *collider_scene;   /* [S + K] or NULL (all colliders act on every scene)  */
 } dxpbd_scene_desc;
 
 /* Build the device-resident scene: uploads topology and parameters, computes rest
@@ -168,6 +180,21 @@ int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
  * Supported: iterations == 1, pd_projection, no tets, grad_flags within FORCES | X0 | V0;
  * the scene must take the TMA path (dxpbd_stats field 13).  Same argument conventions as
  * the scene calls above. */
+/* Host-only partition plan (no GPU, no allocation on a device): the plan dxpbd_group_create /
+ * _create_dist build from the same host topology (Morton tiles, greedy colors R1, halos, TMA
+ * layout).  Partition p owns Morton tiles [t0_p, t1_p).  Exchange lists, ids in INTERNAL vertex
+ * order (Morton; internal vertex i is tile i / kTileV): kind k < nc = the endpoints of the sender's
+ * color-k constraints held by the receiver (sent after every color sweep), k = nc = the sender's
+ * own vertices in the receiver's tile halos (PCG vectors, adjoint), k = nc + 1 = Qt positions of
+ * blocks whose b-tile copy lives in the receiver.  HOST outputs: info[0..6) = {nc, t0_rank,
+ * t1_rank, V, tiles, kTileV}; counts[(k * 2 + dir) * num_parts + q], k < nc + 2, dir 0 = rank ->
+ * q, dir 1 = q -> rank (p == q lists are empty); ids (optional, NULL = counts only): the lists
+ * concatenated in that order, ids_cap >= sum(counts) or DXPBD_ERR_ARG; vperm (optional, [V]):
+ * internal -> user vertex id.  num_parts > tiles -> DXPBD_ERR_ARG; a scene off the TMA path ->
+ * DXPBD_ERR_LIMIT. */
+int dxpbd_partition_plan(const dxpbd_scene_desc *desc, int32_t num_parts, int32_t rank, int32_t *info,
+                         int64_t *counts, int32_t *ids, int64_t ids_cap, int32_t *vperm);
+
 typedef struct dxpbd_group dxpbd_group;
 int dxpbd_group_create(const dxpbd_scene_desc *desc, int32_t num_parts, dxpbd_group **out);
 /* Distributed group: this process holds partition `rank` of `world` (one GPU per process,

@@ -46,6 +46,7 @@ class SceneDesc(ctypes.Structure):
         ("iterations", ctypes.c_int32), ("thickness", ctypes.c_float), ("collision_compliance", ctypes.c_float),
         ("max_frames", ctypes.c_int32), ("grad_flags", ctypes.c_uint32), ("pd_projection", ctypes.c_int32),
         ("cg_tol", ctypes.c_float), ("cg_max_iter", ctypes.c_int32), ("device", ctypes.c_int32),
+        ("num_scenes", ctypes.c_int32), ("vertex_scene", ctypes.c_void_p), ("collider_scene", ctypes.c_void_p),
     ]
 
 
@@ -86,6 +87,7 @@ def lib():
             "dxpbd_group_backward": ([vp, i32, vp, vp, vp, i32, vp, vp], ctypes.c_int),
             "dxpbd_group_grads": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
             "dxpbd_group_stats": ([vp, vp, i32], ctypes.c_int),
+            "dxpbd_partition_plan": ([ctypes.POINTER(SceneDesc), i32, i32, vp, vp, vp, i64, vp], ctypes.c_int),
             "dxpbd_last_error": ([], ctypes.c_char_p),
             "dxpbd_version": ([], ctypes.c_int),
         }
@@ -101,7 +103,7 @@ EXPORTED = ["dxpbd_create", "dxpbd_destroy", "dxpbd_forward", "dxpbd_positions",
             "dxpbd_grads", "dxpbd_set_params", "dxpbd_coloring", "dxpbd_stats", "dxpbd_last_error",
             "dxpbd_version", "dxpbd_profile", "dxpbd_kernel_times", "dxpbd_group_create", "dxpbd_group_destroy",
             "dxpbd_group_forward", "dxpbd_group_positions", "dxpbd_group_backward", "dxpbd_group_grads",
-            "dxpbd_group_stats", "dxpbd_nccl_unique_id", "dxpbd_group_create_dist"]
+            "dxpbd_group_stats", "dxpbd_nccl_unique_id", "dxpbd_group_create_dist", "dxpbd_partition_plan"]
 
 KCLASSES = ["predict", "dist_project", "contact_project", "tet_project", "dist_replay", "contact_replay",
             "tet_replay", "cg_vertex", "cg_dist", "cg_tet", "cg_update", "cg_init", "rhs", "adjoint", "grads",
@@ -192,7 +194,7 @@ def _desc(x_rest, inv_mass, dist_idx=None, dist_compliance=None, tet_idx=None, t
           spheres=None, cap_center=None, cap_axis=None, cap_r0=None, cap_L0=None, cap_rbasis=None,
           cap_lbasis=None, shape_beta=None, gravity=(0.0, -9.81, 0.0), frame_dt=1 / 60, substeps=1,
           iterations=1, thickness=0.0, collision_compliance=0.0, max_frames=1, grad_flags=0,
-          pd_projection=1, cg_tol=1e-6, cg_max_iter=500, device=0):
+          pd_projection=1, cg_tol=1e-6, cg_max_iter=500, device=0, vertex_scene=None, collider_scene=None):
     """dxpbd_scene_desc from host arrays; returns (desc, kept arrays, handle dimensions)."""
     keep = []
 
@@ -240,6 +242,11 @@ def _desc(x_rest, inv_mass, dist_idx=None, dist_compliance=None, tet_idx=None, t
     d.cg_tol = float(cg_tol)
     d.cg_max_iter = int(cg_max_iter)
     d.device = int(device)
+    if vertex_scene is not None:
+        vs = np.asarray(vertex_scene, np.int32).reshape(-1)
+        d.num_scenes = int(vs.max()) + 1 if vs.size else 1
+        d.vertex_scene = h(vs, np.int32)
+        d.collider_scene = h(collider_scene, np.int32) if collider_scene is not None and S + K else None
     return d, keep, (V, E, T, S, K, NS if K else 0, int(max_frames), int(substeps))
 
 
@@ -376,6 +383,37 @@ def dxpbd_group_create(x_rest, inv_mass, num_parts: int = 2, **kw) -> DxGroup:
     return DxGroup(out.value, int(num_parts), *dims)
 
 
+def dxpbd_partition_plan(x_rest, inv_mass, num_parts: int, rank: int, **kw) -> dict:
+    """Host-only partition plan of the domain decomposition (include/dxpbd.h dxpbd_partition_plan):
+    {"colors", "t0", "t1", "V", "tiles", "tile_v", "vperm", "send": {kind: {q: ids}}, "recv": {kind: {q: ids}}}
+    with kind = color index, "halo" or "blocks"; ids in internal (Morton) vertex order, vperm maps
+    internal -> user vertex ids."""
+    d, keep, dims = _desc(x_rest, inv_mass, **kw)
+    P = int(num_parts)
+    info = np.zeros(8, np.int32)
+    # counts size needs the color count: query with a generous bound first
+    counts = np.zeros(2 * P * (256 + 2), np.int64)
+    _check(lib().dxpbd_partition_plan(ctypes.byref(d), P, int(rank), info.ctypes.data, counts.ctypes.data, None, 0,
+                                      None), "dxpbd_partition_plan")
+    nc = int(info[0])
+    total = int(counts[: 2 * P * (nc + 2)].sum())
+    ids = np.zeros(max(total, 1), np.int32)
+    vperm = np.zeros(int(info[3]), np.int32)
+    _check(lib().dxpbd_partition_plan(ctypes.byref(d), P, int(rank), info.ctypes.data, counts.ctypes.data,
+                                      ids.ctypes.data, total, vperm.ctypes.data), "dxpbd_partition_plan")
+    out = {"colors": nc, "t0": int(info[1]), "t1": int(info[2]), "V": int(info[3]), "tiles": int(info[4]),
+           "tile_v": int(info[5]), "vperm": vperm, "send": {}, "recv": {}}
+    o = 0
+    for k in range(nc + 2):
+        name = k if k < nc else ("halo" if k == nc else "blocks")
+        for dirn, key in ((0, "send"), (1, "recv")):
+            for q in range(P):
+                n = int(counts[(k * 2 + dirn) * P + q])
+                out[key].setdefault(name, {})[q] = ids[o:o + n].copy()
+                o += n
+    return out
+
+
 def dxpbd_nccl_unique_id() -> bytes:
     """128-byte NCCL unique id (rank 0), to be broadcast to the other ranks."""
     buf = ctypes.create_string_buffer(128)
@@ -460,6 +498,79 @@ def scene_kwargs(scene) -> dict:
         if len(s.shape_beta):
             kw.update(cap_rbasis=s.cap_rbasis, cap_lbasis=s.cap_lbasis, shape_beta=s.shape_beta)
     return kw
+
+
+def batch_scene_kwargs(scenes) -> dict:
+    """One handle for a batch of independent synth.Scenes (include/dxpbd.h: vertex_scene /
+    collider_scene): vertices, constraints, tets and colliders concatenated in scene order with
+    index offsets; capsule shape bases block-diagonal (each scene keeps its own coefficients).
+    The scenes must share the time stepping, gravity and collision parameters."""
+    s0 = scenes[0]
+    for s in scenes[1:]:
+        for k in ("frame_dt", "substeps", "iterations", "thickness", "collision_compliance"):
+            if getattr(s, k) != getattr(s0, k):
+                raise ValueError(f"batch scenes differ in {k}")
+        if tuple(s.gravity) != tuple(s0.gravity):
+            raise ValueError("batch scenes differ in gravity")
+    voff = np.cumsum([0] + [s.num_vertices for s in scenes])
+    cat = lambda xs: np.concatenate([np.asarray(x) for x in xs], 0)  # noqa: E731
+    kw = dict(x_rest=cat([s.x_rest for s in scenes]), inv_mass=cat([s.inv_mass for s in scenes]),
+              gravity=tuple(s0.gravity), frame_dt=s0.frame_dt, substeps=s0.substeps, iterations=s0.iterations,
+              thickness=s0.thickness, collision_compliance=s0.collision_compliance,
+              vertex_scene=np.repeat(np.arange(len(scenes), dtype=np.int32), [s.num_vertices for s in scenes]))
+    if sum(len(s.dist_idx) for s in scenes):
+        kw.update(dist_idx=cat([np.asarray(s.dist_idx).reshape(-1, 2) + voff[b] for b, s in enumerate(scenes)]),
+                  dist_compliance=cat([s.dist_compliance for s in scenes]))
+    if sum(len(s.tet_idx) for s in scenes):
+        kw.update(tet_idx=cat([np.asarray(s.tet_idx).reshape(-1, 4) + voff[b] for b, s in enumerate(scenes)]),
+                  tet_a=cat([s.tet_a for s in scenes]), tet_b=cat([s.tet_b for s in scenes]))
+    csc = []
+    if sum(len(s.spheres) for s in scenes):
+        kw.update(spheres=cat([np.asarray(s.spheres).reshape(-1, 4) for s in scenes]))
+        csc += [b for b, s in enumerate(scenes) for _ in range(len(s.spheres))]
+    if sum(len(s.cap_center) for s in scenes):
+        kw.update(cap_center=cat([np.asarray(s.cap_center).reshape(-1, 3) for s in scenes]),
+                  cap_axis=cat([np.asarray(s.cap_axis).reshape(-1, 3) for s in scenes]),
+                  cap_r0=cat([s.cap_r0 for s in scenes]), cap_L0=cat([s.cap_L0 for s in scenes]))
+        csc += [b for b, s in enumerate(scenes) for _ in range(len(s.cap_center))]
+        ns = [len(s.shape_beta) if len(s.cap_center) else 0 for s in scenes]
+        if sum(ns):
+            K = sum(len(s.cap_center) for s in scenes)
+            Rb, Lb = np.zeros((K, sum(ns))), np.zeros((K, sum(ns)))
+            k0, n0 = 0, 0
+            for s, n in zip(scenes, ns):
+                k1 = k0 + len(s.cap_center)
+                if n:
+                    Rb[k0:k1, n0:n0 + n] = np.asarray(s.cap_rbasis).reshape(-1, n)
+                    Lb[k0:k1, n0:n0 + n] = np.asarray(s.cap_lbasis).reshape(-1, n)
+                k0, n0 = k1, n0 + n
+            kw.update(cap_rbasis=Rb, cap_lbasis=Lb,
+                      shape_beta=cat([s.shape_beta for s, n in zip(scenes, ns) if n]))
+    if csc:
+        kw.update(collider_scene=np.asarray(csc, np.int32))
+    return kw
+
+
+def batch_inputs(scenes, frames: int):
+    """x0, v0, forces ([frames][V][3] or None) and targets ([keys][V][3]) of a batch, concatenated
+    along vertices in scene order (the scenes must share their keyframes)."""
+    kf = [list(np.asarray(s.key_frames).tolist()) for s in scenes]
+    if any(k != kf[0] for k in kf):
+        raise ValueError("batch scenes differ in key frames")
+    x0 = np.concatenate([s.x0 for s in scenes], 0)
+    v0 = np.concatenate([s.v0 for s in scenes], 0)
+    forces = None
+    if any(s.forces is not None for s in scenes):
+        forces = np.concatenate([s.forces[:frames] if s.forces is not None else np.zeros((frames, s.num_vertices, 3))
+                                 for s in scenes], 1)
+    targets = None if scenes[0].targets is None else np.concatenate([s.targets for s in scenes], 1)
+    return x0, v0, forces, np.asarray(kf[0], np.int32), targets
+
+
+def batch_split(a, scenes, axis: int = 0):
+    """Split a per-vertex result of a batch ([..][V][..] along `axis`) back into per-scene arrays."""
+    cuts = np.cumsum([s.num_vertices for s in scenes])[:-1]
+    return np.split(np.asarray(a), cuts, axis=axis)
 
 
 def flags(*names) -> int:

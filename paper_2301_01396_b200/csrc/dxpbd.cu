@@ -15,6 +15,7 @@
 #include <string>
 #include <memory>
 #include <thread>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -28,7 +29,6 @@ using namespace dx;
 namespace {
 
 thread_local std::string g_err;
-thread_local bool g_keep_host = false;   // dxpbd_create keeps the host layout (partition groups)
 
 struct Err {
     int code;
@@ -311,22 +311,23 @@ static inline uint64_t spread3(uint64_t x) {
 // codes is an aligned lattice block: tiles are compact rectangles / boxes (32 x 16 at kTileV = 512 on
 // a cloth grid), which minimises tile halos and cross-tile constraints.  A cell of extent / 2^21
 // (the key's resolution) when h is unknown or smaller.
-void morton_order(const float *x, int V, double h, std::vector<int32_t> &perm) {
+void morton_order(const float *x, int V, double h, std::vector<int32_t> &perm, const int32_t *scene = nullptr) {
     float lo[3] = {x[0], x[1], x[2]}, hi[3] = {x[0], x[1], x[2]};
     for (int i = 0; i < V; ++i)
         for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], x[3 * i + k]); hi[k] = std::max(hi[k], x[3 * i + k]); }
     float ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
     const double cell = std::max(h, (double)ext / 2097151.0);
     double sc = cell > 0 ? 1.0 / cell : 0.0;
-    std::vector<std::pair<uint64_t, int32_t>> key(V);
+    // (scene, Morton code, index): a batch keeps each scene's vertices contiguous
+    std::vector<std::tuple<int32_t, uint64_t, int32_t>> key(V);
     for (int i = 0; i < V; ++i) {
         uint64_t q[3];
         for (int k = 0; k < 3; ++k) q[k] = (uint64_t)std::llround((x[3 * i + k] - lo[k]) * sc);
-        key[i] = {spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2), i};
+        key[i] = std::make_tuple(scene ? scene[i] : 0, spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2), i);
     }
     std::sort(key.begin(), key.end());
     perm.resize(V);
-    for (int i = 0; i < V; ++i) perm[i] = key[i].second;
+    for (int i = 0; i < V; ++i) perm[i] = std::get<2>(key[i]);
 }
 
 // dst[i] = src[perm[i]] for [count][V][3] arrays (user -> internal vertex order)
@@ -411,7 +412,8 @@ __global__ void k_rest_len(int n, const int2 *__restrict__ idx, const float *__r
 __global__ void k_shape_apply(int nsph, int ncap, int ns, const float *__restrict__ spheres,
                               const float *__restrict__ cc, const float *__restrict__ ca, const float *__restrict__ r0,
                               const float *__restrict__ L0, const float *__restrict__ Rb, const float *__restrict__ Lb,
-                              const float *__restrict__ beta, Collider *__restrict__ out) {
+                              const float *__restrict__ beta, Collider *__restrict__ out,
+                              const int *__restrict__ csc) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < nsph) {
         Collider c;
@@ -420,7 +422,7 @@ __global__ void k_shape_apply(int nsph, int ncap, int ns, const float *__restric
         c.r = spheres[4 * k + 3];
         c.L = 0.f;
         c.type = 0;
-        c.pad = 0;
+        c.scene = csc ? csc[k] : -1;
         out[k] = c;
     } else if (k < nsph + ncap) {
         int q = k - nsph;
@@ -435,7 +437,7 @@ __global__ void k_shape_apply(int nsph, int ncap, int ns, const float *__restric
         c.r = r;
         c.L = L;
         c.type = 1;
-        c.pad = 0;
+        c.scene = csc ? csc[k] : -1;
         out[k] = c;
     }
 }
@@ -453,6 +455,173 @@ __global__ void k_shape_grad(int nsph, int ncap, int ns, const double *__restric
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------ host topology (create time)
+// Everything the scene's distance-constraint layout needs, computed on the host without a GPU, so
+// the same code serves dxpbd_create, the partition planner of the domain decomposition and the
+// host-only dxpbd_partition_plan (tested on CPU with gloo ranks).
+struct DistTopo {
+    int V = 0, E = 0, nt = 0, nc = 0;
+    std::vector<int32_t> vperm;                 // internal -> user vertex (Morton order)
+    std::vector<int32_t> color, perm;           // greedy color per user constraint; sorted position -> user index
+    std::vector<int> dist_off, seg, fseg;       // color offsets; [nc][nt + 1] own / foreign segment offsets
+    std::vector<int2> ab;                       // sorted constraints, internal endpoints (a < b)
+    std::vector<std::vector<int>> halo;         // per tile: halo vertices (sorted)
+    std::vector<int> fidx;                      // foreign lists (sorted constraint positions)
+    int64_t n_foreign = 0, halo_total = 0;
+    int hcap = 0, capm = 0;
+    bool use_tma = false;
+    // TMA layout (use_tma)
+    std::vector<int> hpad, fposv, tpos;
+    std::vector<int4> tseg;
+    std::vector<uint32_t> cpair;
+    std::vector<uint16_t> vslot, hslot;
+    int64_t ntot = 0;
+};
+
+// Morton vertex order with the short-edge quantization cell (see morton_order)
+void vertex_order(const dxpbd_scene_desc *d, std::vector<int32_t> &vperm) {
+    std::vector<double> len;
+    auto edge = [&](int a, int b) {
+        double q = 0;
+        for (int k = 0; k < 3; ++k) { const double u = (double)d->x_rest[3 * a + k] - d->x_rest[3 * b + k]; q += u * u; }
+        if (q > 0) len.push_back(std::sqrt(q));
+    };
+    // short edge length: 10th percentile over a sample of distance-constraint (else tet) edges (on a
+    // cloth grid the structural spacing, not the shear / bending lengths)
+    const int64_t ne = d->num_dist, nte = d->num_tets;
+    for (int64_t j = 0; j < ne; j += std::max<int64_t>(1, ne / 65536)) edge(d->dist_idx[2 * j], d->dist_idx[2 * j + 1]);
+    if (len.empty())
+        for (int64_t j = 0; j < nte; j += std::max<int64_t>(1, nte / 65536)) edge(d->tet_idx[4 * j], d->tet_idx[4 * j + 1]);
+    double h = 0;
+    if (!len.empty()) {
+        std::nth_element(len.begin(), len.begin() + len.size() / 10, len.end());
+        h = len[len.size() / 10];
+    }
+    if (const char *ev = getenv("DXPBD_MORTON_CELL")) h = atof(ev);   // 0: the extent / 2^21 cell (A/B)
+    morton_order(d->x_rest, d->num_vertices, h, vperm, d->vertex_scene);
+}
+
+// Distance constraints: greedy colors in user order (R1), then sorted by (color, owner tile) with
+// each constraint oriented (a < b) in internal ids; owner tile = a / kTileV; halo sets, foreign
+// lists and (when it fits) the TMA tile layout.
+void dist_topology(const dxpbd_scene_desc *d, int qf, DistTopo &T) {
+    const int V = d->num_vertices, E = d->num_dist;
+    T.V = V;
+    T.E = E;
+    vertex_order(d, T.vperm);
+    T.nt = (V + kTileV - 1) / kTileV;
+    if (!E) return;
+    std::vector<int32_t> vinv(V);
+    for (int i = 0; i < V; ++i) vinv[T.vperm[i]] = i;
+    const int nc = greedy_colors(E, 2, d->dist_idx, V, T.color);
+    if (nc < 0) throw Err{DXPBD_ERR_LIMIT, "distance coloring needs more than 256 colors"};
+    T.nc = nc;
+    const int nt = T.nt;
+    const size_t nkeys = (size_t)nc * nt;
+    std::vector<int2> ab(E);
+    std::vector<int64_t> cnt(nkeys + 1, 0);
+    std::vector<int32_t> key(E);
+    for (int j = 0; j < E; ++j) {
+        int a = vinv[d->dist_idx[2 * j]], b = vinv[d->dist_idx[2 * j + 1]];
+        if (a > b) std::swap(a, b);
+        ab[j] = make_int2(a, b);
+        key[j] = T.color[j] * nt + a / kTileV;
+        cnt[key[j] + 1]++;
+    }
+    for (size_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
+    T.seg.assign((size_t)nc * (nt + 1), 0);
+    T.dist_off.assign(nc + 1, 0);
+    for (int c = 0; c < nc; ++c) {
+        for (int t = 0; t <= nt; ++t) T.seg[(size_t)c * (nt + 1) + t] = (int)cnt[(size_t)c * nt + t];
+        T.dist_off[c] = (int)cnt[(size_t)c * nt];
+    }
+    T.dist_off[nc] = E;
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    T.perm.assign(E, 0);
+    for (int j = 0; j < E; ++j) T.perm[pos[key[j]]++] = j;
+    // within each (color, tile) segment order by internal a (vertex-disjoint within a color, so
+    // a is unique there): consecutive threads touch consecutive Morton vertices (no smem bank
+    // conflicts in the tiled matvec); the Gauss-Seidel result does not depend on this order.
+    for (size_t kk = 0; kk < nkeys; ++kk)
+        std::sort(T.perm.begin() + cnt[kk], T.perm.begin() + cnt[kk + 1], [&](int32_t x, int32_t y) { return ab[x].x < ab[y].x; });
+    // halo sets per tile (order-independent): the other endpoints of cross-tile constraints
+    T.halo.assign(nt, {});
+    for (int j = 0; j < E; ++j) {
+        int a = ab[j].x, bb = ab[j].y, ta = a / kTileV, tb = bb / kTileV;
+        if (ta != tb) { T.halo[ta].push_back(bb); T.halo[tb].push_back(a); }
+    }
+    for (int t = 0; t < nt; ++t) {
+        std::sort(T.halo[t].begin(), T.halo[t].end());
+        T.halo[t].erase(std::unique(T.halo[t].begin(), T.halo[t].end()), T.halo[t].end());
+    }
+    T.ab.resize(E);
+    for (int q = 0; q < E; ++q) T.ab[q] = ab[T.perm[q]];
+    const std::vector<int2> &ab_sorted = T.ab;
+    // foreign lists: constraints whose b lies in another tile than a, keyed (color, tile(b))
+    std::vector<int64_t> fc(nkeys + 1, 0);
+    for (int q = 0; q < E; ++q) {
+        int ta = ab_sorted[q].x / kTileV, tb = ab_sorted[q].y / kTileV;
+        if (ta != tb) fc[(size_t)T.color[T.perm[q]] * nt + tb + 1]++;
+    }
+    for (size_t k = 0; k < nkeys; ++k) fc[k + 1] += fc[k];
+    T.fseg.assign((size_t)nc * (nt + 1), 0);
+    for (int c = 0; c < nc; ++c)
+        for (int t = 0; t <= nt; ++t) T.fseg[(size_t)c * (nt + 1) + t] = (int)fc[(size_t)c * nt + t];
+    T.fidx.assign(std::max<int64_t>(fc[nkeys], 1), 0);
+    std::vector<int64_t> fp(fc.begin(), fc.end() - 1);
+    for (int q = 0; q < E; ++q) {
+        int ta = ab_sorted[q].x / kTileV, tb = ab_sorted[q].y / kTileV;
+        if (ta != tb) T.fidx[fp[(size_t)T.color[T.perm[q]] * nt + tb]++] = q;
+    }
+    for (size_t kk = 0; kk < nkeys; ++kk)
+        std::sort(T.fidx.begin() + fc[kk], T.fidx.begin() + fc[kk + 1], [&](int x, int y) { return ab_sorted[x].y < ab_sorted[y].y; });
+    T.n_foreign = fc[nkeys];
+    // CG-local tile structure for the TMA-staged kernels (kernels.cuh "TMA-staged")
+    int hmax = 0;
+    for (int t = 0; t < nt; ++t) {
+        T.halo_total += (int64_t)T.halo[t].size();
+        hmax = std::max(hmax, (int)T.halo[t].size());
+    }
+    T.hcap = (hmax + 31) / 32 * 32;
+    // combined (own + foreign) segments, tile-major: tile t's colors are contiguous
+    std::vector<int64_t> cbase((size_t)nt * nc + 1, 0);
+    int maxn = 0;
+    for (int t = 0; t < nt; ++t)
+        for (int c = 0; c < nc; ++c) {
+            const size_t kk = (size_t)c * nt + t;
+            const int64_t n = (cnt[kk + 1] - cnt[kk]) + (fc[kk + 1] - fc[kk]);
+            cbase[(size_t)t * nc + c + 1] = cbase[(size_t)t * nc + c] + n;
+            maxn = std::max<int>(maxn, (int)n);
+        }
+    T.capm = (maxn + 7) & ~7;
+    T.use_tma = hmax <= 4096 && nc <= kMaxColors && cbase.back() < (int64_t)INT32_MAX &&
+                tma_rhs_smem_bytes(T.hcap, T.capm, qf == 0) <= 200 * 1024;
+    if (!T.use_tma) return;
+    const int hc = T.hcap;
+    T.hpad.assign((size_t)nt * hc, -1);
+    for (int t = 0; t < nt; ++t) std::copy(T.halo[t].begin(), T.halo[t].end(), T.hpad.begin() + (size_t)t * hc);
+    T.tseg.resize((size_t)nt * nc);
+    for (size_t k = 0; k < (size_t)nt * nc; ++k) T.tseg[k] = make_int4((int)cbase[k], (int)cbase[k + 1], 0, 0);
+    T.ntot = cbase.back();
+    T.cpair.assign((size_t)T.ntot + 4, 0);
+    T.fposv.assign(E, -1);
+    T.tpos.assign(E, 0);
+    T.vslot.assign((size_t)nt * kTileV, 0);
+    T.hslot.assign((size_t)nt * hc, 0);
+    // per tile (independent, threaded): bank-balanced shared-memory slots, then conflict-free
+    // groups of every combined (tile, color) segment (tma_tile_layout)
+    auto work = [&](int t0, int t1) {
+        TileLayoutScratch ws;
+        for (int t = t0; t < t1; ++t)
+            tma_tile_layout(t, nc, nt, hc, T.halo[t], t * hc, cnt.data(), fc.data(), ab_sorted.data(), T.fidx.data(),
+                            cbase.data(), T.vslot.data(), T.hslot.data(), T.tpos.data(), T.fposv.data(), T.cpair.data(), ws);
+    };
+    const int nth = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int k = 0; k < nth; ++k) pool.emplace_back(work, (int)((int64_t)nt * k / nth), (int)((int64_t)nt * (k + 1) / nth));
+    for (auto &th : pool) th.join();
+}
 
 struct dxpbd_scene {
     int device = 0;
@@ -493,11 +662,6 @@ struct dxpbd_scene {
     DBuf<float4> d_Qt;                  // Q blocks in the TMA layout (own at tpos[j], foreign copy at fpos[j])
     DBuf<float2> d_Qt2b;                // general blocks (qf == 0): (yz, zz) in the same layout
     DBuf<uint16_t> d_vslot, d_hslot;   // tile-local shared-memory slots (own vertices, halo entries)
-    // host layout kept for partition groups (g_keep_host at create)
-    std::vector<int> seg_h;                 // [nc][nt + 1] sorted-constraint offsets per (color, tile)
-    std::vector<int2> ab_h;                 // sorted constraints: internal endpoints (a < b)
-    std::vector<std::vector<int>> halo_h;   // per tile: halo vertex ids (sorted)
-    std::vector<int> fpos_h;                // per sorted constraint: position of the b-tile copy in Qt, or -1
     DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
     // tets (color-sorted, internal vertex ids)
     DBuf<int4> t_idx;
@@ -546,6 +710,9 @@ struct dxpbd_scene {
     // colliders
     DBuf<float> sph, cap_c, cap_a, cap_r0, cap_L0, cap_Rb, cap_Lb, beta;
     DBuf<Collider> cols;
+    // batch of scenes: per-vertex scene id (internal order) and per-collider scene (-1: all)
+    int num_scenes = 1;
+    DBuf<int> vsc, csc;
 
     // trajectory
     int frames_done = -1;
@@ -649,7 +816,7 @@ void apply_shape(dxpbd_scene *s, cudaStream_t st) {
     if (!s->NC) return;
     k_shape_apply<<<nblk(s->NC), kBlock, 0, st>>>(s->NSH, s->NCAP, s->NS, s->sph.p, s->cap_c.p, s->cap_a.p,
                                                   s->cap_r0.p, s->cap_L0.p, s->cap_Rb.p, s->cap_Lb.p, s->beta.p,
-                                                  s->cols.p);
+                                                  s->cols.p, s->csc.p);
     DX_CHECK_CUDA(cudaGetLastError());
 }
 
@@ -889,14 +1056,14 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             float *eo = s->qc_cper > (size_t)6 * V ? slot + (size_t)6 * V : nullptr;
             ContactScratch cs{s->cc_lam.p, s->cc_T.p, s->cc_sig.p, s->cc_B.p, s->cc_e.p};
             LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd,
-                                                                                                   slot, eo, xo));
+                                                                                                   slot, eo, xo, s->vsc.p));
             ++launches;
         } else if (s->NC) {
             float at = s->coll_alpha * inv_dt2;
-            if (!rd && !wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
-            else if (!rd && wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
-            else if (rd && wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
-            else LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo));
+            if (!rd && !wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo, s->vsc.p));
+            else if (!rd && wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo, s->vsc.p));
+            else if (rd && wr) LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo, s->vsc.p));
+            else LAUNCH(DXPBD_K_CONTACT_PROJECT, k_contact_project<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, s->lam_c.p, xo, s->vsc.p));
             ++launches;
         }
     }
@@ -1018,10 +1185,10 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             float at = s->coll_alpha * inv_dt2;
             float *eo = want_ce ? (s->ec_w ? s->ec_w : s->ec.p) : nullptr;
             float *const Qcw = s->qc_w ? s->qc_w : s->Qc.p;
-            if (first && last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
-            else if (first) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
-            else if (last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
-            else LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x));
+            if (first && last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x, s->vsc.p));
+            else if (first) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<true, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x, s->vsc.p));
+            else if (last) LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, true><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x, s->vsc.p));
+            else LAUNCH(DXPBD_K_CONTACT_REPLAY, k_contact_replay<false, false><<<nblk(V), kBlock, 0, st>>>(V, s->NC, s->cols.p, s->h, at, cs, s->pd, Qcw, eo, x, s->vsc.p));
             ++launches;
         }
     }
@@ -1360,6 +1527,22 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         DX_REQUIRE(d->dist_idx[2 * j] != d->dist_idx[2 * j + 1], DXPBD_ERR_ARG, "degenerate distance constraint");
     for (int j = 0; j < 4 * d->num_tets; ++j)
         DX_REQUIRE(d->tet_idx[j] >= 0 && d->tet_idx[j] < V, DXPBD_ERR_ARG, "tet_idx out of range");
+    if (d->vertex_scene) {   // batch: scene ids in range, no constraint couples two scenes
+        DX_REQUIRE(d->num_scenes >= 1, DXPBD_ERR_ARG, "num_scenes >= 1 with vertex_scene");
+        for (int v = 0; v < V; ++v)
+            DX_REQUIRE(d->vertex_scene[v] >= 0 && d->vertex_scene[v] < d->num_scenes, DXPBD_ERR_ARG, "vertex_scene out of range");
+        for (int j = 0; j < d->num_dist; ++j)
+            DX_REQUIRE(d->vertex_scene[d->dist_idx[2 * j]] == d->vertex_scene[d->dist_idx[2 * j + 1]], DXPBD_ERR_ARG,
+                       "distance constraint couples two scenes");
+        for (int j = 0; j < d->num_tets; ++j)
+            for (int k = 1; k < 4; ++k)
+                DX_REQUIRE(d->vertex_scene[d->tet_idx[4 * j + k]] == d->vertex_scene[d->tet_idx[4 * j]], DXPBD_ERR_ARG,
+                           "tet couples two scenes");
+        if (d->collider_scene)
+            for (int c = 0; c < d->num_spheres + d->num_capsules; ++c)
+                DX_REQUIRE(d->collider_scene[c] >= -1 && d->collider_scene[c] < d->num_scenes, DXPBD_ERR_ARG,
+                           "collider_scene out of range");
+    }
     DX_CHECK_CUDA(cudaSetDevice(d->device));
     s = new dxpbd_scene();
     s->device = d->device;
@@ -1413,27 +1596,10 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
 
     cudaStream_t st = 0;
 
-    // vertex order: Morton order of the rest positions (host, create time)
-    {   // short edge length: 10th percentile over a sample of distance-constraint (else tet) edges (on a
-        // cloth grid the structural spacing, not the shear / bending lengths)
-        std::vector<double> len;
-        auto edge = [&](int a, int b) {
-            double q = 0;
-            for (int k = 0; k < 3; ++k) { const double u = (double)d->x_rest[3 * a + k] - d->x_rest[3 * b + k]; q += u * u; }
-            if (q > 0) len.push_back(std::sqrt(q));
-        };
-        const int64_t ne = d->num_dist, nte = d->num_tets;
-        for (int64_t j = 0; j < ne; j += std::max<int64_t>(1, ne / 65536)) edge(d->dist_idx[2 * j], d->dist_idx[2 * j + 1]);
-        if (len.empty())
-            for (int64_t j = 0; j < nte; j += std::max<int64_t>(1, nte / 65536)) edge(d->tet_idx[4 * j], d->tet_idx[4 * j + 1]);
-        double h = 0;
-        if (!len.empty()) {
-            std::nth_element(len.begin(), len.begin() + len.size() / 10, len.end());
-            h = len[len.size() / 10];
-        }
-        if (const char *ev = getenv("DXPBD_MORTON_CELL")) h = atof(ev);   // 0: the extent / 2^21 cell (A/B)
-        morton_order(d->x_rest, V, h, s->vperm_h);
-    }
+    // host topology: Morton vertex order, colors, constraint order, tiles (no GPU work)
+    DistTopo topo;
+    dist_topology(d, s->qf, topo);
+    s->vperm_h = topo.vperm;
     std::vector<int32_t> vinv(V);
     for (int i = 0; i < V; ++i) vinv[s->vperm_h[i]] = i;
     s->vperm.alloc(V);
@@ -1450,170 +1616,61 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, tmpu.p, s->vperm.p, xr3.p);
     DX_CHECK_CUDA(cudaStreamSynchronize(st));
 
-    // distance constraints: greedy colors in user order (R1), then sorted by (color, owner tile)
-    // with each constraint oriented (a < b) in internal ids; owner tile = a / kTileV.
+    // distance constraints: host topology (dist_topology), then device buffers
     if (s->E) {
         const int E = s->E;
-        int nc = greedy_colors(E, 2, d->dist_idx, V, s->dist_color_h);
-        if (nc < 0) throw Err{DXPBD_ERR_LIMIT, "distance coloring needs more than 256 colors"};
+        const int nc = topo.nc, nt = s->ntiles;
         s->n_dist_colors = nc;
-        const int nt = s->ntiles;
-        const size_t nkeys = (size_t)nc * nt;
-        std::vector<int2> ab(E);
-        std::vector<int64_t> cnt(nkeys + 1, 0);
-        std::vector<int32_t> key(E);
-        for (int j = 0; j < E; ++j) {
-            int a = vinv[d->dist_idx[2 * j]], b = vinv[d->dist_idx[2 * j + 1]];
-            if (a > b) std::swap(a, b);
-            ab[j] = make_int2(a, b);
-            key[j] = s->dist_color_h[j] * nt + a / kTileV;
-            cnt[key[j] + 1]++;
-        }
-        for (size_t k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
-        std::vector<int> seg((size_t)nc * (nt + 1));
-        s->dist_off.assign(nc + 1, 0);
-        for (int c = 0; c < nc; ++c) {
-            for (int t = 0; t <= nt; ++t) seg[(size_t)c * (nt + 1) + t] = (int)cnt[(size_t)c * nt + t];
-            s->dist_off[c] = (int)cnt[(size_t)c * nt];
-        }
-        s->dist_off[nc] = E;
-        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-        s->dist_perm_h.assign(E, 0);
-        std::vector<int2> ab_sorted(E);
-        for (int j = 0; j < E; ++j) {
-            int64_t q = pos[key[j]]++;
-            s->dist_perm_h[q] = j;
-        }
-        // within each (color, tile) segment order by internal a (vertex-disjoint within a color, so
-        // a is unique there): consecutive threads touch consecutive Morton vertices (no smem bank
-        // conflicts in the tiled matvec); the Gauss-Seidel result does not depend on this order.
-        for (size_t kk = 0; kk < nkeys; ++kk)
-            std::sort(s->dist_perm_h.begin() + cnt[kk], s->dist_perm_h.begin() + cnt[kk + 1],
-                      [&](int32_t x, int32_t y) { return ab[x].x < ab[y].x; });
-        // halo sets per tile (order-independent): the other endpoints of cross-tile constraints
-        std::vector<std::vector<int>> halo(nt);
-        for (int j = 0; j < E; ++j) {
-            int a = ab[j].x, bb = ab[j].y, ta = a / kTileV, tb = bb / kTileV;
-            if (ta != tb) { halo[ta].push_back(bb); halo[tb].push_back(a); }
-        }
-        for (int t = 0; t < nt; ++t) {
-            std::sort(halo[t].begin(), halo[t].end());
-            halo[t].erase(std::unique(halo[t].begin(), halo[t].end()), halo[t].end());
-        }
-        for (int q = 0; q < E; ++q) ab_sorted[q] = ab[s->dist_perm_h[q]];
+        s->dist_color_h = topo.color;
+        s->dist_perm_h = topo.perm;
+        s->dist_off = topo.dist_off;
+        const std::vector<int> &seg = topo.seg;
+        const std::vector<int2> &ab_sorted = topo.ab;
         s->d_seg.alloc(seg.size());
         upload(s->d_seg.p, seg.data(), sizeof(int) * seg.size(), DXPBD_MEM_HOST, st);
-        if (s->wave_on && s->iterations == 1 && !g_keep_host) build_wave_plan(s, seg, ab_sorted, d->x_rest, st);
-        // foreign lists: constraints whose b lies in another tile than a, keyed (color, tile(b))
-        {
-            std::vector<int64_t> fc(nkeys + 1, 0);
-            for (int q = 0; q < E; ++q) {
-                int ta = ab_sorted[q].x / kTileV, tb = ab_sorted[q].y / kTileV;
-                if (ta != tb) fc[(size_t)s->dist_color_h[s->dist_perm_h[q]] * nt + tb + 1]++;
-            }
-            for (size_t k = 0; k < nkeys; ++k) fc[k + 1] += fc[k];
-            std::vector<int> fseg((size_t)nc * (nt + 1));
-            for (int c = 0; c < nc; ++c)
-                for (int t = 0; t <= nt; ++t) fseg[(size_t)c * (nt + 1) + t] = (int)fc[(size_t)c * nt + t];
-            std::vector<int> fidx(std::max<int64_t>(fc[nkeys], 1));
-            std::vector<int64_t> fp(fc.begin(), fc.end() - 1);
-            for (int q = 0; q < E; ++q) {
-                int ta = ab_sorted[q].x / kTileV, tb = ab_sorted[q].y / kTileV;
-                if (ta != tb) fidx[fp[(size_t)s->dist_color_h[s->dist_perm_h[q]] * nt + tb]++] = q;
-            }
-            for (size_t kk = 0; kk < nkeys; ++kk)
-                std::sort(fidx.begin() + fc[kk], fidx.begin() + fc[kk + 1],
-                          [&](int x, int y) { return ab_sorted[x].y < ab_sorted[y].y; });
-            s->d_fseg.alloc(fseg.size());
-            upload(s->d_fseg.p, fseg.data(), sizeof(int) * fseg.size(), DXPBD_MEM_HOST, st);
-            s->n_foreign = fc[nkeys];
-            // CG-local tile structure for the TMA-staged kernels (kernels.cuh "TMA-staged")
-            std::vector<int> hoff(nt + 1, 0);
-            int hmax = 0;
-            for (int t = 0; t < nt; ++t) {
-                hoff[t + 1] = hoff[t] + (int)halo[t].size();
-                hmax = std::max(hmax, (int)halo[t].size());
-            }
-            s->hcap = (hmax + 31) / 32 * 32;
-            s->halo_total = hoff[nt];
-            // combined (own + foreign) segments, tile-major: tile t's colors are contiguous
-            std::vector<int64_t> cbase((size_t)nt * nc + 1, 0);
-            int maxn = 0;
-            for (int t = 0; t < nt; ++t)
-                for (int c = 0; c < nc; ++c) {
-                    const size_t kk = (size_t)c * nt + t;
-                    const int64_t n = (cnt[kk + 1] - cnt[kk]) + (fc[kk + 1] - fc[kk]);
-                    cbase[(size_t)t * nc + c + 1] = cbase[(size_t)t * nc + c] + n;
-                    maxn = std::max<int>(maxn, (int)n);
-                }
-            s->capm = (maxn + 7) & ~7;
-            s->use_tma = hmax <= 4096 && nc <= kMaxColors && cbase.back() < (int64_t)INT32_MAX &&
-                         tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0) <= 200 * 1024;
-            if (s->use_tma) {
-                const int hc = s->hcap;
-                std::vector<int> hpad((size_t)nt * hc, -1);
-                for (int t = 0; t < nt; ++t) std::copy(halo[t].begin(), halo[t].end(), hpad.begin() + (size_t)t * hc);
-                std::vector<int4> tseg((size_t)nt * nc);
-                for (size_t k = 0; k < (size_t)nt * nc; ++k) tseg[k] = make_int4((int)cbase[k], (int)cbase[k + 1], 0, 0);
-                const int64_t NTOT = cbase.back();
-                std::vector<uint32_t> cpair((size_t)NTOT + 4, 0);
-                std::vector<int> fposv(E, -1), tpos(E);
-                std::vector<uint16_t> vslot((size_t)nt * kTileV), hslot((size_t)nt * hc);
-                // per tile (independent, threaded): bank-balanced shared-memory slots, then
-                // conflict-free groups of every combined (tile, color) segment (tma_tile_layout)
-                auto work = [&](int t0, int t1) {
-                    TileLayoutScratch ws;
-                    for (int t = t0; t < t1; ++t)
-                        tma_tile_layout(t, nc, nt, hc, halo[t], t * hc, cnt.data(), fc.data(), ab_sorted.data(),
-                                        fidx.data(), cbase.data(), vslot.data(), hslot.data(), tpos.data(),
-                                        fposv.data(), cpair.data(), ws);
-                };
-                const int nth = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
-                std::vector<std::thread> pool;
-                for (int k = 0; k < nth; ++k) pool.emplace_back(work, (int)((int64_t)nt * k / nth), (int)((int64_t)nt * (k + 1) / nth));
-                for (auto &th : pool) th.join();
-                s->d_tseg.alloc(tseg.size());
-                upload(s->d_tseg.p, tseg.data(), sizeof(int4) * tseg.size(), DXPBD_MEM_HOST, st);
-                s->d_hpad.alloc(hpad.size());
-                upload(s->d_hpad.p, hpad.data(), sizeof(int) * hpad.size(), DXPBD_MEM_HOST, st);
-                s->d_vslot.alloc(vslot.size());
-                upload(s->d_vslot.p, vslot.data(), sizeof(uint16_t) * vslot.size(), DXPBD_MEM_HOST, st);
-                s->d_hslot.alloc(hslot.size());
-                upload(s->d_hslot.p, hslot.data(), sizeof(uint16_t) * hslot.size(), DXPBD_MEM_HOST, st);
-                s->d_cpair.alloc(cpair.size());
-                upload(s->d_cpair.p, cpair.data(), sizeof(uint32_t) * cpair.size(), DXPBD_MEM_HOST, st);
-                s->d_fpos.alloc(E);
-                upload(s->d_fpos.p, fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
-                if (g_keep_host) {
-                    s->seg_h = seg;
-                    s->ab_h = ab_sorted;
-                    s->halo_h = halo;
-                    s->fpos_h = fposv;
-                }
-                s->d_tpos.alloc(E);
-                upload(s->d_tpos.p, tpos.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
-                s->d_Qt.alloc((size_t)NTOT + 1);
-                if (s->qf == 0) s->d_Qt2b.alloc((size_t)NTOT + 2);
-                s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->qf == 0);
-                s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0);
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-                if (const char *ev = getenv("DXPBD_CGCG_MINB")) s->cgcg_minb = atoi(ev);
-                if (const char *ev = getenv("DXPBD_CG")) s->cgcg = std::string(ev) == "cgcg";
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
-                DX_CHECK_CUDA(cudaStreamSynchronize(st));
-            }
-            s->d_fidx.alloc(fidx.size());
-            upload(s->d_fidx.p, fidx.data(), sizeof(int) * fidx.size(), DXPBD_MEM_HOST, st);
-            std::vector<int4> fent(fidx.size());
-            for (size_t q = 0; q < fidx.size(); ++q)
-                fent[q] = make_int4(fidx[q], ab_sorted[fidx[q]].x, ab_sorted[fidx[q]].y, 0);
-            s->d_fent.alloc(fent.size());
-            upload(s->d_fent.p, fent.data(), sizeof(int4) * fent.size(), DXPBD_MEM_HOST, st);
-            DX_CHECK_CUDA(cudaStreamSynchronize(st));
+        if (s->wave_on && s->iterations == 1) build_wave_plan(s, seg, ab_sorted, d->x_rest, st);
+        s->d_fseg.alloc(topo.fseg.size());
+        upload(s->d_fseg.p, topo.fseg.data(), sizeof(int) * topo.fseg.size(), DXPBD_MEM_HOST, st);
+        s->n_foreign = topo.n_foreign;
+        s->hcap = topo.hcap;
+        s->halo_total = topo.halo_total;
+        s->capm = topo.capm;
+        s->use_tma = topo.use_tma;
+        (void)nt;
+        if (s->use_tma) {
+            s->d_tseg.alloc(topo.tseg.size());
+            upload(s->d_tseg.p, topo.tseg.data(), sizeof(int4) * topo.tseg.size(), DXPBD_MEM_HOST, st);
+            s->d_hpad.alloc(topo.hpad.size());
+            upload(s->d_hpad.p, topo.hpad.data(), sizeof(int) * topo.hpad.size(), DXPBD_MEM_HOST, st);
+            s->d_vslot.alloc(topo.vslot.size());
+            upload(s->d_vslot.p, topo.vslot.data(), sizeof(uint16_t) * topo.vslot.size(), DXPBD_MEM_HOST, st);
+            s->d_hslot.alloc(topo.hslot.size());
+            upload(s->d_hslot.p, topo.hslot.data(), sizeof(uint16_t) * topo.hslot.size(), DXPBD_MEM_HOST, st);
+            s->d_cpair.alloc(topo.cpair.size());
+            upload(s->d_cpair.p, topo.cpair.data(), sizeof(uint32_t) * topo.cpair.size(), DXPBD_MEM_HOST, st);
+            s->d_fpos.alloc(E);
+            upload(s->d_fpos.p, topo.fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
+            s->d_tpos.alloc(E);
+            upload(s->d_tpos.p, topo.tpos.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
+            s->d_Qt.alloc((size_t)topo.ntot + 1);
+            if (s->qf == 0) s->d_Qt2b.alloc((size_t)topo.ntot + 2);
+            s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->qf == 0);
+            s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0);
+            DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+            DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+            DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+            DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
+            if (const char *ev = getenv("DXPBD_CGCG_MINB")) s->cgcg_minb = atoi(ev);
+            if (const char *ev = getenv("DXPBD_CG")) s->cgcg = std::string(ev) == "cgcg";
+            DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
         }
+        s->d_fidx.alloc(topo.fidx.size());
+        upload(s->d_fidx.p, topo.fidx.data(), sizeof(int) * topo.fidx.size(), DXPBD_MEM_HOST, st);
+        std::vector<int4> fent(topo.fidx.size());
+        for (size_t q = 0; q < topo.fidx.size(); ++q)
+            fent[q] = make_int4(topo.fidx[q], ab_sorted[topo.fidx[q]].x, ab_sorted[topo.fidx[q]].y, 0);
+        s->d_fent.alloc(fent.size());
+        upload(s->d_fent.p, fent.data(), sizeof(int4) * fent.size(), DXPBD_MEM_HOST, st);
         DBuf<float> alpha_u;
         alpha_u.alloc(E);
         upload(alpha_u.p, d->dist_compliance, sizeof(float) * E, DXPBD_MEM_HOST, st);
@@ -1687,7 +1744,18 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
             }
         }
         s->cols.alloc(s->NC);
+        if (d->vertex_scene && d->collider_scene) {
+            s->csc.alloc(s->NC);
+            upload(s->csc.p, d->collider_scene, sizeof(int32_t) * s->NC, DXPBD_MEM_HOST, st);
+        }
         apply_shape(s, st);
+    }
+    if (d->vertex_scene) {   // per-vertex scene ids in internal order
+        s->num_scenes = d->num_scenes;
+        std::vector<int32_t> vs(V);
+        for (int i = 0; i < V; ++i) vs[i] = d->vertex_scene[s->vperm_h[i]];
+        s->vsc.alloc(V);
+        upload(s->vsc.p, vs.data(), sizeof(int32_t) * V, DXPBD_MEM_HOST, st);
     }
     // trajectory storage
     const size_t nstates = (size_t)s->max_frames * s->substeps + 1;

@@ -17,8 +17,13 @@ struct Collider {
     float r;    // radius
     float L;    // segment length (capsule)
     int type;
-    int pad;
+    int scene;  // scene of a batch the collider acts on (-1: every scene)
 };
+
+// collider c acts on vertex v (batches: the vertex's scene; vsc null: one scene)
+DX_INLINE bool acts_on(const Collider &cd, const int *__restrict__ vsc, int v) {
+    return cd.scene < 0 || !vsc || vsc[v] == cd.scene;
+}
 
 // ============================================================================ predict
 // x~ = x_n + dt v_n + dt^2 (g + w f)  for free vertices, x~ = x_n for pinned ones
@@ -357,7 +362,7 @@ DX_INLINE void contact_apply(double4 &p, const ContactCore &o) {
 template <bool READ_LAM, bool WRITE_LAM>
 __global__ void __launch_bounds__(kBlock) k_contact_project(int V, int NC, const Collider *__restrict__ cols,
                                                             float h, float at, float *__restrict__ lam,
-                                                            double4 *__restrict__ x) {
+                                                            double4 *__restrict__ x, const int *__restrict__ vsc = nullptr) {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
     double4 p = x[v];
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(kBlock) k_contact_project(int V, int NC, const
         Collider cd = cols[c];
         float lam0 = READ_LAM ? lam[(size_t)c * V + v] : 0.f;
         ContactCore o;
-        if (contact_core(p, cd, h, at, lam0, o)) {
+        if (acts_on(cd, vsc, v) && contact_core(p, cd, h, at, lam0, o)) {
             if (WRITE_LAM) lam[(size_t)c * V + v] = radd(lam0, o.dl);
             contact_apply(p, o);
             moved = true;
@@ -441,7 +446,7 @@ template <bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kBlock) k_contact_replay(int V, int NC, const Collider *__restrict__ cols,
                                                            float h, float at, ContactScratch sc, int pd,
                                                            float *__restrict__ Qc, float *__restrict__ eout,
-                                                           double4 *__restrict__ x) {
+                                                           double4 *__restrict__ x, const int *__restrict__ vsc = nullptr) {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
     double4 p = x[v];
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(kBlock) k_contact_replay(int V, int NC, const 
                      sc.B[5 * NV + pr]};
         }
         ContactCore o;
-        if (contact_core(p, cd, h, at, lam0, o)) {
+        if (acts_on(cd, vsc, v) && contact_core(p, cd, h, at, lam0, o)) {
             float il = (float)(1.0 / o.len);
             float3 n = o.n;
             contact_deriv(cd, o, at, il, n, sig, B, T, e);

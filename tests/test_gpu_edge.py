@@ -310,3 +310,63 @@ def test_pcg_graph_reports_nonconvergence(monkeypatch):
         api.dxpbd_forward(sc, s.x0, s.v0, None, 2)
         with pytest.raises(api.DxpbdError, match="converge"):
             api.dxpbd_backward(sc, [2], s.targets)
+
+
+def _batch_compare(scenes, grads, frames, per_collider=None):
+    """Run each scene alone and all of them as one batch handle; positions per scene bit-identical
+    (same colors, same per-vertex collider order, same fp64 arithmetic), gradients per scene within
+    the PCG tolerance (the batch solves one block-diagonal system with one global residual test)."""
+    api = _api()
+    solo = [_run_all(s, grads, frames) for s in scenes]
+    kw = api.batch_scene_kwargs(scenes)
+    sc = api.dxpbd_create(**kw, max_frames=frames, grad_flags=api.flags(*grads))
+    x0, v0, forces, kf, tg = api.batch_inputs(scenes, frames)
+    api.dxpbd_forward(sc, x0, v0, forces, frames)
+    xb = [api.dxpbd_positions(sc, f) for f in range(frames + 1)]
+    kf = [k for k in kf.tolist() if k <= frames]
+    loss = api.dxpbd_backward(sc, kf, tg[: len(kf)])
+    assert abs(loss - sum(r[1] for r in solo)) <= 1e-5 * abs(loss)
+    for f in range(frames + 1):
+        for b, xs in enumerate(api.batch_split(xb[f], scenes)):
+            np.testing.assert_array_equal(xs, solo[b][0][f], err_msg=f"scene {b} frame {f}")
+    for k in grads:
+        g = api.dxpbd_grads(sc, k)
+        if k in ("x0", "v0"):
+            parts = api.batch_split(g, scenes)
+        elif k == "compliance":
+            parts = np.split(g, np.cumsum([len(s.dist_idx) for s in scenes])[:-1])
+        else:   # per collider / coefficient families
+            parts = np.split(g, np.cumsum(per_collider)[:-1])
+        for b, gp in enumerate(parts):
+            ref = np.asarray(solo[b][2][k]).ravel()
+            assert rel_l2(np.ravel(gp), ref) < 2e-4, (k, b, rel_l2(np.ravel(gp), ref))
+
+
+def test_batch_of_cloth_sphere_scenes_matches_individual():
+    """configs[1]-shaped batch: three cloths of different sizes, each dropped on its own sphere."""
+    scenes = []
+    for b, n in enumerate((20, 24, 16)):
+        s = f32(medium_cloth(n=n, frames=4, seed=11 + b))
+        sph = np.asarray(s.spheres, np.float64).copy()
+        sph[:, 3] *= 1.0 + 0.1 * b                      # a different sphere per scene
+        scenes.append(f32(s.replace(spheres=sph)))
+    _batch_compare(scenes, ("compliance", "x0", "sphere"), 4, per_collider=[4, 4, 4])
+
+
+def test_batch_of_garments_shape_gradients_match_individual():
+    """configs[3]-shaped batch: two garments on their own 12-capsule bodies with their own shape
+    vectors (block-diagonal shape bases), shape gradients per scene."""
+    from tests.garment_case import garment_case
+    a = garment_case(48, 32, warm_frames=20, frames=3, seed=3)
+    b = garment_case(48, 32, warm_frames=20, frames=3, seed=5)
+    _batch_compare([a, b], ("shape", "x0"), 3, per_collider=[len(a.shape_beta), len(b.shape_beta)])
+
+
+def test_batch_rejects_coupled_scenes():
+    api = _api()
+    s = f32(tiny_cloth(n=4, frames=1))
+    kw = api.batch_scene_kwargs([s, s])
+    kw["dist_idx"] = kw["dist_idx"].copy()
+    kw["dist_idx"][0, 1] = s.num_vertices + 1          # a constraint across scenes 0 and 1
+    with pytest.raises(api.DxpbdError, match="scenes"):
+        api.dxpbd_create(**kw, max_frames=1)

@@ -1,40 +1,93 @@
-"""Vertex-partitioned domain decomposition (paper_2301_01396_b200.partition) on CPU: plan
-invariants, and a world_size-2 gloo execution of the partitioned colored Gauss-Seidel substep and
-of the partitioned PCG matvec that must reproduce the global (single-device) computation.  The
-per-rank compute is the oracle's (test infrastructure), the plan and the exchanges are the
-product's host logic."""
+"""Vertex-partitioned domain decomposition on CPU with the PRODUCT's planner: the host-only C call
+`dxpbd_partition_plan` (the same `partition_plan` / `dist_topology` code that `dxpbd_group_create`
+and `dxpbd_group_create_dist` build their exchange lists from, include/dxpbd.h).  Plan invariants,
+and a world_size-2 gloo execution of the partitioned colored Gauss-Seidel substep and of the
+partitioned PCG matvec driven by those lists, which must reproduce the global (single-device)
+computation.  The per-rank compute is the oracle's (test infrastructure); the plan and the
+exchange pattern are the product's."""
 import os
 import socket
 import sys
 
 import numpy as np
-import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _scene():
     from synth import large_cloth, as_float32_exact
-    return as_float32_exact(large_cloth(n=24, frames=1, substeps=2, iterations=2, side=1.0, key_frames=(1,)))
+    # 48 x 48 = 2304 vertices = 4.5 Morton tiles of 512: a ragged last tile
+    return as_float32_exact(large_cloth(n=48, frames=1, substeps=2, iterations=1, side=1.0, key_frames=(1,)))
+
+
+def _plan(s, world, rank):
+    from paper_2301_01396_b200 import api
+    return api.dxpbd_partition_plan(**api.scene_kwargs(s), num_parts=world, rank=rank, max_frames=1)
+
+
+def _internal(s, pl):
+    """Constraint endpoints in internal (Morton) ids, oriented a < b, and the owning rank of each
+    internal vertex (tile ranges [t0, t1) of every rank)."""
+    vinv = np.empty_like(pl["vperm"])
+    vinv[pl["vperm"]] = np.arange(len(pl["vperm"]))
+    ab = np.sort(vinv[np.asarray(s.dist_idx)], axis=1)
+    return vinv, ab
 
 
 def test_plan_invariants():
     from oracle import greedy_color
-    from paper_2301_01396_b200.partition import plan, morton_order
     s = _scene()
     col = greedy_color(s.dist_idx, s.num_vertices)
+    V, tv = s.num_vertices, 512
     for world in (1, 2, 3, 4):
-        P = plan(s.x_rest, s.dist_idx, col, world)
-        owned = np.concatenate([p.owned for p in P])
-        assert sorted(owned.tolist()) == list(range(s.num_vertices))
-        cons = np.concatenate([c for p in P for c in p.cons])
-        assert sorted(cons.tolist()) == list(range(len(s.dist_idx)))      # each constraint exactly once
-        for p in P:
-            assert not set(p.ghosts.tolist()) & set(p.owned.tolist())
-            for (c, dst), v in p.send.items():
-                np.testing.assert_array_equal(P[dst].recv[(c, p.rank)], v)
-    perm = morton_order(s.x_rest)
-    assert sorted(perm.tolist()) == list(range(s.num_vertices))
+        plans = [_plan(s, world, r) for r in range(world)]
+        pl0 = plans[0]
+        assert sorted(pl0["vperm"].tolist()) == list(range(V))                  # a permutation
+        assert pl0["colors"] == col.max() + 1                                    # the same greedy colors (R1)
+        assert [p["t0"] for p in plans] == sorted(p["t0"] for p in plans)
+        assert plans[0]["t0"] == 0 and plans[-1]["t1"] == pl0["tiles"]
+        for a, b in zip(plans, plans[1:]):
+            assert a["t1"] == b["t0"]                                            # contiguous tile ranges
+        vinv, ab = _internal(s, pl0)
+        owner = np.empty(V, np.int64)
+        for r, p in enumerate(plans):
+            owner[p["t0"] * tv: min(p["t1"] * tv, V)] = r
+        # tile halos: the other endpoints of cross-tile constraints
+        halo = {}
+        cross = ab[:, 0] // tv != ab[:, 1] // tv
+        for a_, b_ in ab[cross]:
+            halo.setdefault(a_ // tv, set()).add(b_)
+            halo.setdefault(b_ // tv, set()).add(a_)
+        for r, p in enumerate(plans):
+            held = set(np.nonzero(owner == r)[0].tolist())
+            myh = set()
+            for t in range(p["t0"], p["t1"]):
+                myh |= {v for v in halo.get(t, ()) if owner[v] != r}
+            held |= myh
+            for q, other in enumerate(plans):
+                for k in list(range(p["colors"])) + ["halo", "blocks"]:
+                    # what r sends to q is exactly what q expects from r
+                    np.testing.assert_array_equal(p["send"][k][q], other["recv"][k][r])
+                if q == r:
+                    continue
+                # per color: every endpoint of r's constraints of that color held by q is sent to q
+                for c in range(p["colors"]):
+                    mine = (col == c) & (owner[ab[:, 0]] == r)
+                    need = {v for v in ab[mine].ravel().tolist() if owner[v] == q or v in _held_halo(plans[q], owner, halo, q)}
+                    assert set(p["send"][c][q].tolist()) == need
+                # halo: r's own vertices in q's tile halos
+                assert set(p["send"]["halo"][q].tolist()) == {v for v in _held_halo(plans[q], owner, halo, q) if owner[v] == r}
+                # blocks: one b-tile copy per constraint owned by r whose b lies in q
+                nb = int(((owner[ab[:, 0]] == r) & (owner[ab[:, 1]] == q) & cross).sum())
+                assert len(p["send"]["blocks"][q]) == nb
+            assert set().union(*[set(p["recv"]["halo"][q].tolist()) for q in range(world)]) == myh
+
+
+def _held_halo(p, owner, halo, q):
+    out = set()
+    for t in range(p["t0"], p["t1"]):
+        out |= {v for v in halo.get(t, ()) if owner[v] != q}
+    return out
 
 
 def _free_port():
@@ -43,18 +96,18 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _exchange(dist, P, key_send, key_recv, x, world):
-    """Point-to-point exchange of vertex rows: send x[ids] for every (key, dst) and overwrite
-    x[ids] with what (key, src) sends; neighbours only."""
+def _exchange(dist, send, recv, x, world, rank):
+    """Point-to-point exchange of vertex rows (user ids): send x[ids] to every peer with a list and
+    overwrite x[ids] with what each peer sends."""
     import torch
     reqs = []
     for dst in range(world):
-        ids = key_send(dst)
-        if ids is not None:
+        ids = send.get(dst)
+        if dst != rank and ids is not None and len(ids):
             reqs.append(dist.isend(torch.as_tensor(x[ids]), dst))
     for src in range(world):
-        ids = key_recv(src)
-        if ids is not None:
+        ids = recv.get(src)
+        if src != rank and ids is not None and len(ids):
             buf = torch.empty((len(ids), 3), dtype=torch.float64)
             dist.recv(buf, src)
             x[ids] = buf.numpy()
@@ -65,60 +118,57 @@ def _exchange(dist, P, key_send, key_recv, x, world):
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     sys.path.insert(0, ROOT)
-    import torch
     import torch.distributed as dist
     from oracle import OracleModel
-    from paper_2301_01396_b200.partition import plan
     dist.init_process_group("gloo", init_method="env://")
     s = _scene()
     m = OracleModel(s)
-    P = plan(s.x_rest, s.dist_idx, m.dist_color, world)[rank]
-    held = np.concatenate([P.owned, P.ghosts])
-    # ---- partitioned forward substeps (R1 sweep, exchange after every color)
+    pl = _plan(s, world, rank)
+    vp = pl["vperm"]                                  # internal -> user
+    vinv, ab = _internal(s, pl)
+    tv = pl["tile_v"]
+    v0, v1 = pl["t0"] * tv, min(pl["t1"] * tv, s.num_vertices)
+    owned = vp[v0:v1]                                 # user ids of the owned vertices
+    mine = np.nonzero((ab[:, 0] >= v0) & (ab[:, 0] < v1))[0]          # constraints owned (lower endpoint)
+    user = lambda lists: {k: vp[v] for k, v in lists.items()}          # noqa: E731
+    # ---- partitioned forward substeps (R1 sweep, exchange along the plan's lists after every color)
     x = s.x0.copy()
     v = s.v0.copy()
-    dt = m.dt
-    for n in range(s.num_steps):
+    for _n in range(s.num_steps):
         xn = x.copy()
         x = m.predict(xn, v, s.forces[0])
         lam = np.zeros(m.E)
-        for _it in range(s.iterations):
-            for c, grp in enumerate(P.cons):
-                if len(grp):
-                    m._project(x, m.dist_idx[grp], m.ev_dist(x, grp), m.at_dist[grp][:, None], lam, None, "dist", grp)
-                _exchange(dist, P, lambda d, c=c: P.send.get((c, d)), lambda r_, c=c: P.recv.get((c, r_)), x, world)
-        v = (x - xn) / dt
-    # ---- partitioned PCG matvec of the global replayed system: q = (M + Sum Q_j) p
+        for c in range(pl["colors"]):
+            grp = mine[m.dist_color[mine] == c]
+            if len(grp):
+                m._project(x, m.dist_idx[grp], m.ev_dist(x, grp), m.at_dist[grp][:, None], lam, None, "dist", grp)
+            _exchange(dist, user(pl["send"][c]), user(pl["recv"][c]), x, world, rank)
+        v = (x - xn) / m.dt
+    # ---- partitioned PCG matvec of the global replayed system, q = (M + Sum Q_j) p, over owned rows:
+    # every constraint touching an owned vertex, with the neighbours' p from the plan's halo lists
     xs_g = m.simulate(s.x0, s.v0, s.forces, 1)
     _, _, rec = m.step(xs_g[0], s.v0, s.forces[0], record=True)
-    Qb = m.blocks(rec)["dist"]                       # (E,6,6) per-constraint blocks
+    Qb = m.blocks(rec)["dist"]
     p = np.random.default_rng(5).standard_normal(x.shape)
-    pl = np.zeros_like(p)
-    pl[P.owned] = p[P.owned]                         # only owned values are known locally
-    _exchange(dist, P, lambda d: P.halo_send.get(d), lambda r_: P.halo_recv.get(r_), pl, world)
+    pl_p = np.zeros_like(p)
+    pl_p[owned] = p[owned]                            # only owned values are known locally
+    _exchange(dist, user(pl["send"]["halo"]), user(pl["recv"]["halo"]), pl_p, world, rank)
+    is_owned = np.zeros(s.num_vertices, bool)
+    is_owned[owned] = True
+    touch = np.nonzero(is_owned[m.dist_idx[:, 0]] | is_owned[m.dist_idx[:, 1]])[0]
+    st = m.dist_idx[touch]
+    dq = np.einsum("nij,nj->ni", Qb[touch], pl_p[st].reshape(len(touch), 6)).reshape(len(touch), 2, 3)
     ql = np.zeros_like(p)
-    ql[P.owned] = (m.m[:, None] * pl)[P.owned]
-    mine = np.concatenate(P.cons)
-    st = m.dist_idx[mine]
-    dq = np.einsum("nij,nj->ni", Qb[mine], pl[st].reshape(len(mine), 6)).reshape(len(mine), 2, 3)
+    ql[owned] = (m.m[:, None] * pl_p)[owned]
     contrib = np.zeros_like(p)
     np.add.at(contrib, st[:, 0], dq[:, 0])
     np.add.at(contrib, st[:, 1], dq[:, 1])
-    # contributions to ghost vertices go to their owners (accumulate)
-    import torch as _t
-    reqs = []
-    for dst, ids in P.halo_recv.items():             # my ghosts are owned by dst
-        reqs.append(dist.isend(_t.as_tensor(contrib[ids]), dst))
-    for src, ids in P.halo_send.items():             # src mirrors my owned vertices
-        buf = _t.empty((len(ids), 3), dtype=_t.float64)
-        dist.recv(buf, src)
-        contrib[ids] += buf.numpy()
-    for r_ in reqs:
-        r_.wait()
-    ql[P.owned] += contrib[P.owned]
+    ql[owned] += contrib[owned]
     ql[~m.free] = 0.0
+    held = np.nonzero(is_owned | np.isin(np.arange(s.num_vertices), vp[np.concatenate(
+        [pl["recv"]["halo"][r] for r in range(world)])]))[0]
     dist.barrier()
-    q.put(dict(rank=rank, held=held, x=x[held], owned=P.owned, q=ql[P.owned]))
+    q.put(dict(rank=rank, x=x[owned], owned=owned, q=ql[owned], held=held, xh=x[held]))
     dist.destroy_process_group()
 
 
@@ -139,9 +189,9 @@ def test_partitioned_sweep_and_matvec_world2():
         pr.join(timeout=60)
         assert pr.exitcode == 0
     for r in res:
-        # every vertex a rank holds (owned and ghost) equals the global sweep bit for bit
-        np.testing.assert_array_equal(r["x"], xs[-1][r["held"]])
-    # global matvec
+        # owned vertices and every halo vertex a rank holds equal the global sweep bit for bit
+        np.testing.assert_array_equal(r["x"], xs[-1][r["owned"]])
+        np.testing.assert_array_equal(r["xh"], xs[-1][r["held"]])
     _, _, rec = m.step(xs[0], s.v0, s.forces[0], record=True)
     A = m.system_matrix(m.blocks(rec)).toarray()
     p = np.random.default_rng(5).standard_normal((m.V, 3))

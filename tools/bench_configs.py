@@ -92,9 +92,59 @@ def run(name, make, grads):
     del sc
 
 
+def run_batch(name, make, grads, B):
+    """B independent seeded copies of a config in ONE handle (include/dxpbd.h vertex_scene): one
+    launch sequence serves every scene, so launch-bound small configs gain throughput ~B."""
+    scenes = [as_float32_exact(make(seed)) for seed in range(1, B + 1)]
+    dev = "cuda:0"
+    t = lambda a: None if a is None else torch.as_tensor(np.asarray(a, np.float32), device=dev)  # noqa: E731
+    kw = api.batch_scene_kwargs(scenes)
+    s0 = scenes[0]
+    t0 = time.perf_counter()
+    sc = api.dxpbd_create(**kw, max_frames=s0.frames, grad_flags=api.flags(*grads), cg_max_iter=2000)
+    t_create = time.perf_counter() - t0
+    x0, v0, f, kf, tg = api.batch_inputs(scenes, s0.frames)
+    x0, v0, f, tg = t(x0), t(v0), t(f), t(tg)
+    fwds, tots = [], []
+    for _ in range(REPEAT):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize()
+        ev[0].record()
+        api.dxpbd_forward(sc, x0, v0, f, s0.frames)
+        ev[1].record()
+        loss = api.dxpbd_backward(sc, kf, tg)
+        for g in grads:
+            api.dxpbd_grads(sc, g)
+        ev[2].record()
+        torch.cuda.synchronize()
+        fwds.append(ev[0].elapsed_time(ev[1]))
+        tots.append(ev[0].elapsed_time(ev[2]))
+    st = api.dxpbd_stats(sc)
+    k = int(np.argmin(tots))
+    N = s0.frames * s0.substeps
+    E = sum(len(s.dist_idx) for s in scenes)
+    line = dict(config=name, batch=B, vertices=sum(s.num_vertices for s in scenes), constraints=E,
+                frames=s0.frames, substeps=s0.substeps, grads=list(grads), ms_forward=fwds[k],
+                ms_forward_adjoint=tots[k], ms_per_substep_fwd=fwds[k] / N, ms_per_substep_fwd_adjoint=tots[k] / N,
+                ms_per_scene_substep_fwd_adjoint=tots[k] / N / B,
+                constraint_solves_per_s=E * N / (tots[k] * 1e-3),
+                cg_iters_per_substep=st["cg_iters_total"] / max(st["solves"], 1), worst_relres=st["worst_relres"],
+                tma_path=st["tma"], loss=loss, create_s=t_create, passes=REPEAT, ms_forward_adjoint_all=tots)
+    print(json.dumps(line), flush=True)
+    del sc
+
+
+BATCHES = {
+    "b0": ("configs[0] tiny_cloth 16x16 x64 batch", lambda seed: tiny_cloth(seed=seed), ("compliance", "v0"), 64),
+    "b1": ("configs[1] medium_cloth 256x256 + sphere x8 batch", lambda seed: medium_cloth(seed=seed), ("compliance", "x0"), 8),
+}
+
 REPEAT = 3
 
 if __name__ == "__main__":
-    which = [int(a) for a in sys.argv[1:]] or range(len(CASES))
-    for i in which:
-        run(*CASES[i])
+    which = sys.argv[1:] or [str(i) for i in range(len(CASES))]
+    for w in which:
+        if w in BATCHES:
+            run_batch(*BATCHES[w])
+        else:
+            run(*CASES[int(w)])
