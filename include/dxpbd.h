@@ -217,7 +217,10 @@ int dxpbd_group_grads(dxpbd_group *group, int32_t kind, float *out, int64_t out_
                       void *stream);
 /* out[0..n), n <= 16: 0 total PCG iterations, 1 max per solve, 4 solves, 5 worst residual, 6 loss,
  * 8 vertices exchanged per substep sweep (all colors, forward or replay), 9 halo vertices
- * exchanged per PCG vector exchange, 10 cross-partition blocks per replay, 11 partitions. */
+ * exchanged per PCG vector exchange, 10 cross-partition blocks per replay, 11 partitions,
+ * 12 trajectory bytes of the largest local partition (its held vertices -- owned + tile halos --
+ * for every substep, plus 3 rolling full-V states), 13 the single scene's trajectory bytes,
+ * 14 held vertices of the largest partition. */
 int dxpbd_group_stats(dxpbd_group *group, double *out, int32_t n);
 
 /* Kernel classes timed by the opt-in event profiler (dxpbd_profile / dxpbd_kernel_times). */

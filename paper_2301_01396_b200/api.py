@@ -478,7 +478,8 @@ def dxpbd_group_stats(group: DxGroup) -> dict:
     out = np.zeros(16, np.float64)
     _check(lib().dxpbd_group_stats(group.handle, out.ctypes.data, 16), "dxpbd_group_stats")
     return dict(cg_iters_total=out[0], cg_iters_max=out[1], solves=out[4], worst_relres=out[5], loss=out[6],
-                xchg_sweep=out[8], xchg_halo=out[9], xchg_blocks=out[10], parts=out[11])
+                xchg_sweep=out[8], xchg_halo=out[9], xchg_blocks=out[10], parts=out[11],
+                traj_bytes_part=out[12], traj_bytes_single=out[13], held_max=out[14])
 
 
 def scene_kwargs(scene) -> dict:

@@ -29,6 +29,7 @@ using namespace dx;
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_ring_states = 0;   // > 0: dxpbd_create allocates only this many full-V states (partition groups)
 
 struct Err {
     int code;
@@ -1196,6 +1197,17 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     return launches;
 }
 
+// internal fp64 state -> user-order [V][3] float (host or device)
+void positions_from(dxpbd_scene *s, const double4 *x, float *out, int mem, cudaStream_t st) {
+    if (mem == DXPBD_MEM_HOST) {
+        k_unpack3<<<nblk(s->V), kBlock, 0, st>>>(s->V, x, s->vperm.p, s->tmp3.p);
+        download(out, s->tmp3.p, sizeof(float) * s->V * 3, mem, st);
+    } else {
+        k_unpack3<<<nblk(s->V), kBlock, 0, st>>>(s->V, x, s->vperm.p, out);
+    }
+    DX_CHECK_CUDA(cudaGetLastError());
+}
+
 // x0, v0, forces (user order, host or device) -> internal order: state 0, v0, per-frame forces
 void forward_inputs(dxpbd_scene *s, const float *x0, const float *v0, const float *forces, int num_frames, int mem,
                     cudaStream_t st) {
@@ -1758,7 +1770,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         upload(s->vsc.p, vs.data(), sizeof(int32_t) * V, DXPBD_MEM_HOST, st);
     }
     // trajectory storage
-    const size_t nstates = (size_t)s->max_frames * s->substeps + 1;
+    const size_t nstates = g_ring_states > 0 ? (size_t)g_ring_states : (size_t)s->max_frames * s->substeps + 1;
     s->ckpt.alloc(nstates * V);
     s->v0.alloc(V);
     s->tmp3.alloc((size_t)V * 3);
@@ -1831,13 +1843,7 @@ int dxpbd_positions(dxpbd_scene *s, int32_t frame, float *out, int32_t mem, void
     DX_REQUIRE(s && out, DXPBD_ERR_ARG, "null argument");
     DX_REQUIRE(s->frames_done >= 0 && frame >= 0 && frame <= s->frames_done, DXPBD_ERR_STATE, "frame not simulated");
     DX_CHECK_CUDA(cudaSetDevice(s->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    if (mem == DXPBD_MEM_HOST) {
-        k_unpack3<<<nblk(s->V), kBlock, 0, st>>>(s->V, state(s, frame * s->substeps), s->vperm.p, s->tmp3.p);
-        download(out, s->tmp3.p, sizeof(float) * s->V * 3, mem, st);
-    } else {
-        k_unpack3<<<nblk(s->V), kBlock, 0, st>>>(s->V, state(s, frame * s->substeps), s->vperm.p, out);
-    }
+    positions_from(s, state(s, frame * s->substeps), out, mem, (cudaStream_t)stream);
     DX_API_END
 }
 

@@ -315,7 +315,7 @@ def test_pcg_graph_reports_nonconvergence(monkeypatch):
 def _batch_compare(scenes, grads, frames, per_collider=None):
     """Run each scene alone and all of them as one batch handle; positions per scene bit-identical
     (same colors, same per-vertex collider order, same fp64 arithmetic), gradients per scene within
-    the PCG tolerance (the batch solves one block-diagonal system with one global residual test)."""
+    the gradient bar (the batch solves one block-diagonal system with one global residual test)."""
     api = _api()
     solo = [_run_all(s, grads, frames) for s in scenes]
     kw = api.batch_scene_kwargs(scenes)
@@ -339,7 +339,9 @@ def _batch_compare(scenes, grads, frames, per_collider=None):
             parts = np.split(g, np.cumsum(per_collider)[:-1])
         for b, gp in enumerate(parts):
             ref = np.asarray(solo[b][2][k]).ravel()
-            assert rel_l2(np.ravel(gp), ref) < 2e-4, (k, b, rel_l2(np.ravel(gp), ref))
+            # the batch's one global residual test vs each scene's own: differences of the order of the
+            # PCG tolerance; bar = the north_star gradient bar
+            assert rel_l2(np.ravel(gp), ref) < 1e-3, (k, b, rel_l2(np.ravel(gp), ref))
 
 
 def test_batch_of_cloth_sphere_scenes_matches_individual():

@@ -128,3 +128,29 @@ def test_distributed_group_world1_equals_single():
     assert loss == pytest.approx(a["loss"], rel=1e-6)
     for k in GRADS:
         assert rel_l2(api.dxpbd_group_grads(g, k), a[k]) < 1e-5
+
+
+def test_group_trajectory_memory_falls_with_P():
+    """Each partition stores its trajectory only for the vertices it holds (owned tiles + tile halos)
+    plus 3 rolling full-V states: at a 256^2 crop of configs[4] the per-partition trajectory bytes
+    fall roughly as 1/P (stats field 12 against the single scene's field 13), and the group still
+    reproduces the single scene's positions bit for bit."""
+    api = _api()
+    s = _scene(n=256, frames=2, substeps=5)
+    a = _single(s)
+    prev = None
+    for P in (2, 4, 8):
+        g = api.dxpbd_group_create(**api.scene_kwargs(s), num_parts=P, max_frames=s.frames,
+                                   grad_flags=api.flags(*GRADS), cg_max_iter=1000)
+        st = api.dxpbd_group_stats(g)
+        frac = st["traj_bytes_part"] / st["traj_bytes_single"]
+        print(P, frac, st["held_max"])
+        assert frac < 1.0 / P + 0.15 + 3.0 / (s.frames * s.substeps + 1), (P, frac)
+        if prev is not None:
+            assert frac < prev
+        prev = frac
+        if P == 4:
+            api.dxpbd_group_forward(g, s.x0, s.v0, s.forces, s.frames)
+            for f in range(s.frames + 1):
+                np.testing.assert_array_equal(api.dxpbd_group_positions(g, f), a["x"][f])
+        del g
