@@ -672,10 +672,11 @@ struct dxpbd_scene {
     DBuf<double4> t_xsave;   // K = 1 tet replay: pre-update vertices of every tet [4T]
     DBuf<float> t_Q2, t_e2;  // second tet block / control buffers (replay / PCG overlap)
     float *tq_w = nullptr, *te_w = nullptr, *tq_r = nullptr, *te_r = nullptr;   // overlap: replay writes, PCG reads
-    DBuf<float4> t_q4;       // tet matvec accumulator (16-byte vector atomics), folded into q
     DBuf<int32_t> t_perm;
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
-    TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p, t_Dmf.p}; }
+    DBuf<int> t_goff, t_ginc;   // per vertex: its tet-corner slots (CSR, fixed order)
+    DBuf<float> t_gq;           // [2][4][3][T] corner contributions (matvec / rhs y, rhs z)
+    TetDev tdev() const { return TetDev{T, t_idx.p, t_Dm.p, t_vol.p, t_a.p, t_b.p, t_Dmf.p, t_goff.p, t_ginc.p, t_gq.p}; }
     TmaTiles tma_tiles() const {
         return TmaTiles{n_dist_colors, ntiles, hcap, capm, d_tseg.p, d_cpair.p, d_hpad.p, qt_read ? qt_read : d_Qt.p,
                         qf == 1 ? nullptr : d_Qt2b.p, d_vslot.p, d_hslot.p};
@@ -754,6 +755,15 @@ struct dxpbd_scene {
     DBuf<float> sc_lam, sc_sig, sc_B, sc_T, sc_e;               // distance scratch (K>1)
     DBuf<float> cc_lam, cc_T, cc_sig, cc_B, cc_e;               // contact scratch (K>1)
     DBuf<double> cg_sc, acc;
+    // sweep graphs: the launch sequence of a K = 1 color sweep (distance colors, tet colors and blocks,
+    // contacts) captured once and replayed per substep (small scenes are launch-latency bound)
+    bool sweep_graph = true;                       // DXPBD_SWEEP_GRAPH
+    int sweep_graph_maxv = 1 << 21;                // only below this many vertices (the forward copies the iterate)
+    cudaGraphExec_t g_fwd = nullptr;
+    std::vector<std::pair<std::vector<const void *>, cudaGraphExec_t>> g_rep;   // keyed by the output buffers
+    int g_fwd_launches = 0, g_rep_launches = 0;
+    DBuf<double4> xw;                              // forward graph iterate
+    cudaStream_t cap_lo = nullptr, cap_mid = nullptr;
     // PCG as a CUDA graph with a conditional WHILE node (no host polls).  Opt-in (DXPBD_PCG_GRAPH=1):
     // measured 3-15 % slower than the host-polled loop with its iteration-count prediction
     bool pcg_graph = false;
@@ -991,6 +1001,29 @@ void launch_wave(dxpbd_scene *s, int k, int grid, const WavePredict &pr, const W
     s->wave_base[k] += (unsigned)(1 + s->n_dist_colors);
 }
 
+// Capture the launches `f(stream)` issues into an executable graph (kernel nodes keep the capture
+// stream's priority: `lowest` for the replay, which runs on the low-priority stream).
+template <class F>
+cudaGraphExec_t capture_graph(dxpbd_scene *s, bool lowest, F f, int &launches) {
+    cudaStream_t &cs = lowest ? s->cap_lo : s->cap_mid;
+    if (!cs) {
+        int least = 0, greatest = 0;
+        DX_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        DX_CHECK_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, lowest ? least : 0));
+    }
+    cudaGraph_t g = nullptr;
+    DX_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    launches = f(cs);
+    DX_CHECK_CUDA(cudaStreamEndCapture(cs, &g));
+    cudaGraphExec_t e = nullptr;
+    DX_CHECK_CUDA(cudaGraphInstantiate(&e, g, 0));
+    DX_CHECK_CUDA(cudaGraphDestroy(g));
+    return e;
+}
+inline bool sweep_graph_on(const dxpbd_scene *s) {
+    return s->sweep_graph && !s->prof && s->iterations == 1 && s->V <= s->sweep_graph_maxv;
+}
+
 // ------------------------------------------------------------------ one forward substep
 int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int V = s->V;
@@ -1002,6 +1035,13 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     int launches = 1;
     bool wave = s->wave_on && s->wave_fwd && s->wave_nitems > 0 && K == 1;
     const bool cached = s->qc_count && n >= s->qc_first;
+    // sweep graph: iterate in the fixed buffer xw, copied to the checkpoint slot afterwards
+    const bool graph = sweep_graph_on(s) && !wave && !cached;
+    double4 *const xckpt = xo;
+    if (graph) {
+        if (s->xw.n < (size_t)V) s->xw.alloc(V);
+        xo = s->xw.p;
+    }
     if (wave) {
         // predict + every distance color in one time-skewed launch (wave.cuh); on cached substeps the
         // replay variant also stores Q_n (same iterates bit for bit)
@@ -1018,6 +1058,8 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
                                                                        s->dtd, 1.0 / s->dtd, s->gravity, xo));
     }
+    auto sweep = [&](cudaStream_t st) -> int {
+    int launches = 0;
     for (int k = 0; k < K; ++k) {
         const bool rd = k > 0, wr = k < K - 1;
         for (int c = 0; c < (wave ? 0 : s->n_dist_colors); ++c) {
@@ -1068,6 +1110,16 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             ++launches;
         }
     }
+    return launches;
+    };
+    if (graph) {
+        if (!s->g_fwd) s->g_fwd = capture_graph(s, false, sweep, s->g_fwd_launches);
+        DX_CHECK_CUDA(cudaGraphLaunch(s->g_fwd, st));
+        DX_CHECK_CUDA(cudaMemcpyAsync(xckpt, xo, sizeof(double4) * V, cudaMemcpyDeviceToDevice, st));
+        launches += s->g_fwd_launches;
+    } else {
+        launches += sweep(st);
+    }
     DX_CHECK_CUDA(cudaGetLastError());
     return launches;
 }
@@ -1101,6 +1153,8 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     DistScratch ds{s->sc_lam.p, s->sc_sig.p, s->sc_B.p, s->sc_T.p, s->sc_e.p};
     ContactScratch cs{s->cc_lam.p, s->cc_T.p, s->cc_sig.p, s->cc_B.p, s->cc_e.p};
     const bool want_ce = (s->grad_flags & ((1u << DXPBD_GRAD_SHAPE) | (1u << DXPBD_GRAD_SPHERE))) != 0;
+    auto sweep = [&](cudaStream_t st) -> int {
+    int launches = 0;
     for (int k = 0; k < K; ++k) {
         const bool first = k == 0, last = k == K - 1;
         for (int c = 0; c < (wave ? 0 : s->n_dist_colors); ++c) {
@@ -1193,6 +1247,26 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             ++launches;
         }
     }
+    return launches;
+    };
+    if (sweep_graph_on(s) && !wave) {
+        // graph per set of output buffers (they alternate with the replay / PCG overlap)
+        const bool g_mat = ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) != 0;
+        std::vector<const void *> key = {qtw, s->tq_w ? s->tq_w : s->t_Q.p, g_mat ? (s->te_w ? s->te_w : s->t_e.p) : nullptr,
+                                         s->qc_w ? s->qc_w : s->Qc.p, want_ce ? (s->ec_w ? s->ec_w : s->ec.p) : nullptr,
+                                         want_e ? s->ed.p : nullptr, s->Qd.p};
+        cudaGraphExec_t e = nullptr;
+        for (auto &kv : s->g_rep)
+            if (kv.first == key) e = kv.second;
+        if (!e) {
+            e = capture_graph(s, true, sweep, s->g_rep_launches);
+            s->g_rep.push_back({key, e});
+        }
+        DX_CHECK_CUDA(cudaGraphLaunch(e, st));
+        launches += s->g_rep_launches;
+    } else {
+        launches += sweep(st);
+    }
     DX_CHECK_CUDA(cudaGetLastError());
     return launches;
 }
@@ -1279,10 +1353,6 @@ BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frame
         if (((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) && s->t_e.n < 18 * T) s->t_e.alloc(18 * T);
         if (s->t_g.n < 2 * T) s->t_g.alloc(2 * T);
         if (s->iterations == 1 && s->t_xsave.n < 4 * T) s->t_xsave.alloc(4 * T);
-        if (s->t_q4.n < (size_t)V) {
-            s->t_q4.alloc(V);
-            DX_CHECK_CUDA(cudaMemsetAsync(s->t_q4.p, 0, sizeof(float4) * V, st));
-        }
         if (s->iterations > 1 && s->ts_lam.n < 2 * T) {
             s->ts_lam.alloc(2 * T); s->ts_S.alloc(18 * T); s->ts_Dt.alloc(45 * T); s->ts_Tu.alloc(4 * T); s->ts_e.alloc(18 * T);
         }
@@ -1367,11 +1437,11 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         if (tetv) {
             if (s->tetv_minb == 3)
                 LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<3><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
-                                                                                     xw, Qc, cs, s->t_q4.p));
+                                                                                     xw, Qc, cs));
             else
                 LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<1><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
-                                                                                     xw, Qc, cs, s->t_q4.p));
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update_tet<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, Qc, cs, s->t_q4.p));
+                                                                                     xw, Qc, cs));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update_tet<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, xw, Qc, cs, s->tdev()));
             return 2;
         }
         int n = 0;
@@ -1388,8 +1458,8 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<0><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
         ++n;
         if (s->T) {
-            LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), tQr, bufs, xw, cs, s->t_q4.p));
-            LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->t_q4.p, cs));
+            LAUNCH(DXPBD_K_CG_TET, k_cg_tet<<<nblk(s->T), kBlock, 0, st>>>(it, s->tdev(), tQr, bufs, xw, cs));
+            LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->tdev(), cs));
             n += 2;
         }
         if (defer)
@@ -1506,6 +1576,10 @@ int dxpbd_destroy(dxpbd_scene *s) {
     if (s->hi) cudaStreamDestroy(s->hi);
     if (s->pcg_exec) cudaGraphExecDestroy(s->pcg_exec);
     if (s->cap) cudaStreamDestroy(s->cap);
+    if (s->g_fwd) cudaGraphExecDestroy(s->g_fwd);
+    for (auto &e : s->g_rep) cudaGraphExecDestroy(e.second);
+    if (s->cap_lo) cudaStreamDestroy(s->cap_lo);
+    if (s->cap_mid) cudaStreamDestroy(s->cap_mid);
     delete s;
     return DXPBD_OK;
 }
@@ -1597,6 +1671,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_QCACHE")) s->qcache_on = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_POLL_EXTRA")) s->poll_extra = atoi(ev);
     if (const char *ev = getenv("DXPBD_PCG_GRAPH")) s->pcg_graph = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_SWEEP_GRAPH")) s->sweep_graph = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_WAVE")) s->wave_on = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_WAVE_G")) s->wave_g = std::max(1, atoi(ev));
     if (const char *ev = getenv("DXPBD_WAVE_FWD")) s->wave_fwd = atoi(ev) != 0;
@@ -1718,6 +1793,25 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         for (int q = 0; q < T; ++q) ts[q] = ti[s->tet_perm_h[q]];
         s->t_idx.alloc(T);
         upload(s->t_idx.p, ts.data(), sizeof(int4) * T, DXPBD_MEM_HOST, st);
+        {   // deterministic corner gather: per vertex its (corner c, sorted tet q) slots 3 c T + q, ascending
+            std::vector<int> goff(V + 1, 0), ginc((size_t)4 * T);
+            for (int q = 0; q < T; ++q)
+                for (int v : {ts[q].x, ts[q].y, ts[q].z, ts[q].w}) goff[v + 1]++;
+            for (int v = 0; v < V; ++v) goff[v + 1] += goff[v];
+            std::vector<int> fill(goff.begin(), goff.end() - 1);
+            for (int c = 0; c < 4; ++c)
+                for (int q = 0; q < T; ++q) {
+                    const int v = c == 0 ? ts[q].x : c == 1 ? ts[q].y : c == 2 ? ts[q].z : ts[q].w;
+                    ginc[fill[v]++] = 3 * c * T + q;
+                }
+            s->t_goff.alloc(V + 1);
+            upload(s->t_goff.p, goff.data(), sizeof(int) * (V + 1), DXPBD_MEM_HOST, st);
+            s->t_ginc.alloc(ginc.size());
+            upload(s->t_ginc.p, ginc.data(), sizeof(int) * ginc.size(), DXPBD_MEM_HOST, st);
+            s->t_gq.alloc((size_t)24 * T);
+            DX_CHECK_CUDA(cudaMemsetAsync(s->t_gq.p, 0, sizeof(float) * 24 * T, st));   // pinned corners stay 0
+            DX_CHECK_CUDA(cudaStreamSynchronize(st));
+        }
         s->t_perm.alloc(T);
         upload(s->t_perm.p, s->tet_perm_h.data(), sizeof(int32_t) * T, DXPBD_MEM_HOST, st);
         DBuf<float> tmpab;
@@ -2001,7 +2095,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         if (s->T) {
             LAUNCH(DXPBD_K_RHS, k_rhs_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->tq_r ? s->tq_r : s->t_Q.p, s->y.p, s->u0.p, s->rhs.p, s->r.p,
                                                                         s->inv_mass.p));
-            ++launches;
+            LAUNCH(DXPBD_K_RHS, k_rhs_tet_gather<<<nblk(V), kBlock, 0, st>>>(V, s->tdev(), s->rhs.p, s->r.p, s->inv_mass.p));
+            launches += 2;
         }
         int iters = 0;
         double rel = 0.0;

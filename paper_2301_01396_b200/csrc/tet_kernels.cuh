@@ -22,7 +22,29 @@ struct TetDev {
     const double *vol;    // [T] rest volume (fp64)
     const float *ta, *tb; // [T] material a, b
     const float *Dmf;     // [9T] Dm^-1 rounded to fp32 (the fp32 kernels' copy: half the bytes)
+    // deterministic corner gather (no float atomics): per-tet corner contributions gq[set][corner][k][T]
+    // and, per vertex, its corner slots in a fixed order (CSR: ginc[goff[v] .. goff[v+1]) = 3 c T + j)
+    const int *goff = nullptr, *ginc = nullptr;
+    float *gq = nullptr;
 };
+
+// corner contribution g of tet j at corner c into gather set `set` (0: matvec / rhs y, 1: rhs z)
+DX_INLINE void tet_corner_store(const TetDev &D, int set, int c, int j, float3 g) {
+    float *o = D.gq + (size_t)set * 12 * D.T + (size_t)3 * c * D.T + j;
+    o[0] = g.x;
+    o[D.T] = g.y;
+    o[2 * (size_t)D.T] = g.z;
+}
+// sum of the corner contributions at vertex v, in the fixed slot order (deterministic)
+DX_INLINE float3 tet_gather(const TetDev &D, int set, int v) {
+    float3 g = make_float3(0.f, 0.f, 0.f);
+    const float *base = D.gq + (size_t)set * 12 * D.T;
+    for (int e = D.goff[v]; e < D.goff[v + 1]; ++e) {
+        const float *o = base + D.ginc[e];
+        g = g + make_float3(o[0], o[D.T], o[2 * (size_t)D.T]);
+    }
+    return g;
+}
 
 struct TetCore {
     tr F[9];              // column-major
@@ -499,8 +521,7 @@ DX_INLINE void tet_Qmul(const float *__restrict__ Qt, int T, int j, const float 
 // Tet part of the PCG matvec (after the tile kernel wrote q): q += G^T Qt~ G p per tet with
 // vector reductions, and the p.q partial dF^T Qt~ dF.  p = p_it buffer (written by the tile kernel).
 __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float *__restrict__ Qt, CGBufs B,
-                                                   const float *__restrict__ wv, CGState s,
-                                                   float4 *__restrict__ q4 = nullptr) {
+                                                   const float *__restrict__ wv, CGState s) {
     it = cg_iter(s, it);
     if (s.pp) {
         Qt = s.pp->tQ;
@@ -527,34 +548,31 @@ __global__ void __launch_bounds__(kBlock) k_cg_tet(int it, TetDev D, const float
         for (int v = 0; v < 4; ++v) {
             if (!(wv[vid[v]] > 0.f)) continue;
             float3 g = c[v][0] * f3at(q, 0) + c[v][1] * f3at(q, 1) + c[v][2] * f3at(q, 2);
-            if (q4) red_add_f4(q4 + vid[v], make_float4(g.x, g.y, g.z, 0.f));   // one 16-byte atomic
-            else red_add_f3(B.q + vid[v], g);
+            tet_corner_store(D, 0, v, j, g);   // gathered per vertex by k_fold_q4 (deterministic)
         }
     }
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// q += xyz(q4) (the tet matvec's float4 accumulator), q4 <- 0 for the next iteration
-__global__ void k_fold_q4(int V, int it, CGBufs B, float4 *__restrict__ q4, CGState s) {
+// q += the tets' corner contributions of this iteration, gathered per vertex in a fixed order
+__global__ void k_fold_q4(int V, int it, CGBufs B, TetDev D, CGState s) {
     it = cg_iter(s, it);
     if (cg_done(s, it + 1)) return;
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= V) return;
-    const float4 a = q4[v];
-    B.q[v] = B.q[v] + make_float3(a.x, a.y, a.z);
-    q4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    B.q[v] = B.q[v] + tet_gather(D, 0, v);
 }
 
 // Scenes without distance constraints (tets, contacts): one PCG iteration in two launches instead
 // of four (tile matvec, k_cg_tet, k_fold_q4, update).  Blocks [0, nbt) are k_cg_tet's tets, which
 // form p_it at their corners on the fly (halo_p) instead of reading it; blocks [nbt, ..) form
 // p_it = M^-1 r_it + beta p_{it-1} per vertex (stored, the same halo_p expression) and add
-// p.(M + Qc) p to p.q.  q is not stored: k_cg_update_tet rebuilds q = (M + Qc) p + q4.
+// p.(M + Qc) p to p.q.  q is not stored: k_cg_update_tet rebuilds q = (M + Qc) p + the gathered
+// corner contributions.
 template <int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_cg_tetv(int it, int nbt, int V, TetDev D, const float *__restrict__ Qt,
                                                     CGBufs B, const float *__restrict__ wv,
-                                                    const float *__restrict__ Qc, CGState s,
-                                                    float4 *__restrict__ q4) {
+                                                    const float *__restrict__ Qc, CGState s) {
     it = cg_iter(s, it);
     if (s.pp) {
         const PcgPtrs pp = *s.pp;
@@ -603,7 +621,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_cg_tetv(int it, int nbt, int V
             for (int v = 0; v < 4; ++v) {
                 if (!(wv[vid[v]] > 0.f)) continue;
                 float3 g = c[v][0] * f3at(q, 0) + c[v][1] * f3at(q, 1) + c[v][2] * f3at(q, 2);
-                red_add_f4(q4 + vid[v], make_float4(g.x, g.y, g.z, 0.f));
+                tet_corner_store(D, 0, v, j, g);   // gathered by k_cg_update_tet (deterministic)
             }
         }
     } else {
@@ -626,11 +644,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_cg_tetv(int it, int nbt, int V
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// PCG update after k_cg_tetv: q = (M + Qc) p + q4 (q4 <- 0), u += alpha p, r -= alpha q,
+// PCG update after k_cg_tetv: q = (M + Qc) p + Sum of the corner contributions (fixed order), u += alpha p, r -= alpha q,
 // r.M^-1 r and r.r into slot it+1.
 __global__ void __launch_bounds__(kBlock) k_cg_update_tet(int V, int it, CGBufs B, const float *__restrict__ wv,
-                                                          const float *__restrict__ Qc, CGState s,
-                                                          float4 *__restrict__ q4) {
+                                                          const float *__restrict__ Qc, CGState s, TetDev D) {
     it = cg_iter(s, it);
     if (s.pp) {
         const PcgPtrs pp = *s.pp;
@@ -658,9 +675,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update_tet(int V, int it, CGBufs 
                               Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
                 qv = qv + sym3_mul(A, pv);
             }
-            const float4 a = q4[v];
-            qv = qv + make_float3(a.x, a.y, a.z);
-            q4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            qv = qv + tet_gather(D, 0, v);
             rv = B.r[v] - alpha * qv;
         }
         B.r[v] = rv;
@@ -698,9 +713,19 @@ __global__ void __launch_bounds__(kBlock) k_rhs_tet(TetDev D, const float *__res
         if (!(wv[vid[v]] > 0.f)) continue;
         float3 gy = c[v][0] * f3at(qy, 0) + c[v][1] * f3at(qy, 1) + c[v][2] * f3at(qy, 2);
         float3 gz = c[v][0] * f3at(qz, 0) + c[v][1] * f3at(qz, 1) + c[v][2] * f3at(qz, 2);
-        red_add_f3(b + vid[v], make_float3(-gy.x, -gy.y, -gy.z));
-        red_add_f3(r0 + vid[v], make_float3(-gz.x, -gz.y, -gz.z));
+        tet_corner_store(D, 0, v, j, gy);
+        tet_corner_store(D, 1, v, j, gz);
     }
+}
+
+// b -= G^T Qt~ G y and r0 -= G^T Qt~ G (y + u0) at every free vertex: the corner contributions of
+// k_rhs_tet gathered per vertex in a fixed order (deterministic)
+__global__ void k_rhs_tet_gather(int V, TetDev D, float3 *__restrict__ b, float3 *__restrict__ r0,
+                                 const float *__restrict__ wv) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V || !(wv[v] > 0.f)) return;
+    b[v] = b[v] - tet_gather(D, 0, v);
+    r0[v] = r0[v] - tet_gather(D, 1, v);
 }
 
 // dphi/d(a,b)_t += e~_u . vec F(y)   (Eq. gradientRule)

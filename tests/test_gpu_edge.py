@@ -336,7 +336,7 @@ def _batch_compare(scenes, grads, frames, per_collider=None):
         elif k == "compliance":
             parts = np.split(g, np.cumsum([len(s.dist_idx) for s in scenes])[:-1])
         else:   # per collider / coefficient families
-            parts = np.split(g, np.cumsum(per_collider)[:-1])
+            parts = np.split(np.ravel(g), np.cumsum(per_collider)[:-1])
         for b, gp in enumerate(parts):
             ref = np.asarray(solo[b][2][k]).ravel()
             # the batch's one global residual test vs each scene's own: differences of the order of the
