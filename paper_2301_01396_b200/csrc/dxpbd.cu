@@ -761,6 +761,8 @@ struct dxpbd_scene {
     int sweep_graph_maxv = 1 << 21;                // only below this many vertices (the forward copies the iterate)
     cudaGraphExec_t g_fwd = nullptr;
     std::vector<std::pair<std::vector<const void *>, cudaGraphExec_t>> g_rep;   // keyed by the output buffers
+    struct PcgChunk { int iters, launches; cudaGraphExec_t e; };
+    std::vector<PcgChunk> g_pcg;                   // first PCG chunk, keyed by its iteration count
     int g_fwd_launches = 0, g_rep_launches = 0;
     DBuf<double4> xw;                              // forward graph iterate
     cudaStream_t cap_lo = nullptr, cap_mid = nullptr;
@@ -1004,12 +1006,12 @@ void launch_wave(dxpbd_scene *s, int k, int grid, const WavePredict &pr, const W
 // Capture the launches `f(stream)` issues into an executable graph (kernel nodes keep the capture
 // stream's priority: `lowest` for the replay, which runs on the low-priority stream).
 template <class F>
-cudaGraphExec_t capture_graph(dxpbd_scene *s, bool lowest, F f, int &launches) {
-    cudaStream_t &cs = lowest ? s->cap_lo : s->cap_mid;
+cudaGraphExec_t capture_graph(dxpbd_scene *s, int prio, F f, int &launches) {   // prio -1 lowest, 0 default, 1 highest
+    cudaStream_t &cs = prio < 0 ? s->cap_lo : (prio > 0 ? s->cap : s->cap_mid);
     if (!cs) {
         int least = 0, greatest = 0;
         DX_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        DX_CHECK_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, lowest ? least : 0));
+        DX_CHECK_CUDA(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio < 0 ? least : (prio > 0 ? greatest : 0)));
     }
     cudaGraph_t g = nullptr;
     DX_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -1113,7 +1115,7 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     return launches;
     };
     if (graph) {
-        if (!s->g_fwd) s->g_fwd = capture_graph(s, false, sweep, s->g_fwd_launches);
+        if (!s->g_fwd) s->g_fwd = capture_graph(s, 0, sweep, s->g_fwd_launches);
         DX_CHECK_CUDA(cudaGraphLaunch(s->g_fwd, st));
         DX_CHECK_CUDA(cudaMemcpyAsync(xckpt, xo, sizeof(double4) * V, cudaMemcpyDeviceToDevice, st));
         launches += s->g_fwd_launches;
@@ -1259,7 +1261,7 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         for (auto &kv : s->g_rep)
             if (kv.first == key) e = kv.second;
         if (!e) {
-            e = capture_graph(s, true, sweep, s->g_rep_launches);
+            e = capture_graph(s, st == s->aux ? -1 : 0, sweep, s->g_rep_launches);
             s->g_rep.push_back({key, e});
         }
         DX_CHECK_CUDA(cudaGraphLaunch(e, st));
@@ -1525,10 +1527,37 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     int chunk = s->last_iters > 0 ? std::max(s->last_iters + s->poll_extra, 2) : 8;
     iters_out = -1;
     relres_out = 0.0;
+    // small scenes: the first chunk (the previous solve's iteration count) as ONE graph launch of that
+    // many iterations (kernels with their iteration index baked in, the substep's rotating buffers read
+    // from pcg_pp; iterations past convergence exit at once as in the stream launches)
+    const bool chunk_graph = sweep_graph_on(s) && !cgcg;
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         chunk = 2;
-        for (; it < end; ++it) launches += iteration(it, st, cs);
+        if (chunk_graph && it == 0 && end >= 2) {
+            const dxpbd_scene::PcgChunk *ch = nullptr;
+            for (auto &c : s->g_pcg)
+                if (c.iters == end) ch = &c;
+            if (!ch) {
+                if (!s->pcg_pp.p) s->pcg_pp.alloc(1);
+                CGState cg = cs;
+                cg.pp = s->pcg_pp.p;
+                int nl = 0;
+                cudaGraphExec_t e = capture_graph(s, st == s->hi ? 1 : 0, [&](cudaStream_t cst) {
+                    int n = 0;
+                    for (int k = 0; k < end; ++k) n += iteration(k, cst, cg);
+                    return n;
+                }, nl);
+                s->g_pcg.push_back({end, nl, e});
+                ch = &s->g_pcg.back();
+            }
+            k_set_pcg_ptrs<<<1, 1, 0, st>>>(s->pcg_pp.p, PcgPtrs{s->ax.p, tt.Q4, Qc, tQr});
+            DX_CHECK_CUDA(cudaGraphLaunch(ch->e, st));
+            launches += 1 + ch->launches;
+            it = end;
+        } else {
+            for (; it < end; ++it) launches += iteration(it, st, cs);
+        }
         // convergence check: rr of the last completed iteration against |b|^2
         DX_CHECK_CUDA(cudaMemcpyAsync(s->h_scal, s->cg_sc.p, sizeof(double) * (size_t)(maxit + 2) * 4, cudaMemcpyDeviceToHost, st));
         DX_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -1578,6 +1607,7 @@ int dxpbd_destroy(dxpbd_scene *s) {
     if (s->cap) cudaStreamDestroy(s->cap);
     if (s->g_fwd) cudaGraphExecDestroy(s->g_fwd);
     for (auto &e : s->g_rep) cudaGraphExecDestroy(e.second);
+    for (auto &e : s->g_pcg) cudaGraphExecDestroy(e.e);
     if (s->cap_lo) cudaStreamDestroy(s->cap_lo);
     if (s->cap_mid) cudaStreamDestroy(s->cap_mid);
     delete s;
@@ -1968,10 +1998,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     // PCG iteration loops as graph launches (pcg_solve): counts and convergence come back once, at the end
     const bool gmode = s->pcg_graph && !s->prof && !(s->use_tma && s->qf == 1 && !s->T && s->cgcg);
     if (gmode) {
-        if (!s->pcg_ctl.p) {
-            s->pcg_ctl.alloc(1);
-            s->pcg_pp.alloc(1);
-        }
+        if (!s->pcg_ctl.p) s->pcg_ctl.alloc(1);
+        if (!s->pcg_pp.p) s->pcg_pp.alloc(1);
         DX_CHECK_CUDA(cudaMemsetAsync(s->pcg_ctl.p, 0, sizeof(PcgCtl), st));
     }
     // PCG start fused into the TMA rhs kernel (no tet rhs pass after it, standard PCG)
