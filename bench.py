@@ -305,6 +305,9 @@ def run_partitioned(a):
             "exchange": {"vertices_per_sweep": st["xchg_sweep"], "halo_vertices": st["xchg_halo"],
                          "cross_blocks": st["xchg_blocks"],
                          "bytes_per_substep_forward": 32.0 * st["xchg_sweep"]},
+            "memory": {"trajectory_bytes_largest_partition": st["traj_bytes_part"],
+                       "trajectory_bytes_single_scene": st["traj_bytes_single"],
+                       "held_vertices_largest_partition": st["held_max"]},
             "cg_iters_per_substep": st["cg_iters_total"] / max(st["solves"], 1), "create_s": t_create}
     print(json.dumps(line), flush=True)
     par.shutdown()
