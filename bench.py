@@ -412,9 +412,11 @@ def run_ours(a):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(n_e2e):
+            # forces travel frame by frame under the forward, force gradients frame by frame under the
+            # backward (dxpbd_grads_stream); both calls return with the host buffers complete
             api.dxpbd_forward(sc, x0_h, v0_h, forces_h, a.frames)
+            api.dxpbd_grads_stream(sc, "forces", gforce_h)
             api.dxpbd_backward(sc, kf, tg_h)
-            api.dxpbd_grads(sc, "forces", gforce_h)
         e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0

@@ -148,6 +148,14 @@ int dxpbd_grads(dxpbd_scene *scene, int32_t kind, float *out, int64_t out_len, i
                 void *stream);
 
 /* Replace a parameter family (DXPBD_PARAM_*) between optimization iterations. */
+/* Stream the force gradients of the NEXT dxpbd_backward into `out` ([frames][V][3], user order;
+ * HOST or DEVICE per `mem`): each frame's slice leaves the device as soon as the backward has
+ * passed that frame (HOST: D2H on a copy stream, overlapping the rest of the backward; use pinned
+ * memory for the overlap).  The backward returns after every slice has arrived; the registration
+ * is then cleared.  kind must be DXPBD_GRAD_FORCES (enabled in grad_flags), after a forward, with
+ * out_len = frames * 3V. */
+int dxpbd_grads_stream(dxpbd_scene *scene, int32_t kind, float *out, int64_t out_len, int32_t mem);
+
 int dxpbd_set_params(dxpbd_scene *scene, int32_t kind, const float *data, int64_t len,
                      int32_t mem, void *stream);
 

@@ -74,6 +74,7 @@ def lib():
             "dxpbd_backward": ([vp, i32, vp, vp, vp, i32, vp, vp], ctypes.c_int),
             "dxpbd_grads": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
             "dxpbd_set_params": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
+            "dxpbd_grads_stream": ([vp, i32, vp, i64, i32], ctypes.c_int),
             "dxpbd_coloring": ([vp, i32, vp, i64, vp], ctypes.c_int),
             "dxpbd_stats": ([vp, vp, i32], ctypes.c_int),
             "dxpbd_profile": ([vp, i32], ctypes.c_int),
@@ -103,7 +104,8 @@ EXPORTED = ["dxpbd_create", "dxpbd_destroy", "dxpbd_forward", "dxpbd_positions",
             "dxpbd_grads", "dxpbd_set_params", "dxpbd_coloring", "dxpbd_stats", "dxpbd_last_error",
             "dxpbd_version", "dxpbd_profile", "dxpbd_kernel_times", "dxpbd_group_create", "dxpbd_group_destroy",
             "dxpbd_group_forward", "dxpbd_group_positions", "dxpbd_group_backward", "dxpbd_group_grads",
-            "dxpbd_group_stats", "dxpbd_nccl_unique_id", "dxpbd_group_create_dist", "dxpbd_partition_plan"]
+            "dxpbd_group_stats", "dxpbd_nccl_unique_id", "dxpbd_group_create_dist", "dxpbd_partition_plan",
+            "dxpbd_grads_stream"]
 
 KCLASSES = ["predict", "dist_project", "contact_project", "tet_project", "dist_replay", "contact_replay",
             "tet_replay", "cg_vertex", "cg_dist", "cg_tet", "cg_update", "cg_init", "rhs", "adjoint", "grads",
@@ -310,6 +312,19 @@ def dxpbd_grads(scene: DxScene, kind, out=None):
     n = int(np.prod(shape))
     a = _out_arg(out, n, "dxpbd_grads")
     _check(lib().dxpbd_grads(scene.handle, int(kind), a.ptr, n, a.mem, _stream(out)), "dxpbd_grads")
+    return out
+
+
+def dxpbd_grads_stream(scene: DxScene, kind, out):
+    """Register `out` (host numpy / pinned torch CPU tensor, or a CUDA tensor) to receive the force
+    gradients of the NEXT dxpbd_backward, frame by frame as the backward passes them (include/dxpbd.h).
+    `out` must stay alive until that backward returns."""
+    kind = GRAD_NAMES.get(kind, kind)
+    shape = _grad_size(scene, kind)
+    n = int(np.prod(shape))
+    a = _out_arg(out, n, "dxpbd_grads_stream")
+    scene._stream_keep = (out, a)
+    _check(lib().dxpbd_grads_stream(scene.handle, int(kind), a.ptr, n, a.mem), "dxpbd_grads_stream")
     return out
 
 

@@ -723,6 +723,13 @@ struct dxpbd_scene {
     DBuf<float> forces;   // [max_frames * V * 3]
     bool have_forces = false;
     DBuf<float> tmp3;     // [V*3] staging
+    // host <-> device pipelining: per-frame force uploads overlap the forward, per-frame force-gradient
+    // downloads (dxpbd_grads_stream) overlap the backward; two staging slots on a copy stream
+    cudaStream_t cpy = nullptr;
+    DBuf<float> stage[2];
+    cudaEvent_t ev_cp[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    float *gs_out = nullptr;   // registered output of the next backward's force gradients
+    int gs_mem = 0;
 
     // forward scratch for iterations > 1
     DBuf<float> lam_d, lam_c;
@@ -823,6 +830,16 @@ void download(void *dst, const void *src, size_t bytes, int mem, cudaStream_t st
     DX_REQUIRE(dst != nullptr, DXPBD_ERR_ARG, "null output pointer");
     DX_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, mem == DXPBD_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
     if (mem == DXPBD_MEM_HOST) DX_CHECK_CUDA(cudaStreamSynchronize(st));
+}
+
+void ensure_copy_pipe(dxpbd_scene *s) {
+    if (s->cpy) return;
+    DX_CHECK_CUDA(cudaStreamCreateWithFlags(&s->cpy, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_cp[k], cudaEventDisableTiming));
+        DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_free[k], cudaEventDisableTiming));
+        s->stage[k].alloc((size_t)3 * s->V);
+    }
 }
 
 void apply_shape(dxpbd_scene *s, cudaStream_t st) {
@@ -1299,14 +1316,43 @@ void forward_inputs(dxpbd_scene *s, const float *x0, const float *v0, const floa
     if (forces) {
         if (s->forces.n < (size_t)s->max_frames * V * 3) s->forces.alloc((size_t)s->max_frames * V * 3);
         if (mem == DXPBD_MEM_HOST) {
-            for (int f = 0; f < num_frames; ++f) {
-                upload(s->tmp3.p, forces + (size_t)f * V * 3, sizeof(float) * V * 3, mem, st);
-                k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->tmp3.p, s->vperm.p, s->forces.p + (size_t)f * V * 3);
-            }
+            // per frame, overlapped with the forward (dxpbd_forward: upload_frame_forces)
         } else {
             k_gather3<<<nblk((int64_t)V * num_frames), kBlock, 0, st>>>(V, num_frames, forces, s->vperm.p, s->forces.p);
         }
     }
+}
+
+// Host forces of frame f: H2D into a staging slot on the copy stream (overlapping the substeps of
+// earlier frames), then the gather into internal order on the compute stream.
+void upload_frame_forces(dxpbd_scene *s, const float *forces, int f, cudaStream_t st) {
+    const int V = s->V, k = f & 1;
+    ensure_copy_pipe(s);
+    DX_CHECK_CUDA(cudaStreamWaitEvent(s->cpy, s->ev_free[k], 0));   // the gather of frame f - 2 consumed the slot
+    DX_CHECK_CUDA(cudaMemcpyAsync(s->stage[k].p, forces + (size_t)f * V * 3, sizeof(float) * V * 3, cudaMemcpyHostToDevice, s->cpy));
+    DX_CHECK_CUDA(cudaEventRecord(s->ev_cp[k], s->cpy));
+    DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_cp[k], 0));
+    k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->stage[k].p, s->vperm.p, s->forces.p + (size_t)f * V * 3);
+    DX_CHECK_CUDA(cudaEventRecord(s->ev_free[k], st));
+}
+
+// Force gradients of frame f (final once the backward has passed the frame's first substep) to the
+// output registered with dxpbd_grads_stream: scatter to user order into a staging slot, D2H on the
+// copy stream while the backward continues.
+void stream_frame_grads(dxpbd_scene *s, int f, cudaStream_t st) {
+    const int V = s->V, k = f & 1;
+    float *dst = s->gs_out + (size_t)f * V * 3;
+    if (s->gs_mem != DXPBD_MEM_HOST) {
+        k_scatter3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->g_force.p + (size_t)f * V * 3, s->vperm.p, dst);
+        return;
+    }
+    ensure_copy_pipe(s);
+    DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_free[k], 0));   // the D2H of frame f + 2 released the slot
+    k_scatter3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->g_force.p + (size_t)f * V * 3, s->vperm.p, s->stage[k].p);
+    DX_CHECK_CUDA(cudaEventRecord(s->ev_cp[k], st));
+    DX_CHECK_CUDA(cudaStreamWaitEvent(s->cpy, s->ev_cp[k], 0));
+    DX_CHECK_CUDA(cudaMemcpyAsync(dst, s->stage[k].p, sizeof(float) * V * 3, cudaMemcpyDeviceToHost, s->cpy));
+    DX_CHECK_CUDA(cudaEventRecord(s->ev_free[k], s->cpy));
 }
 
 struct BwdSetup {
@@ -1603,6 +1649,9 @@ int dxpbd_destroy(dxpbd_scene *s) {
         if (e) cudaEventDestroy(e);
     if (s->aux) cudaStreamDestroy(s->aux);
     if (s->hi) cudaStreamDestroy(s->hi);
+    for (cudaEvent_t e : {s->ev_cp[0], s->ev_cp[1], s->ev_free[0], s->ev_free[1]})
+        if (e) cudaEventDestroy(e);
+    if (s->cpy) cudaStreamDestroy(s->cpy);
     if (s->pcg_exec) cudaGraphExecDestroy(s->pcg_exec);
     if (s->cap) cudaStreamDestroy(s->cap);
     if (s->g_fwd) cudaGraphExecDestroy(s->g_fwd);
@@ -1954,7 +2003,15 @@ int dxpbd_forward(dxpbd_scene *s, const float *x0, const float *v0, const float 
             s->qc_count = M;
         }
     }
-    for (int n = 0; n < N; ++n) launches += forward_substep(s, n, st);
+    const bool host_forces = forces && mem == DXPBD_MEM_HOST;
+    if (host_forces && num_frames > 0) upload_frame_forces(s, forces, 0, st);
+    for (int n = 0; n < N; ++n) {
+        // the next frame's forces travel while this frame's substeps run
+        if (host_forces && n % s->substeps == 0 && n / s->substeps + 1 < num_frames)
+            upload_frame_forces(s, forces, n / s->substeps + 1, st);
+        launches += forward_substep(s, n, st);
+    }
+    if (host_forces) DX_CHECK_CUDA(cudaStreamSynchronize(s->cpy));   // the caller's buffer may be reused
     DX_CHECK_CUDA(cudaGetLastError());
     s->frames_done = num_frames;
     s->have_grads = false;
@@ -2154,6 +2211,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             ++launches;
         }
         if (ovl) DX_CHECK_CUDA(cudaEventRecord(s->ev_pcg[n & 1], st));   // buffer n & 1 free again
+        if (s->gs_out && g_forces && n % sub == 0) stream_frame_grads(s, frame, st);   // frame complete
     }
     s->qt_read = s->qt_write = nullptr;
     s->tq_w = s->te_w = s->tq_r = s->te_r = nullptr;
@@ -2162,6 +2220,11 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         DX_CHECK_CUDA(cudaEventRecord(s->ev_end, st));
         DX_CHECK_CUDA(cudaStreamWaitEvent(user_st, s->ev_end, 0));
         st = user_st;
+    }
+    if (s->gs_out && g_forces) {   // frames after the last keyframe (zero gradients) and the sync
+        for (int f = std::max(0, (std::min(N, last_key_state) + sub - 1) / sub); f < s->frames_done; ++f) stream_frame_grads(s, f, st);
+        if (s->gs_mem == DXPBD_MEM_HOST) DX_CHECK_CUDA(cudaStreamSynchronize(s->cpy));
+        s->gs_out = nullptr;
     }
     if (s->g_x0.n < (size_t)3 * V) s->g_x0.alloc((size_t)3 * V);
     if (s->g_v0.n < (size_t)3 * V) s->g_v0.alloc((size_t)3 * V);
@@ -2277,6 +2340,18 @@ int dxpbd_grads(dxpbd_scene *s, int32_t kind, float *out, int64_t out_len, int32
             break;
         }
     }
+    DX_API_END
+}
+
+int dxpbd_grads_stream(dxpbd_scene *s, int32_t kind, float *out, int64_t out_len, int32_t mem) {
+    DX_API_BEGIN
+    DX_REQUIRE(s && out, DXPBD_ERR_ARG, "null argument");
+    DX_REQUIRE(kind == DXPBD_GRAD_FORCES, DXPBD_ERR_ARG, "streamed gradients: forces only");
+    DX_REQUIRE((s->grad_flags >> DXPBD_GRAD_FORCES) & 1, DXPBD_ERR_STATE, "gradient family not enabled in grad_flags");
+    DX_REQUIRE(s->frames_done >= 1, DXPBD_ERR_STATE, "no forward has run");
+    DX_REQUIRE(out_len == (int64_t)s->frames_done * s->V * 3, DXPBD_ERR_ARG, "out_len must be frames*3V");
+    s->gs_out = out;
+    s->gs_mem = mem;
     DX_API_END
 }
 

@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
 // vertex-disjoint within a color by R1).
 constexpr int kTmaStages = 3;
 constexpr int kTmaThreads = kTileV / 2;                  // rhs kernel threads per tile
-constexpr int kRhsMinB = kTileV == 512 ? 3 : 1;           // its launch-bounds CTAs per SM
+constexpr int kRhsMinB = kTileV >= 1024 ? 1 : 1536 / kTileV;   // its launch-bounds CTAs per SM (3 at 512)
 constexpr int kMvThreads = kTileV / 2;                   // matvec threads per tile
 constexpr int kMvMinB = 2048 / kTileV;                   // its resident CTAs per SM (64 registers)
 constexpr int kMaxColors = 64;   // bounds table in shared memory (more colors: generic kernel)

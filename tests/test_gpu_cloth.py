@@ -143,3 +143,31 @@ def test_medium_full_size_forward_one_frame():
     g = gpu_run(s, backward=False, frames=1)
     o = oracle_run(s, frames=1, backward=False)
     assert rel_l2(g["x"][-1], o["x"][-1]) < POS_TOL
+
+
+def test_host_pipelined_forces_and_streamed_gradients():
+    """Host forces uploaded frame by frame under the forward, force gradients streamed frame by frame
+    under the backward (dxpbd_grads_stream, pinned host and device outputs): identical to the device
+    inputs / dxpbd_grads path, including frames after the last keyframe (zero gradients)."""
+    import torch
+    from paper_2301_01396_b200 import api
+    s = f32(large_cloth(n=24, frames=4, substeps=3, side=1.0, key_frames=(1, 3)))
+    sc = api.dxpbd_create(**api.scene_kwargs(s), max_frames=4, grad_flags=api.flags("forces"))
+    dev = lambda a: torch.as_tensor(np.asarray(a, np.float32), device="cuda")  # noqa: E731
+    api.dxpbd_forward(sc, dev(s.x0), dev(s.v0), dev(s.forces), 4)
+    ref_x = api.dxpbd_positions(sc, 4)
+    api.dxpbd_backward(sc, s.key_frames, dev(s.targets))
+    ref = api.dxpbd_grads(sc, "forces")
+    pin = lambda a: torch.as_tensor(np.asarray(a, np.float32)).pin_memory()  # noqa: E731
+    api.dxpbd_forward(sc, pin(s.x0), pin(s.v0), pin(s.forces), 4)
+    np.testing.assert_array_equal(api.dxpbd_positions(sc, 4), ref_x)
+    out_h = torch.zeros(ref.shape, dtype=torch.float32).pin_memory()
+    api.dxpbd_grads_stream(sc, "forces", out_h)
+    api.dxpbd_backward(sc, s.key_frames, pin(s.targets))
+    np.testing.assert_array_equal(out_h.numpy(), ref)
+    assert np.abs(ref[3]).max() == 0.0 and np.abs(ref[2]).max() > 0.0
+    out_d = torch.zeros(ref.shape, dtype=torch.float32, device="cuda")
+    api.dxpbd_grads_stream(sc, "forces", out_d)
+    api.dxpbd_backward(sc, s.key_frames, dev(s.targets))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out_d.cpu().numpy(), ref)
