@@ -1303,7 +1303,7 @@ void positions_from(dxpbd_scene *s, const double4 *x, float *out, int mem, cudaS
 
 // x0, v0, forces (user order, host or device) -> internal order: state 0, v0, per-frame forces
 void forward_inputs(dxpbd_scene *s, const float *x0, const float *v0, const float *forces, int num_frames, int mem,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool defer_host_forces = false) {
     const int V = s->V;
     // user vertex order -> internal (Morton) order at the boundary
     const float *src = x0;
@@ -1315,8 +1315,13 @@ void forward_inputs(dxpbd_scene *s, const float *x0, const float *v0, const floa
     s->have_forces = forces != nullptr;
     if (forces) {
         if (s->forces.n < (size_t)s->max_frames * V * 3) s->forces.alloc((size_t)s->max_frames * V * 3);
-        if (mem == DXPBD_MEM_HOST) {
+        if (mem == DXPBD_MEM_HOST && defer_host_forces) {
             // per frame, overlapped with the forward (dxpbd_forward: upload_frame_forces)
+        } else if (mem == DXPBD_MEM_HOST) {
+            for (int f = 0; f < num_frames; ++f) {
+                upload(s->tmp3.p, forces + (size_t)f * V * 3, sizeof(float) * V * 3, mem, st);
+                k_gather3<<<nblk(V), kBlock, 0, st>>>(V, 1, s->tmp3.p, s->vperm.p, s->forces.p + (size_t)f * V * 3);
+            }
         } else {
             k_gather3<<<nblk((int64_t)V * num_frames), kBlock, 0, st>>>(V, num_frames, forces, s->vperm.p, s->forces.p);
         }
@@ -1972,7 +1977,7 @@ int dxpbd_forward(dxpbd_scene *s, const float *x0, const float *v0, const float 
     DX_REQUIRE(num_frames >= 0 && num_frames <= s->max_frames, DXPBD_ERR_LIMIT, "num_frames exceeds max_frames");
     DX_CHECK_CUDA(cudaSetDevice(s->device));
     cudaStream_t st = (cudaStream_t)stream;
-    forward_inputs(s, x0, v0, forces, num_frames, mem, st);
+    forward_inputs(s, x0, v0, forces, num_frames, mem, st, true);
     int launches = 4;
     const int N = num_frames * s->substeps;
     // block cache for the last substeps in spare HBM (K = 1 TMA path without tets / compliance
