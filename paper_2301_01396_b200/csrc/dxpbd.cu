@@ -21,6 +21,7 @@
 
 #include "../../include/dxpbd.h"
 #include "kernels.cuh"
+#include "pull.cuh"
 #include "tet_kernels.cuh"
 #include "wave.cuh"
 
@@ -298,6 +299,188 @@ static void tma_tile_layout(int t, int nc, int nt, int hcap, const std::vector<i
     }
 }
 
+// Pull layout of one tile (pull.cuh; create time, host).  Every constraint incident to the tile gets
+// one primary own vertex: internal constraints the endpoint from which the rest-pose offset to the
+// other endpoint is lexicographically positive (quantized on the Morton cell, so on a lattice every
+// vertex is primary for the same set of directions), cross-tile constraints their own endpoint
+// (they are primary in both tiles).  A vertex's primaries are ordered (canonical direction first,
+// then by offset) and the first K0 fill the dense slabs [k][i]; the rest go to the tile's overflow
+// list.  Slot (k, i) / K0 * kTileV + e is both the block's position in the tile's Q region and the
+// y slot the secondary endpoint (or the overflow entry's own vertex) reads.  Local slots: own
+// vertex v -> v - t * kTileV, halo vertex -> kTileV + rank in the tile's sorted halo list.
+// count mode (idx == nullptr): only td.z / td.w (K0 | KS2 << 8, overflow entries).
+struct PullScratch {
+    struct Prim { int flag; long long kx, ky, kz; int q, other, kind, color, slot; };   // kind 0 internal, 1 own cross, 2 foreign
+    std::vector<std::vector<Prim>> prim;
+    std::vector<std::vector<int>> sec;               // y-slot entries (slot | add flag << 15)
+    std::vector<std::pair<int, int>> internal_sec;   // (secondary vertex, constraint q) resolved after ranking
+    std::vector<std::pair<int, int>> qpos;           // (q, slot) of internal constraints
+    std::vector<std::tuple<int, int, int>> order;    // (color, vertex, rank)
+    std::vector<int> lane;                           // [slab][vertex]: lane of the vertex's slot in its warp's 32
+};
+
+static void pull_tile_layout(int t, int nc, int nt, const std::vector<int> &halo_t, const int64_t *cnt,
+                             const int64_t *fc, const int2 *ab, const int *fidx, const float *xrest,
+                             const int32_t *vperm, double hcell, int nvt, int4 &td, uint32_t *idx, int *tpos,
+                             int *fposv, PullScratch &w) {
+    auto local = [&](int v) {
+        return v / kTileV == t ? v - t * kTileV
+                               : kTileV + (int)(std::lower_bound(halo_t.begin(), halo_t.end(), v) - halo_t.begin());
+    };
+    const double ih = hcell > 0 ? 1.0 / hcell : 0.0;
+    auto offset = [&](int from, int to, long long (&k)[3]) {   // quantized rest offset; returns its lexicographic sign
+        for (int c = 0; c < 3; ++c)
+            k[c] = std::llround(((double)xrest[3 * (size_t)vperm[to] + c] - (double)xrest[3 * (size_t)vperm[from] + c]) * ih);
+        for (int c = 0; c < 3; ++c)
+            if (k[c] != 0) return k[c] > 0 ? 1 : -1;
+        return 0;
+    };
+    w.prim.resize(kTileV);
+    w.sec.resize(kTileV);
+    for (int i = 0; i < kTileV; ++i) { w.prim[i].clear(); w.sec[i].clear(); }
+    w.internal_sec.clear();
+    for (int c = 0; c < nc; ++c) {
+        const size_t kk = (size_t)c * nt + t;
+        for (int64_t q = cnt[kk]; q < cnt[kk + 1]; ++q) {   // a own
+            const int a = ab[q].x, b = ab[q].y;
+            long long k[3];
+            const int sg = offset(a, b, k);
+            if (b / kTileV == t) {
+                if (sg >= 0) {
+                    w.prim[a - t * kTileV].push_back({0, k[0], k[1], k[2], (int)q, b - t * kTileV, 0, c, 0});
+                    w.internal_sec.push_back({b - t * kTileV, (int)q});
+                } else {
+                    w.prim[b - t * kTileV].push_back({0, -k[0], -k[1], -k[2], (int)q, a - t * kTileV, 0, c, 0});
+                    w.internal_sec.push_back({a - t * kTileV, (int)q});
+                }
+            } else {
+                w.prim[a - t * kTileV].push_back({sg >= 0 ? 0 : 1, k[0], k[1], k[2], (int)q, local(b), 1, c, 0});
+            }
+        }
+        for (int64_t k2 = fc[kk]; k2 < fc[kk + 1]; ++k2) {   // b own, a in another tile
+            const int q = fidx[k2];
+            const int a = ab[q].x, b = ab[q].y;
+            long long k[3];
+            const int sg = offset(b, a, k);
+            w.prim[b - t * kTileV].push_back({sg > 0 ? 0 : 1, k[0], k[1], k[2], q, local(a), 2, c, 0});
+        }
+    }
+    int fill[kPullK0] = {0};
+    w.lane.assign((size_t)kPullK0 * kTileV, 0);
+    for (int i = 0; i < kTileV; ++i) {
+        auto &p = w.prim[i];
+        std::sort(p.begin(), p.end(), [](const PullScratch::Prim &x, const PullScratch::Prim &y) {
+            return std::tie(x.flag, x.kx, x.ky, x.kz, x.q) < std::tie(y.flag, y.kx, y.ky, y.kz, y.q);
+        });
+        for (int k = 0; k < std::min<int>(kPullK0, (int)p.size()); ++k) fill[k]++;
+    }
+    // dense slab k pays off while at least half of the tile's vertices use it (a padded entry costs
+    // 18 bytes, an overflow entry 22 and a secondary)
+    int K0 = 0;
+    while (K0 < kPullK0 && fill[K0] > 0 && (K0 == 0 || 2 * fill[K0] >= nvt)) ++K0;
+    const int K02 = (K0 + 1) / 2;
+    // y slots = Q positions.  Dense slab k: within each aligned block of 32 vertices (one warp) the
+    // entries are grouped by color, so the replay's per-color launches write runs of consecutive
+    // blocks (a lattice direction holds two colors: 256-byte runs); inside its color's lane range
+    // each vertex takes a lane whose 16-byte bank group is still free in its quarter-warp's access
+    // phase (conflict-free direct accesses).  The lane goes into the primary entry.  Overflow
+    // entries: by color.
+    for (int k = 0; k < K0; ++k)
+        for (int b0 = 0; b0 < kTileV; b0 += 32) {
+            w.order.clear();
+            for (int i = b0; i < b0 + 32; ++i)
+                if ((int)w.prim[i].size() > k) w.order.push_back({w.prim[i][k].color, i, k});
+            std::sort(w.order.begin(), w.order.end());
+            int lo[32], hi[32];   // per vertex of the block: its color's lane range
+            for (size_t l = 0; l < w.order.size();) {
+                size_t m = l;
+                while (m < w.order.size() && std::get<0>(w.order[m]) == std::get<0>(w.order[l])) ++m;
+                for (size_t q = l; q < m; ++q) { lo[std::get<1>(w.order[q]) - b0] = (int)l; hi[std::get<1>(w.order[q]) - b0] = (int)m; }
+                l = m;
+            }
+            uint32_t taken = 0;
+            for (int i = b0; i < b0 + 32; ++i) w.lane[(size_t)k * kTileV + i] = -1;
+            for (int q8 = 0; q8 < 4; ++q8) {
+                uint32_t banks = 0;   // 16-byte bank groups used by this quarter-warp's access phase
+                for (int i = b0 + 8 * q8; i < b0 + 8 * q8 + 8; ++i) {
+                    if ((int)w.prim[i].size() <= k) continue;
+                    int best = -1;
+                    for (int l = lo[i - b0]; l < hi[i - b0]; ++l) {
+                        if ((taken >> l) & 1) continue;
+                        if (best < 0) best = l;
+                        if (!((banks >> (l & 7)) & 1)) { best = l; break; }
+                    }
+                    taken |= 1u << best;
+                    banks |= 1u << (best & 7);
+                    w.prim[i][k].slot = k * kTileV + b0 + best;
+                    w.lane[(size_t)k * kTileV + i] = best;
+                }
+            }
+            // vertices without a k-th primary take the lanes left over (their entry is "none", but
+            // the kernels stay branch-free: every thread owns one slot of the slab)
+            int free_l = 0;
+            for (int i = b0; i < b0 + 32; ++i)
+                if (w.lane[(size_t)k * kTileV + i] < 0) {
+                    while ((taken >> free_l) & 1) ++free_l;
+                    taken |= 1u << free_l;
+                    w.lane[(size_t)k * kTileV + i] = free_l;
+                }
+        }
+    w.order.clear();
+    for (int i = 0; i < kTileV; ++i)
+        for (int r = K0; r < (int)w.prim[i].size(); ++r) w.order.push_back({w.prim[i][r].color, i, r});
+    std::sort(w.order.begin(), w.order.end());
+    const int nover = (int)w.order.size();
+    for (int e = 0; e < nover; ++e) {
+        const int i = std::get<1>(w.order[e]);
+        w.prim[i][std::get<2>(w.order[e])].slot = K0 * kTileV + e;
+        w.sec[i].push_back((K0 * kTileV + e) | 0x8000);   // the own vertex adds y = Q (p_own - p_other)
+    }
+    w.qpos.clear();
+    for (int i = 0; i < kTileV; ++i)
+        for (auto &pr : w.prim[i]) {
+            if (pr.kind == 0) w.qpos.push_back({pr.q, pr.slot});
+            if (idx) {
+                if (pr.kind == 2) fposv[pr.q] = td.x + pr.slot;
+                else tpos[pr.q] = td.x + pr.slot;
+            }
+        }
+    std::sort(w.qpos.begin(), w.qpos.end());
+    for (auto &is : w.internal_sec) {
+        auto itp = std::lower_bound(w.qpos.begin(), w.qpos.end(), std::make_pair(is.second, INT32_MIN));
+        w.sec[is.first].push_back(itp->second);   // the partner subtracts
+    }
+    int KS = 0;
+    for (int i = 0; i < kTileV; ++i) {
+        std::sort(w.sec[i].begin(), w.sec[i].end(), [](int x, int y) { return (x & 0x7fff) < (y & 0x7fff); });
+        KS = std::max(KS, (int)w.sec[i].size());
+    }
+    const int KS2 = (KS + 1) / 2;
+    td.z = K0 | (KS2 << 8);
+    td.w = nover;
+    if (!idx) return;
+    uint32_t *pw = idx, *sw = idx + (size_t)K02 * kTileV, *ow = sw + (size_t)KS2 * kTileV;
+    for (size_t k = 0; k < (size_t)(K02 + KS2) * kTileV; ++k) idx[k] = 0xffffffffu;
+    for (int k = 0; k < K0; ++k)   // "none" primaries: other = 0x7ff, their own (unused) lane
+        for (int i = 0; i < kTileV; ++i)
+            if ((int)w.prim[i].size() <= k) {
+                uint32_t &wd = pw[(size_t)(k / 2) * kTileV + i];
+                const uint32_t v = 0x7ffu | ((uint32_t)w.lane[(size_t)k * kTileV + i] << 11);
+                wd = (k & 1) ? ((wd & 0xffffu) | (v << 16)) : ((wd & 0xffff0000u) | v);
+            }
+    auto put16 = [](uint32_t &wd, int r, uint32_t v) {
+        wd = (r & 1) ? ((wd & 0xffffu) | (v << 16)) : ((wd & 0xffff0000u) | v);
+    };
+    for (int i = 0; i < kTileV; ++i) {
+        auto &p = w.prim[i];
+        for (int r = 0; r < (int)p.size(); ++r) {
+            if (r < K0) put16(pw[(size_t)(r / 2) * kTileV + i], r, (uint32_t)p[r].other | ((uint32_t)(p[r].slot & 31) << 11));
+            else ow[p[r].slot - K0 * kTileV] = (uint32_t)i | ((uint32_t)p[r].other << 16);
+        }
+        for (int r = 0; r < (int)w.sec[i].size(); ++r) put16(sw[(size_t)(r / 2) * kTileV + i], r, (uint32_t)w.sec[i][r]);
+    }
+}
+
 static inline uint64_t spread3(uint64_t x) {
     x &= 0x1fffff;
     x = (x | x << 32) & 0x1f00000000ffffull;
@@ -478,10 +661,15 @@ struct DistTopo {
     std::vector<uint32_t> cpair;
     std::vector<uint16_t> vslot, hslot;
     int64_t ntot = 0;
+    // pull layout (use_tma && pull; closed-form K = 1 blocks only): replaces tseg / cpair / vslot / hslot
+    bool pull = false;
+    int ycap = 0;
+    std::vector<int4> ptd;
+    std::vector<uint32_t> pidx;
 };
 
 // Morton vertex order with the short-edge quantization cell (see morton_order)
-void vertex_order(const dxpbd_scene_desc *d, std::vector<int32_t> &vperm) {
+double vertex_order(const dxpbd_scene_desc *d, std::vector<int32_t> &vperm) {
     std::vector<double> len;
     auto edge = [&](int a, int b) {
         double q = 0;
@@ -501,6 +689,7 @@ void vertex_order(const dxpbd_scene_desc *d, std::vector<int32_t> &vperm) {
     }
     if (const char *ev = getenv("DXPBD_MORTON_CELL")) h = atof(ev);   // 0: the extent / 2^21 cell (A/B)
     morton_order(d->x_rest, d->num_vertices, h, vperm, d->vertex_scene);
+    return h;
 }
 
 // Distance constraints: greedy colors in user order (R1), then sorted by (color, owner tile) with
@@ -510,7 +699,7 @@ void dist_topology(const dxpbd_scene_desc *d, int qf, DistTopo &T) {
     const int V = d->num_vertices, E = d->num_dist;
     T.V = V;
     T.E = E;
-    vertex_order(d, T.vperm);
+    const double hcell = vertex_order(d, T.vperm);
     T.nt = (V + kTileV - 1) / kTileV;
     if (!E) return;
     std::vector<int32_t> vinv(V);
@@ -602,6 +791,52 @@ void dist_topology(const dxpbd_scene_desc *d, int qf, DistTopo &T) {
     const int hc = T.hcap;
     T.hpad.assign((size_t)nt * hc, -1);
     for (int t = 0; t < nt; ++t) std::copy(T.halo[t].begin(), T.halo[t].end(), T.hpad.begin() + (size_t)t * hc);
+    const int nth = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
+    auto run_tiles = [&](auto &&work) {
+        std::vector<std::thread> pool;
+        for (int k = 0; k < nth; ++k) pool.emplace_back(work, (int)((int64_t)nt * k / nth), (int)((int64_t)nt * (k + 1) / nth));
+        for (auto &th : pool) th.join();
+    };
+    // pull layout (pull.cuh) for closed-form blocks: count pass, offsets, fill pass
+    const char *pe = getenv("DXPBD_PULL");
+    const char *cge = getenv("DXPBD_CG");
+    if (qf == 1 && !(pe && atoi(pe) == 0) && !(cge && std::string(cge) == "cgcg")) {
+        T.ptd.assign(nt, make_int4(0, 0, 0, 0));
+        auto tile = [&](int t, uint32_t *idx, PullScratch &ws) {
+            pull_tile_layout(t, nc, nt, T.halo[t], cnt.data(), fc.data(), ab_sorted.data(), T.fidx.data(), d->x_rest,
+                             T.vperm.data(), hcell, std::min(kTileV, V - t * kTileV), T.ptd[t], idx, T.tpos.data(),
+                             T.fposv.data(), ws);
+        };
+        run_tiles([&](int t0, int t1) {
+            PullScratch ws;
+            for (int t = t0; t < t1; ++t) tile(t, nullptr, ws);
+        });
+        int64_t qb = 0, ib = 0;
+        int ycap = 0;
+        for (int t = 0; t < nt; ++t) {
+            const int K0 = T.ptd[t].z & 0xff, KS2 = (T.ptd[t].z >> 8) & 0xff, no = T.ptd[t].w;
+            T.ptd[t].x = (int)qb;
+            T.ptd[t].y = (int)ib;
+            qb += (int64_t)K0 * kTileV + no;
+            ib += ((int64_t)((K0 + 1) / 2 + KS2) * kTileV + no + 3) & ~(int64_t)3;
+            ycap = std::max(ycap, K0 * kTileV + no);
+        }
+        if (qb < (int64_t)INT32_MAX && ib < (int64_t)INT32_MAX && ycap <= kPullMaxY && kTileV + hc <= kPullMaxSlot &&
+            pull_smem_bytes(hc, ycap, 2) <= 110 * 1024) {
+            T.pull = true;
+            T.ycap = ycap;
+            T.ntot = qb;
+            T.pidx.assign((size_t)ib + 4, 0xffffffffu);
+            T.fposv.assign(E, -1);
+            T.tpos.assign(E, 0);
+            run_tiles([&](int t0, int t1) {
+                PullScratch ws;
+                for (int t = t0; t < t1; ++t) tile(t, T.pidx.data() + T.ptd[t].y, ws);
+            });
+            return;
+        }
+        T.ptd.clear();
+    }
     T.tseg.resize((size_t)nt * nc);
     for (size_t k = 0; k < (size_t)nt * nc; ++k) T.tseg[k] = make_int4((int)cbase[k], (int)cbase[k + 1], 0, 0);
     T.ntot = cbase.back();
@@ -618,10 +853,7 @@ void dist_topology(const dxpbd_scene_desc *d, int qf, DistTopo &T) {
             tma_tile_layout(t, nc, nt, hc, T.halo[t], t * hc, cnt.data(), fc.data(), ab_sorted.data(), T.fidx.data(),
                             cbase.data(), T.vslot.data(), T.hslot.data(), T.tpos.data(), T.fposv.data(), T.cpair.data(), ws);
     };
-    const int nth = std::max(1, std::min(32, (int)std::thread::hardware_concurrency()));
-    std::vector<std::thread> pool;
-    for (int k = 0; k < nth; ++k) pool.emplace_back(work, (int)((int64_t)nt * k / nth), (int)((int64_t)nt * (k + 1) / nth));
-    for (auto &th : pool) th.join();
+    run_tiles(work);
 }
 
 struct dxpbd_scene {
@@ -664,6 +896,16 @@ struct dxpbd_scene {
     DBuf<float2> d_Qt2b;                // general blocks (qf == 0): (yz, zz) in the same layout
     DBuf<uint16_t> d_vslot, d_hslot;   // tile-local shared-memory slots (own vertices, halo entries)
     DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
+    // pull layout (pull.cuh): closed-form K = 1 blocks; replaces tseg / cpair / vslot / hslot
+    bool pull = false;
+    int ycap = 0, pull_minb = 3;
+    bool pull_keep = true;   // L2 evict-last for the static per-tile data (A/B: DXPBD_PULL_KEEP)
+    size_t pull_smem = 0, pull_rhs_smem = 0;
+    DBuf<int4> d_ptd;
+    DBuf<uint32_t> d_pidx;
+    PullTiles pull_tiles() const {
+        return PullTiles{ntiles, hcap, ycap, d_ptd.p, d_pidx.p, d_hpad.p, qt_read ? qt_read : d_Qt.p};
+    }
     // tets (color-sorted, internal vertex ids)
     DBuf<int4> t_idx;
     DBuf<double> t_Dm, t_vol;
@@ -1498,7 +1740,18 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             return 2;
         }
         int n = 0;
-        if (s->use_tma) {
+        if (s->pull) {
+            const PullTiles pt = s->pull_tiles();
+            float3 *uf = defer ? s->ax.p : nullptr;
+            if (s->pull_minb == 1)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<1><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
+            else if (s->pull_minb == 3 && !s->pull_keep)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<3, false><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
+            else if (s->pull_minb == 3)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<3><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
+            else
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<2><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
+        } else if (s->use_tma) {
             if (s->mv_minb == 3)
                 LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<kMvThreads, kMvMinB - 1><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
                                                                                                          defer ? s->ax.p : nullptr)));
@@ -1808,17 +2061,35 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         s->capm = topo.capm;
         s->use_tma = topo.use_tma;
         (void)nt;
+        s->pull = topo.pull;
         if (s->use_tma) {
-            s->d_tseg.alloc(topo.tseg.size());
-            upload(s->d_tseg.p, topo.tseg.data(), sizeof(int4) * topo.tseg.size(), DXPBD_MEM_HOST, st);
             s->d_hpad.alloc(topo.hpad.size());
             upload(s->d_hpad.p, topo.hpad.data(), sizeof(int) * topo.hpad.size(), DXPBD_MEM_HOST, st);
-            s->d_vslot.alloc(topo.vslot.size());
-            upload(s->d_vslot.p, topo.vslot.data(), sizeof(uint16_t) * topo.vslot.size(), DXPBD_MEM_HOST, st);
-            s->d_hslot.alloc(topo.hslot.size());
-            upload(s->d_hslot.p, topo.hslot.data(), sizeof(uint16_t) * topo.hslot.size(), DXPBD_MEM_HOST, st);
-            s->d_cpair.alloc(topo.cpair.size());
-            upload(s->d_cpair.p, topo.cpair.data(), sizeof(uint32_t) * topo.cpair.size(), DXPBD_MEM_HOST, st);
+            if (s->pull) {
+                s->ycap = topo.ycap;
+                s->d_ptd.alloc(topo.ptd.size());
+                upload(s->d_ptd.p, topo.ptd.data(), sizeof(int4) * topo.ptd.size(), DXPBD_MEM_HOST, st);
+                s->d_pidx.alloc(topo.pidx.size());
+                upload(s->d_pidx.p, topo.pidx.data(), sizeof(uint32_t) * topo.pidx.size(), DXPBD_MEM_HOST, st);
+                s->pull_smem = pull_smem_bytes(s->hcap, s->ycap, 1);
+                s->pull_rhs_smem = pull_smem_bytes(s->hcap, s->ycap, 2);
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
+                if (const char *ev = getenv("DXPBD_PULL_KEEP")) s->pull_keep = atoi(ev) != 0;
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_smem));
+                if (const char *ev = getenv("DXPBD_PULL_MINB")) s->pull_minb = std::max(1, std::min(3, atoi(ev)));
+            } else {
+                s->d_tseg.alloc(topo.tseg.size());
+                upload(s->d_tseg.p, topo.tseg.data(), sizeof(int4) * topo.tseg.size(), DXPBD_MEM_HOST, st);
+                s->d_vslot.alloc(topo.vslot.size());
+                upload(s->d_vslot.p, topo.vslot.data(), sizeof(uint16_t) * topo.vslot.size(), DXPBD_MEM_HOST, st);
+                s->d_hslot.alloc(topo.hslot.size());
+                upload(s->d_hslot.p, topo.hslot.data(), sizeof(uint16_t) * topo.hslot.size(), DXPBD_MEM_HOST, st);
+                s->d_cpair.alloc(topo.cpair.size());
+                upload(s->d_cpair.p, topo.cpair.data(), sizeof(uint32_t) * topo.cpair.size(), DXPBD_MEM_HOST, st);
+            }
             s->d_fpos.alloc(E);
             upload(s->d_fpos.p, topo.fposv.data(), sizeof(int) * E, DXPBD_MEM_HOST, st);
             s->d_tpos.alloc(E);
@@ -2167,7 +2438,12 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         {
             TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
             TmaTiles tt = s->tma_tiles();
-            if (s->use_tma)
+            if (s->pull)
+                LAUNCH(DXPBD_K_RHS, k_rhs_pull<<<s->ntiles, kTileV, s->pull_rhs_smem, st>>>(
+                    s->pull_tiles(), V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
+                    s->r.p, s->u0.p, 0, fuse_start ? s->p.p : nullptr,
+                    CGState{s->cg_sc.p, s->cg_sc.p + (size_t)(s->cg_max_iter + 1) * 4, s->cg_tol * s->cg_tol}));
+            else if (s->use_tma)
                 LAUNCH(DXPBD_K_RHS, k_rhs_tma<<<s->ntiles, kTmaThreads, s->tma_rhs_smem, st>>>(
                     tt, V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
                     s->r.p, s->u0.p, 0, fuse_start ? s->p.p : nullptr,

@@ -603,6 +603,15 @@ DX_INLINE void pcg_ctl_end(const CGState &s, int it) {
     cudaGraphSetConditional(s.cond, stop ? 0u : 1u);
 }
 
+// a / b of two PCG scalars (double accumulators) as a float: one fp32 division when both are in the
+// normal float range (always, in practice), else the fp64 division.  Every kernel forms alpha and
+// beta with this, so the schedules stay bit-identical.
+DX_INLINE float ratio_f(double a, double b) {
+    const float af = (float)a, bf = (float)b;
+    if (fabsf(bf) > 1e-30f && fabsf(bf) < 1e30f && fabsf(af) < 1e30f) return __fdiv_rn(af, bf);
+    return (float)(a / b);
+}
+
 DX_INLINE bool cg_done(const CGState &s, int it) {
     // converged after iteration it-1 ?
     if (it == 0) return false;
@@ -703,7 +712,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_matvec(int it, TileLists L, int V
     const int nv = min(kTileV, V - v0);
     const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;   // p_{it-1}
     float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;         // p_it
-    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
+    const float beta = it > 0 ? ratio_f(s.sc[it * 4 + 1], s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
     for (int i = threadIdx.x; i < kTileV; i += blockDim.x) {
         float3 pv = make_float3(0.f, 0.f, 0.f);
@@ -976,11 +985,11 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
         for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
     }
     // ---- round trip 2: halo values
-    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
+    const float beta = it > 0 ? ratio_f(s.sc[it * 4 + 1], s.sc[(it - 1) * 4 + 1]) : 0.f;
     float alpha_prev = 0.f;
     if (ufix && it > 0) {
         const double pq = s.sc[it * 4 + 0];
-        alpha_prev = pq > 0.0 ? (float)(s.sc[(it - 1) * 4 + 1] / pq) : 0.f;
+        alpha_prev = pq > 0.0 ? ratio_f(s.sc[(it - 1) * 4 + 1], pq) : 0.f;
     }
     float acc[1] = {0.f};
     float hw[NH];
@@ -1549,7 +1558,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         float4 *__restrict__ r = reinterpret_cast<float4 *>(B.r);
         const float4 *__restrict__ q = reinterpret_cast<const float4 *>(B.q);
         const double pq = s.sc[(it + 1) * 4 + 0];
-        const float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
+        const float alpha = pq > 0.0 ? ratio_f(s.sc[it * 4 + 1], pq) : 0.f;
         const float4 w4 = reinterpret_cast<const float4 *>(wv)[t];
         const float w[4] = {w4.x, w4.y, w4.z, w4.w};
         float uu[12], rr[12], pp[12], qq[12];
@@ -1579,7 +1588,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         for (int v = 4 * nq; v < V; ++v) {
             const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
             const double pq = s.sc[(it + 1) * 4 + 0];
-            const float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
+            const float alpha = pq > 0.0 ? ratio_f(s.sc[it * 4 + 1], pq) : 0.f;
             const float w = wv[v];
             float3 uv = B.u[v], rv = B.r[v], pv = p[v], qv = B.q[v];
             uv = uv + alpha * pv;
@@ -1606,7 +1615,7 @@ __global__ void k_cg_ufinal(int V, int K, CGBufs B, CGState s) {
     }
     if (v >= V || K <= 0) return;
     const double pq = s.sc[K * 4 + 0];
-    const float alpha = pq > 0.0 ? (float)(s.sc[(K - 1) * 4 + 1] / pq) : 0.f;
+    const float alpha = pq > 0.0 ? ratio_f(s.sc[(K - 1) * 4 + 1], pq) : 0.f;
     const float3 *__restrict__ p = ((K - 1) & 1) ? B.p1 : B.p0;
     B.u[v] = B.u[v] + alpha * p[v];
 }

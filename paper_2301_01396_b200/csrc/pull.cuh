@@ -1,0 +1,401 @@
+// Pull-style tile matvec / rhs of the adjoint PCG for closed-form K = 1 blocks (QF = 1).
+//
+// Eq. adjointXPBD is solved matrix-free: q = (M + Q_c + Sum_j P_j^T Q_j P_j) p
+// with one symmetric block Q_j = c I + s n n^T per distance constraint (Sec.4.3 l.166-194, PD
+// projected, l.201).  The push kernels (k_cg_matvec_tma) walk a tile's constraints color by color and
+// read-modify-write both endpoints in shared memory (7 sixteen-byte shared accesses per constraint,
+// one barrier per color).  Here every thread owns ONE vertex of the tile and gathers:
+//
+//   primary pass    every constraint of the tile has one primary endpoint i among the tile's own
+//                   vertices; thread i reads Q_j straight from HBM into registers (dense slabs
+//                   [k][i]: the k-th primary constraint of vertex i, coalesced 16-byte loads, no
+//                   staging), the other endpoint's p from shared memory, adds y = Q_j (p_i - p_o)
+//                   to its own q and leaves y in shared memory at slot (k, i);
+//   secondary pass  (one barrier later) the other endpoint, when it is an own vertex too, subtracts
+//                   the y its partner left (position list per vertex).
+//
+// A constraint that crosses two tiles is primary in both (its block is stored in both tiles, as in
+// the push layout), so no y crosses CTAs.  Primary constraints beyond the K0 dense slabs of a tile
+// (vertices with many cross-tile constraints) go to a per-tile overflow list: thread e computes
+// y = Q (p_other - p_own) into slot K0 * kTileV + e and the own vertex subtracts it as a secondary.
+// Per constraint: 3 sixteen-byte shared accesses, 2 barriers per tile, q accumulated in registers.
+// Summation order per vertex is fixed by the layout (deterministic).
+#pragma once
+#include "kernels.cuh"
+
+namespace dx {
+
+constexpr int kPullK0 = 6;      // dense primary slabs (cloth: 12 incident constraints / 2)
+constexpr int kPullKS2 = 4;     // secondary position pairs held in registers (8 secondaries)
+constexpr uint32_t kPullNone = 0xffffu;
+constexpr int kPullMaxSlot = 2046;    // primary entry: other-endpoint slot (11 bits) | lane (5 bits) << 11
+constexpr int kPullMaxY = 32766;      // secondary entry: y slot (15 bits) | add flag << 15
+
+struct PullTiles {
+    int ntiles, hcap, ycap;      // ycap: y slots of the largest tile (K0 * kTileV + overflow entries)
+    const int4 *tdesc;           // per tile {qbase (float4 units), ibase (u32 units), K0 | KS2 << 8, overflow entries}
+    const uint32_t *idx;         // per tile: prim2[(K0+1)/2][kTileV], sec2[KS2][kTileV] (two u16 per word), over[n] (own | other << 16)
+    const int *hpad;             // [tile][hcap] halo vertex ids, -1 padded (slot kTileV + h)
+    const float4 *Q4;            // blocks: per tile [K0][kTileV] dense + [n] overflow
+};
+
+// dynamic shared memory: [mbarrier 16][vector slots (kTileV + hcap) float4] x nvec [Q / y slots ycap float4]
+__host__ __device__ inline size_t pull_smem_bytes(int hcap, int ycap, int nvec = 1) {
+    return 16 + 16 * ((size_t)nvec * (kTileV + hcap) + (size_t)ycap);
+}
+
+// static per-tile data (descriptors, halo ids, inverse masses: ~70 MB at 26 M DoF) is asked to stay
+// in L2 across the PCG iterations (evict-last), so the halo gather's dependent load hits L2
+DX_INLINE uint64_t l2_keep_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+DX_INLINE int ld_keep(const int *a, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+DX_INLINE float ld_keep(const float *a, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+DX_INLINE int4 ld_keep(const int4 *a, uint64_t pol) {
+    int4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a), "l"(pol));
+    return v;
+}
+
+struct PullRegs {   // a thread's slice of the tile's index data
+    uint32_t pr[kPullK0 / 2], se[kPullKS2], ov;
+};
+
+DX_INLINE void pull_load(PullRegs &R, const PullTiles &T, const int4 td, const int i) {
+    const int K0 = td.z & 0xff, KS2 = (td.z >> 8) & 0xff, K02 = (K0 + 1) >> 1;
+    const uint32_t *ix = T.idx + td.y;
+#pragma unroll
+    for (int k = 0; k < kPullK0 / 2; ++k) R.pr[k] = k < K02 ? __ldcs(ix + k * kTileV + i) : 0xffffffffu;
+    ix += K02 * kTileV;
+#pragma unroll
+    for (int k = 0; k < kPullKS2; ++k) R.se[k] = k < KS2 ? __ldcs(ix + k * kTileV + i) : 0xffffffffu;
+    ix += KS2 * kTileV;
+    R.ov = i < td.w ? __ldcs(ix + i) : 0xffffffffu;
+}
+
+// one thread: the tile's whole Q region (dense slabs + overflow entries, contiguous) into the y slots
+// with one bulk copy (cp.async.bulk -> mbarrier); every y later overwrites the block it came from
+DX_INLINE void pull_issue(uint64_t *bar, float4 *yb, const PullTiles &T, const int4 td) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = (uint32_t)((td.z & 0xff) * kTileV + td.w) * 16u;
+    mbar_expect_tx(bar, bytes);
+    if (bytes) bulk_g2s(yb, T.Q4 + td.x, bytes, bar);
+}
+
+// primary entry (16 bits): other-endpoint slot (11 bits; 0x7ff: none) | lane of the thread's slot << 11
+DX_INLINE float3 pull_dense(const uint32_t en, const int k, const int i, const float3 pv, const float4 *sp,
+                            float4 *yb, float4 *keep) {
+    const uint32_t o = en & 0x7ffu;
+    float3 y = make_float3(0.f, 0.f, 0.f);
+    if (o != 0x7ffu) {
+        const int pos = k * kTileV + (i & ~31) + (int)(en >> 11);
+        const float4 Q = yb[pos];
+        if (keep) *keep = Q;
+        y = qmul_iso_rank1(Q, pv - f3(sp[o]));
+        yb[pos] = make_float4(y.x, y.y, y.z, 0.f);
+    }
+    return y;
+}
+
+// primary pass for one vector: sp holds the vector at every slot of the tile, yb the blocks; returns
+// the sum of the thread's own primaries y = Q (p_i - p_o) and leaves every y in place of its block.
+// KEEP: the blocks are also returned in Qk (registers) for a second pass (pull_primary_regs).
+template <bool KEEP>
+DX_INLINE float3 pull_primary(const PullRegs &R, const PullTiles &T, const int4 td, const int i, const float3 pv,
+                              const float4 *sp, float4 *yb, float4 (&Qk)[kPullK0 + 1]) {
+    const int K0 = td.z & 0xff;
+    float3 qv = make_float3(0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < kPullK0; ++k)
+        if (k < K0) qv = qv + pull_dense((R.pr[k >> 1] >> (16 * (k & 1))) & 0xffffu, k, i, pv, sp, yb, KEEP ? &Qk[k] : nullptr);
+    for (int e = i; e < td.w; e += kTileV) {   // overflow entries (own | other << 16), y = Q (p_own - p_other)
+        uint32_t pr = R.ov;
+        if (e >= kTileV) pr = T.idx[td.y + (((K0 + 1) >> 1) + ((td.z >> 8) & 0xff)) * kTileV + e];   // rare
+        const float4 Qo = yb[K0 * kTileV + e];
+        if (KEEP && e < kTileV) Qk[kPullK0] = Qo;
+        const float3 y = qmul_iso_rank1(Qo, f3(sp[pr & 0xffffu]) - f3(sp[pr >> 16]));
+        yb[K0 * kTileV + e] = make_float4(y.x, y.y, y.z, 0.f);
+    }
+    return qv;
+}
+
+// second pass with the blocks kept in registers (entries beyond the first kTileV overflow entries
+// are re-read from HBM)
+DX_INLINE float3 pull_primary_regs(const PullRegs &R, const PullTiles &T, const int4 td, const int i, const float3 pv,
+                                   const float4 *sp, float4 *yb, const float4 (&Qk)[kPullK0 + 1]) {
+    const int K0 = td.z & 0xff;
+    float3 qv = make_float3(0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < kPullK0; ++k)
+        if (k < K0) {
+            const uint32_t en = (R.pr[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+            if ((en & 0x7ffu) != 0x7ffu) {
+                const float3 y = qmul_iso_rank1(Qk[k], pv - f3(sp[en & 0x7ffu]));
+                qv = qv + y;
+                yb[k * kTileV + (i & ~31) + (int)(en >> 11)] = make_float4(y.x, y.y, y.z, 0.f);
+            }
+        }
+    for (int e = i; e < td.w; e += kTileV) {
+        uint32_t pr = R.ov;
+        float4 Q = Qk[kPullK0];
+        if (e >= kTileV) {   // rare
+            pr = T.idx[td.y + (((K0 + 1) >> 1) + ((td.z >> 8) & 0xff)) * kTileV + e];
+            Q = T.Q4[td.x + K0 * kTileV + e];
+        }
+        const float3 y = qmul_iso_rank1(Q, f3(sp[pr & 0xffffu]) - f3(sp[pr >> 16]));
+        yb[K0 * kTileV + e] = make_float4(y.x, y.y, y.z, 0.f);
+    }
+    return qv;
+}
+
+// secondary pass: signed sum of the y slots listed for vertex i (entry: y slot (15 bits) | add flag
+// << 15, else subtract)
+DX_INLINE float3 pull_secondary(const PullRegs &R, const PullTiles &T, const int4 td, const int i, const float4 *yb) {
+    float3 s = make_float3(0.f, 0.f, 0.f);
+    auto take = [&](uint32_t en) {
+        if (en != kPullNone) {
+            const float3 y = f3(yb[en & 0x7fffu]);
+            s = (en & 0x8000u) ? s + y : s - y;
+        }
+    };
+#pragma unroll
+    for (int k = 0; k < kPullKS2; ++k) {
+        take(R.se[k] & 0xffffu);
+        take(R.se[k] >> 16);
+    }
+    const int KS2 = (td.z >> 8) & 0xff;
+    if (KS2 > kPullKS2) {   // rare: vertices with more than 8 secondaries
+        const uint32_t *sx = T.idx + td.y + (((td.z & 0xff) + 1) >> 1) * kTileV;
+        for (int k = kPullKS2; k < KS2; ++k) {
+            const uint32_t w = sx[k * kTileV + i];
+            take(w & 0xffffu);
+            take(w >> 16);
+        }
+    }
+    return s;
+}
+
+// PCG matvec, same contract as k_cg_matvec_tma: p_it for own and halo vertices (fused update),
+// q = A p for own vertices, p.q into slot it + 1, optional deferred u += alpha_{it-1} p_{it-1}.
+constexpr int kPullScale = kTileV < 512 ? 512 / kTileV : 1;   // CTAs per SM are given per 512 threads
+
+template <int MINB, bool KEEP = true>
+__global__ void __launch_bounds__(kTileV, MINB * kPullScale) k_cg_matvec_pull(int it, PullTiles T, int V, const float *__restrict__ Qc,
+                                                                  CGBufs B, const float *__restrict__ wv, CGState s,
+                                                                  int t0 = 0, float3 *__restrict__ ufix = nullptr) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
+    float4 *sp = reinterpret_cast<float4 *>(smem_raw + 16);
+    float4 *yb = sp + kTileV + T.hcap;
+    it = cg_iter(s, it);
+    if (s.pp) {   // graph mode: this substep's buffers
+        const PcgPtrs pp = *s.pp;
+        T.Q4 = pp.Qt;
+        if (Qc) Qc = pp.Qc;
+        B.u = pp.u;
+        if (ufix) ufix = pp.u;
+    }
+    const int t = blockIdx.x + t0, i = threadIdx.x;
+    const int v0 = t * kTileV;
+    const int nv = min(kTileV, V - v0);
+    const int hcap = T.hcap;
+    // ---- round trip 1: descriptor, halo id, own vector values
+    const bool done = cg_done(s, it + 1);
+    const uint64_t keep = l2_keep_policy();
+    const int4 td = KEEP ? ld_keep(T.tdesc + t, keep) : T.tdesc[t];
+    const int v = min(v0 + i, V - 1);
+    const float w = KEEP ? ld_keep(wv + v, keep) : wv[v];
+    const int hv = i < hcap ? (KEEP ? ld_keep(T.hpad + (size_t)t * hcap + i, keep) : T.hpad[(size_t)t * hcap + i]) : -1;
+    const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
+    float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
+    const float3 z3 = make_float3(0.f, 0.f, 0.f);
+    const float3 ro = it > 0 ? B.r[v] : pnew[v];
+    const float3 po = it > 0 ? pold[v] : z3;
+    const float3 uo = (ufix && it > 0) ? ufix[v] : z3;
+    if (done) return;
+    // ---- round trip 2: blocks (bulk copy), index data (registers), halo values
+    if (i == kTileV - 32) pull_issue(bar, yb, T, td);
+    PullRegs R;
+    pull_load(R, T, td, i);
+    const float beta = it > 0 ? ratio_f(s.sc[it * 4 + 1], s.sc[(it - 1) * 4 + 1]) : 0.f;
+    float alpha_prev = 0.f;
+    if (ufix && it > 0) {
+        const double pq = s.sc[it * 4 + 0];
+        alpha_prev = pq > 0.0 ? ratio_f(s.sc[(it - 1) * 4 + 1], pq) : 0.f;
+    }
+    const int hvv = max(hv, 0);
+    const float hw = KEEP ? ld_keep(wv + hvv, keep) : wv[hvv];
+    const float3 hr = it > 0 ? B.r[hvv] : pnew[hvv];
+    const float3 hp = it > 0 ? pold[hvv] : z3;
+    float3 pv = z3, qv = z3;
+    if (i < nv) {
+        if (w > 0.f) {
+            pv = it > 0 ? make_float3(w * ro.x + beta * po.x, w * ro.y + beta * po.y, w * ro.z + beta * po.z) : ro;
+            qv = (1.f / w) * pv;
+            if (Qc) {
+                Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v], Qc[4 * (size_t)V + v],
+                              Qc[5 * (size_t)V + v]};
+                qv = qv + sym3_mul(A, pv);
+            }
+        }
+        if (it > 0) pnew[v] = pv;
+        if (ufix && it > 0) ufix[v] = uo + alpha_prev * po;   // deferred u += alpha_{it-1} p_{it-1}
+    }
+    sp[i] = make_float4(pv.x, pv.y, pv.z, 0.f);
+    if (hv >= 0) {
+        float3 ph = z3;
+        if (hw > 0.f)
+            ph = it > 0 ? make_float3(hw * hr.x + beta * hp.x, hw * hr.y + beta * hp.y, hw * hr.z + beta * hp.z) : hr;
+        sp[kTileV + i] = make_float4(ph.x, ph.y, ph.z, 0.f);
+    }
+    for (int h = i + kTileV; h < hcap; h += kTileV) {   // rare: large halos
+        const int u = T.hpad[(size_t)t * hcap + h];
+        if (u >= 0) {
+            const float3 ph = halo_p(it, u, beta, B.r, pold, pnew, wv);
+            sp[kTileV + h] = make_float4(ph.x, ph.y, ph.z, 0.f);
+        }
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    float4 Qk[kPullK0 + 1];
+    qv = qv + pull_primary<false>(R, T, td, i, pv, sp, yb, Qk);
+    __syncthreads();
+    qv = qv + pull_secondary(R, T, td, i, yb);
+    float acc[1] = {0.f};
+    if (i < nv) {
+        const bool fr = w > 0.f;
+        B.q[v] = fr ? qv : z3;
+        if (fr) acc[0] = dot3(pv, qv);
+    }
+    block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
+}
+
+// rhs with warm start, same contract as k_rhs_tma: b = M u - Q_n y + dphi, r0 = b - A_n (u + du),
+// u0 = u + du; with p0out the PCG start is fused.  A_dist is applied to y and to z = y + u0 in
+// two pull passes that share the y slots.
+__global__ void __launch_bounds__(kTileV, 2 * kPullScale) k_rhs_pull(PullTiles T, int V, const float *__restrict__ Qc,
+                                                        const float3 *__restrict__ u, const float3 *__restrict__ uprev,
+                                                        const float3 *__restrict__ uprev2, const float3 *__restrict__ y,
+                                                        const double4 *__restrict__ xkey, const float *__restrict__ target,
+                                                        const float *__restrict__ weights, const float *__restrict__ wv,
+                                                        float3 *__restrict__ bout, float3 *__restrict__ r0out,
+                                                        float3 *__restrict__ u0out, int t0 = 0,
+                                                        float3 *__restrict__ p0out = nullptr, CGState cs = CGState{}) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int hcap = T.hcap;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
+    float4 *sy = reinterpret_cast<float4 *>(smem_raw + 16);
+    float4 *sz = sy + kTileV + hcap;
+    float4 *yb = sz + kTileV + hcap;
+    const int t = blockIdx.x + t0, i = threadIdx.x;
+    const int v0 = t * kTileV;
+    const int nv = min(kTileV, V - v0);
+    const float3 z3 = make_float3(0.f, 0.f, 0.f);
+    // ---- round trip 1
+    const int4 td = T.tdesc[t];
+    const int v = min(v0 + i, V - 1);
+    const float w = wv[v];
+    const int hv = i < hcap ? T.hpad[(size_t)t * hcap + i] : -1;
+    const float3 yo = y[v], uo = u[v], po = uprev[v], p2o = uprev2 ? uprev2[v] : z3;
+    double4 xo = make_double4(0, 0, 0, 0);
+    float3 to = z3;
+    float Wo = 1.f;
+    if (target) {
+        xo = xkey[v];
+        to = make_float3(target[3 * v], target[3 * v + 1], target[3 * v + 2]);
+        if (weights) Wo = weights[v];
+    }
+    // ---- round trip 2
+    if (i == kTileV - 32) pull_issue(bar, yb, T, td);
+    PullRegs R;
+    pull_load(R, T, td, i);
+    const int hvv = max(hv, 0);
+    const float3 hy = y[hvv], hu = u[hvv], hp = uprev[hvv], hp2 = uprev2 ? uprev2[hvv] : z3;
+    float3 yv = z3, zv = z3, bb = z3, rr = z3;
+    if (i < nv) {
+        yv = yo;
+        // warm start u0 = u + dv: linear 2u_{n+1} - u_{n+2}, or quadratic 3u_{n+1} - 3u_{n+2} + u_{n+3}
+        const float3 dv = uprev2 ? 2.f * uo - 3.f * po + p2o : uo - po;
+        const float3 u0 = uo + dv;
+        zv = yv + u0;
+        u0out[v] = w > 0.f ? u0 : z3;
+        if (w > 0.f) {
+            bb = (1.f / w) * uo;
+            rr = (-1.f / w) * dv;
+            if (Qc) {
+                Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v], Qc[4 * (size_t)V + v],
+                              Qc[5 * (size_t)V + v]};
+                bb = bb - sym3_mul(A, yv);
+                rr = rr - sym3_mul(A, zv);
+            }
+            if (target) {
+                const float3 g = Wo * make_float3((float)(xo.x - to.x), (float)(xo.y - to.y), (float)(xo.z - to.z));
+                bb = bb + g;
+                rr = rr + g;
+            }
+        }
+    }
+    sy[i] = make_float4(yv.x, yv.y, yv.z, 0.f);
+    sz[i] = make_float4(zv.x, zv.y, zv.z, 0.f);
+    if (hv >= 0) {
+        const float3 dh = uprev2 ? 2.f * hu - 3.f * hp + hp2 : hu - hp;
+        const float3 zh = hy + hu + dh;
+        sy[kTileV + i] = make_float4(hy.x, hy.y, hy.z, 0.f);
+        sz[kTileV + i] = make_float4(zh.x, zh.y, zh.z, 0.f);
+    }
+    for (int h = i + kTileV; h < hcap; h += kTileV) {   // rare: large halos
+        const int q = T.hpad[(size_t)t * hcap + h];
+        if (q < 0) continue;
+        const float3 uh = u[q];
+        const float3 dh = uprev2 ? 2.f * uh - 3.f * uprev[q] + uprev2[q] : uh - uprev[q];
+        const float3 yh = y[q], zh = yh + uh + dh;
+        sy[kTileV + h] = make_float4(yh.x, yh.y, yh.z, 0.f);
+        sz[kTileV + h] = make_float4(zh.x, zh.y, zh.z, 0.f);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    float4 Qk[kPullK0 + 1];
+    float3 ay = pull_primary<true>(R, T, td, i, yv, sy, yb, Qk);
+    __syncthreads();
+    ay = ay + pull_secondary(R, T, td, i, yb);
+    __syncthreads();
+    float3 az = pull_primary_regs(R, T, td, i, zv, sz, yb, Qk);
+    __syncthreads();
+    az = az + pull_secondary(R, T, td, i, yb);
+    // epilogue; with p0out the PCG start is fused (k_cg_start): p_0 = M^-1 r_0, slot 0 gets r.z and
+    // r.r, cs.bnorm2 gets |b|^2
+    float acc[3] = {0.f, 0.f, 0.f};
+    if (i < nv) {
+        const bool fr = w > 0.f;
+        const float3 bv = fr ? bb - ay : z3, rv = fr ? rr - az : z3;
+        bout[v] = bv;
+        r0out[v] = rv;
+        if (p0out) {
+            p0out[v] = w * rv;
+            const float r2 = dot3(rv, rv);
+            acc[0] = w * r2;
+            acc[1] = r2;
+            acc[2] = dot3(bv, bv);
+        }
+    }
+    if (p0out) {
+        float a2[2] = {acc[0], acc[1]};
+        block_reduce_add<2>(a2, cs.sc + 1);
+        float b1[1] = {acc[2]};
+        block_reduce_add<1>(b1, cs.bnorm2);
+    }
+}
+
+}  // namespace dx

@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_cg_tetv(int it, int nbt, int V
     if (cg_done(s, it + 1)) return;
     const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;   // p_{it-1}
     float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;         // p_it
-    const float beta = it > 0 ? (float)(s.sc[it * 4 + 1] / s.sc[(it - 1) * 4 + 1]) : 0.f;
+    const float beta = it > 0 ? ratio_f(s.sc[it * 4 + 1], s.sc[(it - 1) * 4 + 1]) : 0.f;
     float acc[1] = {0.f};
     if ((int)blockIdx.x < nbt) {
         const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update_tet(int V, int it, CGBufs 
     if (v < V) {
         const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
         const double pq = s.sc[(it + 1) * 4 + 0];
-        const float alpha = pq > 0.0 ? (float)(s.sc[it * 4 + 1] / pq) : 0.f;
+        const float alpha = pq > 0.0 ? ratio_f(s.sc[it * 4 + 1], pq) : 0.f;
         const float w = wv[v];
         const float3 pv = p[v];
         B.u[v] = B.u[v] + alpha * pv;
