@@ -188,12 +188,19 @@ def algo_bytes(cls, st, units_per_launch=None):
 
 
 def layout_overhead_bytes(cls, st):
-    """Bytes per launch this layout moves beyond the method's: the TMA matvec re-reads halo vertices of
-    neighbouring tiles (id 4 + slot 2 + w 4 + r 12 + p_old 12 = 34 B per halo entry) and streams a copy of
-    each cross-tile constraint in the b-endpoint's tile (20 B)."""
-    if cls == "cg_dist":
-        return 20.0 * st["n_foreign"] + 34.0 * st["halo_total"]
-    return 0.0
+    """Bytes per launch the tile layout moves beyond the method's.  Push layout (k_cg_matvec_tma): halo
+    vertices of neighbouring tiles are re-read (id 4 + slot 2 + w 4 + r 12 + p_old 12 = 34 B per halo
+    entry) and each cross-tile constraint is streamed again in the b-endpoint's tile (20 B).  Pull layout
+    (k_cg_matvec_pull): every block slot of the layout (constraints, cross-tile copies, padding of the
+    dense slabs) 16 B, its index words 4 B each, a 16-byte descriptor per tile, 32 B per halo entry
+    (id 4 + w 4 + r 12 + p_old 12) and 76 B per vertex (no slot table), minus the method's 20 E + 78 V."""
+    if cls != "cg_dist":
+        return 0.0
+    if st.get("pull"):
+        actual = (16.0 * st["block_slots"] + 4.0 * st["pull_index_words"] + 16.0 * st["tiles"] + 32.0 * st["halo_total"]
+                  + 76.0 * st["V"])
+        return actual - algo_bytes("cg_dist", st)
+    return 20.0 * st["n_foreign"] + 34.0 * st["halo_total"]
 
 
 def unique_step_bytes(st, S, M, E, V, cg_mv, cg_it):

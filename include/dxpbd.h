@@ -164,7 +164,7 @@ int dxpbd_set_params(dxpbd_scene *scene, int32_t kind, const float *data, int64_
 int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out_len,
                    int32_t *num_colors);
 
-/* Statistics into HOST out[0..n), n <= 20:
+/* Statistics into HOST out[0..n), n <= 24:
  *  0: total PCG iterations of the last backward, 1: max PCG iterations of one solve,
  *  2: kernel launches of the last forward, 3: of the last backward, 4: substeps solved,
  *  5: worst final relative residual, 6: last loss, 7: foreign constraint entries (tiled PCG),
@@ -173,7 +173,9 @@ int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out
  *      matvec per solve for the single-reduction PCG), 15: substeps of the last backward whose
  *      derivative blocks came from the forward's cache (no replay),
  *  16: wave tiles of the wavefront sweep (0: per-color launches), 17: its work items per substep,
- *  18: its ticket lag L (bandwidth of the wave-tile order + 1), 19: most neighbours of a wave tile. */
+ *  18: its ticket lag L (bandwidth of the wave-tile order + 1), 19: most neighbours of a wave tile,
+ *  20: pull layout on (closed-form K = 1 blocks, csrc/pull.cuh), 21: block slots of the tile layout
+ *      (constraints + cross-tile copies + padding), 22: 32-bit index words of the pull layout. */
 int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
 
 /* ---- Vertex-partitioned domain decomposition -------------------------

@@ -344,13 +344,13 @@ def dxpbd_coloring(scene: DxScene, family: int = 0) -> np.ndarray:
 
 
 def dxpbd_stats(scene: DxScene) -> dict:
-    out = np.zeros(20, np.float64)
-    _check(lib().dxpbd_stats(scene.handle, out.ctypes.data, 20), "dxpbd_stats")
+    out = np.zeros(24, np.float64)
+    _check(lib().dxpbd_stats(scene.handle, out.ctypes.data, 24), "dxpbd_stats")
     return dict(cg_iters_total=out[0], cg_iters_max=out[1], fwd_launches=out[2], bwd_launches=out[3],
                 solves=out[4], worst_relres=out[5], loss=out[6], n_foreign=out[7], halo_total=out[8],
                 E=out[9], V=out[10], T=out[11], tiles=out[12], tma=bool(out[13]), cg_matvecs=out[14],
                 cached_substeps=out[15], wave_tiles=out[16], wave_items=out[17], wave_lag=out[18],
-                wave_max_neighbours=out[19])
+                wave_max_neighbours=out[19], pull=bool(out[20]), block_slots=out[21], pull_index_words=out[22])
 
 
 def dxpbd_profile(scene: DxScene, enable: bool = True):

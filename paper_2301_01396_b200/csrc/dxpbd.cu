@@ -898,8 +898,11 @@ struct dxpbd_scene {
     DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
     // pull layout (pull.cuh): closed-form K = 1 blocks; replaces tseg / cpair / vslot / hslot
     bool pull = false;
-    int ycap = 0, pull_minb = 3;
+    int ycap = 0, pull_minb = 2;
     bool pull_keep = true;   // L2 evict-last for the static per-tile data (A/B: DXPBD_PULL_KEEP)
+    bool pull_persist = true;   // persistent matvec CTAs with next-tile prefetch (A/B: DXPBD_PULL_PERSIST)
+    size_t pull_psmem = 0;
+    int num_sms = 148;
     size_t pull_smem = 0, pull_rhs_smem = 0;
     DBuf<int4> d_ptd;
     DBuf<uint32_t> d_pidx;
@@ -1029,7 +1032,7 @@ struct dxpbd_scene {
     bool have_grads = false;
 
     // stats
-    double stats[20] = {0};
+    double stats[24] = {0};
     // opt-in event profiler
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -1743,7 +1746,11 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         if (s->pull) {
             const PullTiles pt = s->pull_tiles();
             float3 *uf = defer ? s->ax.p : nullptr;
-            if (s->pull_minb == 1)
+            if (s->pull_persist && s->pull_minb == 3)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull_p<3><<<std::min(s->ntiles, 3 * s->num_sms), kTileV, s->pull_psmem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, s->ntiles, uf)));
+            else if (s->pull_persist)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull_p<2><<<std::min(s->ntiles, 2 * s->num_sms), kTileV, s->pull_psmem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, s->ntiles, uf)));
+            else if (s->pull_minb == 1)
                 LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<1><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
             else if (s->pull_minb == 3 && !s->pull_keep)
                 LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<3, false><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
@@ -2078,6 +2085,11 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
                 if (const char *ev = getenv("DXPBD_PULL_KEEP")) s->pull_keep = atoi(ev) != 0;
+                s->pull_psmem = pull_persist_smem_bytes(s->hcap, s->ycap);
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull_p<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_psmem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull_p<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_psmem));
+                DX_CHECK_CUDA(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, s->device));
+                if (const char *ev = getenv("DXPBD_PULL_PERSIST")) s->pull_persist = atoi(ev) != 0;
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_smem));
                 if (const char *ev = getenv("DXPBD_PULL_MINB")) s->pull_minb = std::max(1, std::min(3, atoi(ev)));
             } else {
@@ -2728,7 +2740,10 @@ int dxpbd_stats(dxpbd_scene *s, double *out, int32_t n) {
     s->stats[17] = wave ? s->wave_nitems : 0;
     s->stats[18] = wave ? s->wave_L : 0;
     s->stats[19] = wave ? s->wave_maxnbr : 0;
-    for (int k = 0; k < n && k < 20; ++k) out[k] = s->stats[k];
+    s->stats[20] = s->pull ? 1.0 : 0.0;
+    s->stats[21] = s->use_tma ? (double)(s->d_Qt.n - 1) : 0.0;
+    s->stats[22] = s->pull ? (double)s->d_pidx.n : 0.0;
+    for (int k = 0; k < n && k < 24; ++k) out[k] = s->stats[k];
     DX_API_END
 }
 

@@ -282,6 +282,146 @@ __global__ void __launch_bounds__(kTileV, MINB * kPullScale) k_cg_matvec_pull(in
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
+// Persistent variant: a CTA walks tiles t = first + k * gridDim.x.  While tile k computes, the next
+// tile's descriptor is loaded and its halo ids are bulk-copied into shared memory; its blocks are
+// bulk-copied into the y slots as soon as tile k's secondary pass has read them.  A tile therefore
+// starts with its descriptor, halo ids and (in flight) blocks at hand and issues ALL its loads in one
+// round trip (the one-tile-per-CTA kernel needs descriptor -> index data and halo ids -> halo
+// values).  p.q is accumulated over the CTA's tiles and reduced once.
+// dynamic shared memory: [3 mbarriers 32][2 descriptors 32][2 x hcap halo ids][vector slots][Q / y slots]
+__host__ __device__ inline size_t pull_persist_smem_bytes(int hcap, int ycap) {
+    return 64 + 8 * (size_t)hcap + 16 * ((size_t)(kTileV + hcap) + (size_t)ycap);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kTileV, MINB) k_cg_matvec_pull_p(int it, PullTiles T, int V, const float *__restrict__ Qc,
+                                                                    CGBufs B, const float *__restrict__ wv, CGState s,
+                                                                    int t0, int ntiles, float3 *__restrict__ ufix) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bar_q = reinterpret_cast<uint64_t *>(smem_raw);          // blocks of the current tile
+    uint64_t *bar_h = bar_q + 1;                                        // [2] halo ids
+    int4 *s_td = reinterpret_cast<int4 *>(smem_raw + 32);               // [2]
+    const int hcap = T.hcap;
+    int *s_hp = reinterpret_cast<int *>(smem_raw + 64);                 // [2][hcap]
+    float4 *sp = reinterpret_cast<float4 *>(smem_raw + 64 + 8 * (size_t)hcap);
+    float4 *yb = sp + kTileV + hcap;
+    it = cg_iter(s, it);
+    if (s.pp) {   // graph mode: this substep's buffers
+        const PcgPtrs pp = *s.pp;
+        T.Q4 = pp.Qt;
+        if (Qc) Qc = pp.Qc;
+        B.u = pp.u;
+        if (ufix) ufix = pp.u;
+    }
+    if (cg_done(s, it + 1)) return;
+    const int i = threadIdx.x;
+    const bool lead = i == kTileV - 32;
+    const int tend = t0 + ntiles;
+    int t = t0 + blockIdx.x;
+    if (t >= tend) return;
+    const uint64_t keep = l2_keep_policy();
+    const float3 *__restrict__ pold = (it & 1) ? B.p0 : B.p1;
+    float3 *__restrict__ pnew = (it & 1) ? B.p1 : B.p0;
+    const float3 z3 = make_float3(0.f, 0.f, 0.f);
+    const float beta = it > 0 ? ratio_f(s.sc[it * 4 + 1], s.sc[(it - 1) * 4 + 1]) : 0.f;
+    float alpha_prev = 0.f;
+    if (ufix && it > 0) {
+        const double pq = s.sc[it * 4 + 0];
+        alpha_prev = pq > 0.0 ? ratio_f(s.sc[(it - 1) * 4 + 1], pq) : 0.f;
+    }
+    const uint32_t hbytes = (uint32_t)hcap * 4u;
+    if (lead) {   // first tile: nothing was prefetched
+        mbar_init(bar_q, 1);
+        mbar_init(bar_h, 1);
+        mbar_init(bar_h + 1, 1);
+        fence_mbar_init();
+        const int4 td0 = T.tdesc[t];
+        s_td[0] = td0;
+        mbar_expect_tx(bar_h, hbytes);
+        bulk_g2s(s_hp, T.hpad + (size_t)t * hcap, hbytes, bar_h);
+        const uint32_t bytes = (uint32_t)((td0.z & 0xff) * kTileV + td0.w) * 16u;
+        mbar_expect_tx(bar_q, bytes);
+        if (bytes) bulk_g2s(yb, T.Q4 + td0.x, bytes, bar_q);
+    }
+    __syncthreads();
+    float acc[1] = {0.f};
+    for (int k = 0; t < tend; t += gridDim.x, ++k) {
+        const int cur = k & 1, tn = t + gridDim.x;
+        const int4 td = s_td[cur];
+        const int v0 = t * kTileV;
+        const int nv = min(kTileV, V - v0);
+        const int v = min(v0 + i, V - 1);
+        // ---- one round trip: own values, index data, halo values
+        const float w = ld_keep(wv + v, keep);
+        const float3 ro = it > 0 ? B.r[v] : pnew[v];
+        const float3 po = it > 0 ? pold[v] : z3;
+        const float3 uo = (ufix && it > 0) ? ufix[v] : z3;
+        PullRegs R;
+        pull_load(R, T, td, i);
+        int4 tdn = make_int4(0, 0, 0, 0);
+        if (lead && tn < tend) {   // next tile: descriptor (register), halo ids (bulk copy)
+            tdn = T.tdesc[tn];
+            mbar_expect_tx(bar_h + (cur ^ 1), hbytes);
+            bulk_g2s(s_hp + (size_t)(cur ^ 1) * hcap, T.hpad + (size_t)tn * hcap, hbytes, bar_h + (cur ^ 1));
+        }
+        mbar_wait(bar_h + cur, (uint32_t)((k >> 1) & 1));
+        const int *hp_s = s_hp + (size_t)cur * hcap;
+        const int hv = i < hcap ? hp_s[i] : -1;
+        const int hvv = max(hv, 0);
+        const float hw = ld_keep(wv + hvv, keep);
+        const float3 hr = it > 0 ? B.r[hvv] : pnew[hvv];
+        const float3 hp = it > 0 ? pold[hvv] : z3;
+        float3 pv = z3, qv = z3;
+        if (i < nv) {
+            if (w > 0.f) {
+                pv = it > 0 ? make_float3(w * ro.x + beta * po.x, w * ro.y + beta * po.y, w * ro.z + beta * po.z) : ro;
+                qv = (1.f / w) * pv;
+                if (Qc) {
+                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v], Qc[4 * (size_t)V + v],
+                                  Qc[5 * (size_t)V + v]};
+                    qv = qv + sym3_mul(A, pv);
+                }
+            }
+            if (it > 0) pnew[v] = pv;
+            if (ufix && it > 0) ufix[v] = uo + alpha_prev * po;   // deferred u += alpha_{it-1} p_{it-1}
+        }
+        sp[i] = make_float4(pv.x, pv.y, pv.z, 0.f);
+        if (hv >= 0) {
+            float3 ph = z3;
+            if (hw > 0.f)
+                ph = it > 0 ? make_float3(hw * hr.x + beta * hp.x, hw * hr.y + beta * hp.y, hw * hr.z + beta * hp.z) : hr;
+            sp[kTileV + i] = make_float4(ph.x, ph.y, ph.z, 0.f);
+        }
+        for (int h = i + kTileV; h < hcap; h += kTileV) {   // rare: large halos
+            const int u = hp_s[h];
+            if (u >= 0) {
+                const float3 ph = halo_p(it, u, beta, B.r, pold, pnew, wv);
+                sp[kTileV + h] = make_float4(ph.x, ph.y, ph.z, 0.f);
+            }
+        }
+        if (lead && tn < tend) s_td[cur ^ 1] = tdn;
+        __syncthreads();
+        mbar_wait(bar_q, (uint32_t)(k & 1));
+        float4 Qk[kPullK0 + 1];
+        qv = qv + pull_primary<false>(R, T, td, i, pv, sp, yb, Qk);
+        __syncthreads();
+        qv = qv + pull_secondary(R, T, td, i, yb);
+        __syncthreads();   // every y slot has been read: the next tile's blocks may land
+        if (lead && tn < tend) {
+            fence_proxy_async();
+            const uint32_t bytes = (uint32_t)((tdn.z & 0xff) * kTileV + tdn.w) * 16u;
+            mbar_expect_tx(bar_q, bytes);
+            if (bytes) bulk_g2s(yb, T.Q4 + tdn.x, bytes, bar_q);
+        }
+        if (i < nv) {
+            const bool fr = w > 0.f;
+            B.q[v] = fr ? qv : z3;
+            if (fr) acc[0] += dot3(pv, qv);
+        }
+    }
+    block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
+}
+
 // rhs with warm start, same contract as k_rhs_tma: b = M u - Q_n y + dphi, r0 = b - A_n (u + du),
 // u0 = u + du; with p0out the PCG start is fused.  A_dist is applied to y and to z = y + u0 in
 // two pull passes that share the y slots.
