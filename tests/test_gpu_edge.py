@@ -259,6 +259,31 @@ def test_wave_sweep_bit_identical(monkeypatch, case):
             np.testing.assert_array_equal(ga[k], gb[k], err_msg=f"{name} g={g} {k}")
 
 
+@pytest.mark.parametrize("case", range(4))
+def test_pull_matvec_matches_push(monkeypatch, case):
+    """The pull-style PCG kernels (pull.cuh: one vertex per thread, persistent and one tile per CTA)
+    solve the same systems as the push kernels (k_cg_matvec_tma / k_rhs_tma): identical positions,
+    loss and gradients up to the summation order of the solves (1e-5), same iteration counts +- 1."""
+    name, mk, grads = _wave_cases()[case]
+    s = mk()
+    frames = s.frames
+    monkeypatch.setenv("DXPBD_PULL", "0")
+    xa, la, ga, sa = _run_all(s, grads, frames)
+    assert not sa["pull"]
+    monkeypatch.setenv("DXPBD_PULL", "1")
+    for persist in ("1", "0"):
+        monkeypatch.setenv("DXPBD_PULL_PERSIST", persist)
+        xb, lb, gb, sb = _run_all(s, grads, frames)
+        if case == 0:
+            assert sb["pull"], name
+        for f in range(frames + 1):
+            np.testing.assert_array_equal(xa[f], xb[f], err_msg=f"{name} frame {f}")
+        assert abs(la - lb) <= 1e-6 * abs(la), name
+        assert abs(sa["cg_iters_total"] - sb["cg_iters_total"]) <= sa["solves"], name
+        for k in grads:
+            assert rel_l2(gb[k], ga[k]) < 1e-5, (name, persist, k, rel_l2(gb[k], ga[k]))
+
+
 def _pcg_cases():
     from synth import volumetric_block
     return [
