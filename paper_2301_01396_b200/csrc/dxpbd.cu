@@ -916,6 +916,10 @@ struct dxpbd_scene {
     DBuf<float> t_a, t_b, t_Q, t_e, t_g, lam_t;
     DBuf<double4> t_xsave;   // K = 1 tet replay: pre-update vertices of every tet [4T]
     DBuf<float> t_Q2, t_e2;  // second tet block / control buffers (replay / PCG overlap)
+    DBuf<float> t_Q3, t_e3;  // third buffers: three-stage tet pipeline (iterate + blocks | PD projection | PCG)
+    bool tet_pipe = true;    // DXPBD_TET_PIPE
+    cudaStream_t aux2 = nullptr;
+    cudaEvent_t ev_A[3] = {nullptr, nullptr, nullptr}, ev_B[3] = {nullptr, nullptr, nullptr}, ev_P[3] = {nullptr, nullptr, nullptr};
     float *tq_w = nullptr, *te_w = nullptr, *tq_r = nullptr, *te_r = nullptr;   // overlap: replay writes, PCG reads
     DBuf<int32_t> t_perm;
     DBuf<float> ts_lam, ts_S, ts_Dt, ts_Tu, ts_e;   // replay scratch (K > 1)
@@ -1012,10 +1016,11 @@ struct dxpbd_scene {
     bool sweep_graph = true;                       // DXPBD_SWEEP_GRAPH
     int sweep_graph_maxv = 1 << 21;                // only below this many vertices (the forward copies the iterate)
     cudaGraphExec_t g_fwd = nullptr;
-    std::vector<std::pair<std::vector<const void *>, cudaGraphExec_t>> g_rep;   // keyed by the output buffers
+    struct RepGraph { std::vector<const void *> key; cudaGraphExec_t e; int launches; };
+    std::vector<RepGraph> g_rep;                   // keyed by the output buffers (and the replay stage)
     struct PcgChunk { int iters, launches; cudaGraphExec_t e; };
     std::vector<PcgChunk> g_pcg;                   // first PCG chunk, keyed by its iteration count
-    int g_fwd_launches = 0, g_rep_launches = 0;
+    int g_fwd_launches = 0;
     DBuf<double4> xw;                              // forward graph iterate
     cudaStream_t cap_lo = nullptr, cap_mid = nullptr;
     // PCG as a CUDA graph with a conditional WHILE node (no host polls).  Opt-in (DXPBD_PCG_GRAPH=1):
@@ -1389,7 +1394,9 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ replay of substep n
-int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
+// stage 0: the whole replay; 1: everything but the tets' PD projection; 2: the tets' PD projection only
+// (K = 1 tet scenes: the two halves run on two streams)
+int replay_substep(dxpbd_scene *s, int n, cudaStream_t st, int stage = 0) {
     const int V = s->V, E = s->E;
     float4 *qtw = s->qt_write ? s->qt_write : s->d_Qt.p;   // TMA-layout block buffer written
     const bool lay = s->use_tma && s->qf == 0;              // general blocks into the TMA layout
@@ -1401,6 +1408,20 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const int K = s->iterations;
     const bool want_e = (s->grad_flags >> DXPBD_GRAD_COMPLIANCE) & 1;
     const bool wave = s->wave_on && s->wave_rep && s->wave_nitems > 0 && K == 1 && s->qf == 1;
+    auto tet_psd = [&](cudaStream_t st) {
+        float *const tQ = s->tq_w ? s->tq_w : s->t_Q.p;
+        if (s->psd_minb == 3)
+            LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<3><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
+        else if (s->psd_minb == 4)
+            LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<4><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
+        else
+            LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<1><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
+    };
+    if (stage == 2) {
+        tet_psd(st);
+        DX_CHECK_CUDA(cudaGetLastError());
+        return 1;
+    }
     if (wave) {
         WavePredict pr{state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f, s->dtd, 1.0 / s->dtd, s->gravity};
         float4 *Q = s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p);
@@ -1489,13 +1510,8 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
                 LAUNCH(DXPBD_K_TET_REPLAY, (k_tet_replay<true, true, 2><<<(s->T + 127) / 128, 128, 0, st>>>(
                                                0, s->T, s->tdev(), s->inv_dt2d, tsc, s->pd, tQ, teo, x, s->t_xsave.p)));
                 ++launches;
-                if (s->pd) {
-                    if (s->psd_minb == 3)
-                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<3><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
-                    else if (s->psd_minb == 4)
-                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<4><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
-                    else
-                        LAUNCH(DXPBD_K_TET_REPLAY, k_tet_psd<1><<<(s->T + 127) / 128, 128, 0, st>>>(s->T, tQ, s->psd_tol, s->psd_sweeps));
+                if (s->pd && stage == 0) {
+                    tet_psd(st);
                     ++launches;
                 }
             }
@@ -1518,16 +1534,18 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         const bool g_mat = ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) != 0;
         std::vector<const void *> key = {qtw, s->tq_w ? s->tq_w : s->t_Q.p, g_mat ? (s->te_w ? s->te_w : s->t_e.p) : nullptr,
                                          s->qc_w ? s->qc_w : s->Qc.p, want_ce ? (s->ec_w ? s->ec_w : s->ec.p) : nullptr,
-                                         want_e ? s->ed.p : nullptr, s->Qd.p};
-        cudaGraphExec_t e = nullptr;
+                                         want_e ? s->ed.p : nullptr, s->Qd.p, reinterpret_cast<const void *>((size_t)stage)};
+        const dxpbd_scene::RepGraph *rg = nullptr;
         for (auto &kv : s->g_rep)
-            if (kv.first == key) e = kv.second;
-        if (!e) {
-            e = capture_graph(s, st == s->aux ? -1 : 0, sweep, s->g_rep_launches);
-            s->g_rep.push_back({key, e});
+            if (kv.key == key) rg = &kv;
+        if (!rg) {
+            int nl = 0;
+            cudaGraphExec_t e = capture_graph(s, (st == s->aux || st == s->aux2) ? -1 : 0, sweep, nl);
+            s->g_rep.push_back({key, e, nl});
+            rg = &s->g_rep.back();
         }
-        DX_CHECK_CUDA(cudaGraphLaunch(e, st));
-        launches += s->g_rep_launches;
+        DX_CHECK_CUDA(cudaGraphLaunch(rg->e, st));
+        launches += rg->launches;
     } else {
         launches += sweep(st);
     }
@@ -1913,6 +1931,10 @@ int dxpbd_destroy(dxpbd_scene *s) {
     for (cudaEvent_t e : {s->ev_rep[0], s->ev_rep[1], s->ev_pcg[0], s->ev_pcg[1], s->ev_go, s->ev_end})
         if (e) cudaEventDestroy(e);
     if (s->aux) cudaStreamDestroy(s->aux);
+    if (s->aux2) cudaStreamDestroy(s->aux2);
+    for (int k = 0; k < 3; ++k)
+        for (cudaEvent_t e : {s->ev_A[k], s->ev_B[k], s->ev_P[k]})
+            if (e) cudaEventDestroy(e);
     if (s->hi) cudaStreamDestroy(s->hi);
     for (cudaEvent_t e : {s->ev_cp[0], s->ev_cp[1], s->ev_free[0], s->ev_free[1]})
         if (e) cudaEventDestroy(e);
@@ -1920,7 +1942,7 @@ int dxpbd_destroy(dxpbd_scene *s) {
     if (s->pcg_exec) cudaGraphExecDestroy(s->pcg_exec);
     if (s->cap) cudaStreamDestroy(s->cap);
     if (s->g_fwd) cudaGraphExecDestroy(s->g_fwd);
-    for (auto &e : s->g_rep) cudaGraphExecDestroy(e.second);
+    for (auto &e : s->g_rep) cudaGraphExecDestroy(e.e);
     for (auto &e : s->g_pcg) cudaGraphExecDestroy(e.e);
     if (s->cap_lo) cudaStreamDestroy(s->cap_lo);
     if (s->cap_mid) cudaStreamDestroy(s->cap_mid);
@@ -2002,6 +2024,7 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     // A/B switches for measurements (defaults are the measured-best settings)
     if (const char *ev = getenv("DXPBD_WARM")) s->warm_order = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_NB")) s->nb = atoi(ev) == 2 ? 2 : 1;
+    if (const char *ev = getenv("DXPBD_TET_PIPE")) s->tet_pipe = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
@@ -2356,10 +2379,13 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     const bool ovl_tet = s->overlap && s->T && E == 0 && !s->NC && !s->use_tma;
     const bool ovl = ovl_cloth || ovl_tet;
     const bool g_mat = ((s->grad_flags >> DXPBD_GRAD_MATERIAL) & 1) != 0;
-    auto set_write = [&](int k) {   // replay output buffers of parity k
+    // three-stage tet pipeline: A(n-2) = iterate passes + derivative blocks on aux2, B(n-1) = PD projection
+    // of the blocks on aux, PCG(n) on hi; blocks / controls triple-buffered (index n % 3)
+    const bool tet3 = ovl_tet && s->tet_pipe && s->pd && s->iterations == 1;
+    auto set_write = [&](int k) {   // replay output buffers of parity k (tet3: index k of 3)
         if (ovl_tet) {
-            s->tq_w = k ? s->t_Q2.p : s->t_Q.p;
-            s->te_w = g_mat ? (k ? s->t_e2.p : s->t_e.p) : nullptr;
+            s->tq_w = k == 2 ? s->t_Q3.p : (k ? s->t_Q2.p : s->t_Q.p);
+            s->te_w = g_mat ? (k == 2 ? s->t_e3.p : (k ? s->t_e2.p : s->t_e.p)) : nullptr;
         } else {
             s->qt_write = k ? s->d_Qt2.p : s->d_Qt.p;
         }
@@ -2370,8 +2396,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     };
     auto set_read = [&](int k) {
         if (ovl_tet) {
-            s->tq_r = k ? s->t_Q2.p : s->t_Q.p;
-            s->te_r = g_mat ? (k ? s->t_e2.p : s->t_e.p) : nullptr;
+            s->tq_r = k == 2 ? s->t_Q3.p : (k ? s->t_Q2.p : s->t_Q.p);
+            s->te_r = g_mat ? (k == 2 ? s->t_e3.p : (k ? s->t_e2.p : s->t_e.p)) : nullptr;
         } else {
             s->qt_read = k ? s->d_Qt2.p : s->d_Qt.p;
         }
@@ -2393,6 +2419,10 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         if (ovl_tet) {
             if (s->t_Q2.n < s->t_Q.n) s->t_Q2.alloc(s->t_Q.n);
             if (g_mat && s->t_e2.n < s->t_e.n) s->t_e2.alloc(s->t_e.n);
+            if (tet3) {
+                if (s->t_Q3.n < s->t_Q.n) s->t_Q3.alloc(s->t_Q.n);
+                if (g_mat && s->t_e3.n < s->t_e.n) s->t_e3.alloc(s->t_e.n);
+            }
         }
         if (!s->aux) {
             int least = 0, greatest = 0;
@@ -2406,13 +2436,36 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_go, cudaEventDisableTiming));
             DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_end, cudaEventDisableTiming));
         }
+        if (tet3 && !s->aux2) {
+            int least = 0, greatest = 0;
+            DX_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            DX_CHECK_CUDA(cudaStreamCreateWithPriority(&s->aux2, cudaStreamNonBlocking, least));
+            for (int k = 0; k < 3; ++k) {
+                DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_A[k], cudaEventDisableTiming));
+                DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_B[k], cudaEventDisableTiming));
+                DX_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_P[k], cudaEventDisableTiming));
+            }
+        }
         DX_CHECK_CUDA(cudaEventRecord(s->ev_go, st));   // inputs of this call are on `st`
         DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_go, 0));
+        if (tet3) DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux2, s->ev_go, 0));
         // the PCG path runs on the high-priority stream; the replay fills the SMs it leaves idle
         DX_CHECK_CUDA(cudaStreamWaitEvent(s->hi, s->ev_go, 0));
         user_st = st;
         st = s->hi;
-        if (!cached(n_hi)) {
+        if (tet3) {   // fill the pipeline: A(n_hi), B(n_hi), A(n_hi - 1)
+            auto stage_a = [&](int m) {
+                set_write(m % 3);
+                launches += replay_substep(s, m, s->aux2, 1);
+                DX_CHECK_CUDA(cudaEventRecord(s->ev_A[m % 3], s->aux2));
+            };
+            stage_a(n_hi);
+            DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_A[n_hi % 3], 0));
+            set_write(n_hi % 3);
+            launches += replay_substep(s, n_hi, s->aux, 2);
+            DX_CHECK_CUDA(cudaEventRecord(s->ev_B[n_hi % 3], s->aux));
+            if (n_hi >= 1) stage_a(n_hi - 1);
+        } else if (!cached(n_hi)) {
             set_write(n_hi & 1);
             launches += replay_substep(s, n_hi, s->aux);
             DX_CHECK_CUDA(cudaEventRecord(s->ev_rep[n_hi & 1], s->aux));
@@ -2421,7 +2474,22 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     for (int n = n_hi; n >= 0; --n) {
         const int frame = n / sub;
         float *gf = g_forces ? s->g_force.p + (size_t)frame * V * 3 : nullptr;
-        if (ovl) {
+        if (tet3) {
+            if (n >= 1) {   // B(n-1): PD projection of the blocks A(n-1) wrote
+                DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_A[(n - 1) % 3], 0));
+                set_write((n - 1) % 3);
+                launches += replay_substep(s, n - 1, s->aux, 2);
+                DX_CHECK_CUDA(cudaEventRecord(s->ev_B[(n - 1) % 3], s->aux));
+            }
+            if (n >= 2) {   // A(n-2) into the buffer PCG(n+1) finished reading
+                if (n + 1 <= n_hi) DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux2, s->ev_P[(n + 1) % 3], 0));
+                set_write((n - 2) % 3);
+                launches += replay_substep(s, n - 2, s->aux2, 1);
+                DX_CHECK_CUDA(cudaEventRecord(s->ev_A[(n - 2) % 3], s->aux2));
+            }
+            DX_CHECK_CUDA(cudaStreamWaitEvent(st, s->ev_B[n % 3], 0));
+            set_read(n % 3);
+        } else if (ovl) {
             if (n >= 1 && !cached(n - 1)) {   // blocks of substep n-1 into the buffer PCG(n+1) finished reading
                 if (n + 1 <= n_hi && !cached(n + 1)) DX_CHECK_CUDA(cudaStreamWaitEvent(s->aux, s->ev_pcg[(n - 1) & 1], 0));
                 set_write((n - 1) & 1);
@@ -2503,7 +2571,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
             LAUNCH(DXPBD_K_GRADS, k_grad_tet<<<nblk(s->T), kBlock, 0, st>>>(s->tdev(), s->te_r ? s->te_r : s->t_e.p, s->y.p, s->t_g.p));
             ++launches;
         }
-        if (ovl) DX_CHECK_CUDA(cudaEventRecord(s->ev_pcg[n & 1], st));   // buffer n & 1 free again
+        if (tet3) DX_CHECK_CUDA(cudaEventRecord(s->ev_P[n % 3], st));    // buffer n % 3 free again
+        else if (ovl) DX_CHECK_CUDA(cudaEventRecord(s->ev_pcg[n & 1], st));   // buffer n & 1 free again
         if (s->gs_out && g_forces && n % sub == 0) stream_frame_grads(s, frame, st);   // frame complete
     }
     s->qt_read = s->qt_write = nullptr;
