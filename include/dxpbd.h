@@ -190,6 +190,27 @@ int dxpbd_stats(dxpbd_scene *scene, double *out, int32_t n);
  * Supported: iterations == 1, pd_projection, no tets, grad_flags within FORCES | X0 | V0;
  * the scene must take the TMA path (dxpbd_stats field 13).  Same argument conventions as
  * the scene calls above. */
+/* Host-only view of the pull layout of the adjoint PCG's tile kernels (csrc/pull.cuh; no GPU): the
+ * layout dxpbd_create builds for scenes with closed-form K = 1 blocks (Sec.4.3 l.166-194,
+ * 4.3.2 l.201: one PD-projected block Q_j per distance constraint; Eq. adjointXPBD l.150-161 is
+ * solved matrix-free over them).  All ids in INTERNAL vertex order (Morton; vertex i is in tile
+ * i / kTileV).  HOST outputs, each optional (NULL) except sizes:
+ *   sizes[0..8) = {tiles, hcap, ycap, block slots, index words, kTileV, colors, dense slabs max};
+ *   vperm [V] internal -> user vertex; sorted_ab [E][2] endpoints of the color-sorted constraints;
+ *   perm [E] sorted position -> user constraint; tpos / fpos [E] block slot of the sorted
+ *   constraint in its a-tile / in its b-tile (-1 if a and b share a tile);
+ *   tdesc [tiles][4] = {first block slot, first index word, K0 | KS2 << 8, overflow entries};
+ *   hpad [tiles][hcap] halo vertex ids (-1 padded; shared-memory slot kTileV + h);
+ *   idx [index words]: per tile prim2[(K0 + 1) / 2][kTileV] (two 16-bit entries per word: other
+ *   endpoint's slot (11 bits, 0x7ff = none) | lane << 11; the entry's block / y slot is
+ *   k * kTileV + (i & ~31) + lane), sec2[KS2][kTileV] (y slot (15 bits) | add flag << 15, 0xffff =
+ *   none), over[n] (own slot | other slot << 16; y slot K0 * kTileV + e).
+ * idx_cap < index words -> DXPBD_ERR_ARG; a scene that does not take the pull layout ->
+ * DXPBD_ERR_LIMIT. */
+int dxpbd_pull_layout(const dxpbd_scene_desc *desc, int64_t *sizes, int32_t *vperm, int32_t *sorted_ab,
+                      int32_t *perm, int32_t *tpos, int32_t *fpos, int32_t *tdesc, int32_t *hpad,
+                      uint32_t *idx, int64_t idx_cap);
+
 /* Host-only partition plan (no GPU, no allocation on a device): the plan dxpbd_group_create /
  * _create_dist build from the same host topology (Morton tiles, greedy colors R1, halos, TMA
  * layout).  Partition p owns Morton tiles [t0_p, t1_p).  Exchange lists, ids in INTERNAL vertex

@@ -89,6 +89,7 @@ def lib():
             "dxpbd_group_grads": ([vp, i32, vp, i64, i32, vp], ctypes.c_int),
             "dxpbd_group_stats": ([vp, vp, i32], ctypes.c_int),
             "dxpbd_partition_plan": ([ctypes.POINTER(SceneDesc), i32, i32, vp, vp, vp, i64, vp], ctypes.c_int),
+            "dxpbd_pull_layout": ([ctypes.POINTER(SceneDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, i64], ctypes.c_int),
             "dxpbd_last_error": ([], ctypes.c_char_p),
             "dxpbd_version": ([], ctypes.c_int),
         }
@@ -105,7 +106,7 @@ EXPORTED = ["dxpbd_create", "dxpbd_destroy", "dxpbd_forward", "dxpbd_positions",
             "dxpbd_version", "dxpbd_profile", "dxpbd_kernel_times", "dxpbd_group_create", "dxpbd_group_destroy",
             "dxpbd_group_forward", "dxpbd_group_positions", "dxpbd_group_backward", "dxpbd_group_grads",
             "dxpbd_group_stats", "dxpbd_nccl_unique_id", "dxpbd_group_create_dist", "dxpbd_partition_plan",
-            "dxpbd_grads_stream"]
+            "dxpbd_grads_stream", "dxpbd_pull_layout"]
 
 KCLASSES = ["predict", "dist_project", "contact_project", "tet_project", "dist_replay", "contact_replay",
             "tet_replay", "cg_vertex", "cg_dist", "cg_tet", "cg_update", "cg_init", "rhs", "adjoint", "grads",
@@ -426,6 +427,25 @@ def dxpbd_partition_plan(x_rest, inv_mass, num_parts: int, rank: int, **kw) -> d
                 n = int(counts[(k * 2 + dirn) * P + q])
                 out[key].setdefault(name, {})[q] = ids[o:o + n].copy()
                 o += n
+    return out
+
+
+def dxpbd_pull_layout(x_rest, inv_mass, **kw) -> dict:
+    """Host-only view of the pull layout of the PCG tile kernels (include/dxpbd.h dxpbd_pull_layout):
+    sizes plus the arrays vperm, sorted_ab, perm, tpos, fpos, tdesc, hpad, idx (numpy, internal vertex ids)."""
+    d, keep, dims = _desc(x_rest, inv_mass, **kw)
+    sizes = np.zeros(8, np.int64)
+    _check(lib().dxpbd_pull_layout(ctypes.byref(d), sizes.ctypes.data, None, None, None, None, None, None, None, None, 0),
+           "dxpbd_pull_layout")
+    nt, hcap, ycap, slots, words, tile_v, nc, k0max = (int(v) for v in sizes)
+    V, E = int(d.num_vertices), int(d.num_dist)
+    out = dict(tiles=nt, hcap=hcap, ycap=ycap, block_slots=slots, index_words=words, tile_v=tile_v, colors=nc,
+               dense_slabs_max=k0max, vperm=np.zeros(V, np.int32), sorted_ab=np.zeros((E, 2), np.int32),
+               perm=np.zeros(E, np.int32), tpos=np.zeros(E, np.int32), fpos=np.zeros(E, np.int32),
+               tdesc=np.zeros((nt, 4), np.int32), hpad=np.zeros((nt, hcap), np.int32), idx=np.zeros(words, np.uint32))
+    _check(lib().dxpbd_pull_layout(ctypes.byref(d), sizes.ctypes.data, *(out[k].ctypes.data for k in
+                                   ("vperm", "sorted_ab", "perm", "tpos", "fpos", "tdesc", "hpad", "idx")), words),
+           "dxpbd_pull_layout")
     return out
 
 
