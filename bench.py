@@ -464,7 +464,10 @@ def run_ours(a):
                 "frac_incl_layout_overhead": ((b + ovh) / (avg_ms / 1e3) / 1e9 / peak) if b else None,
                 "avg_launch_ms": avg_ms, "launches": cnt, "working_launches": work, "share_of_kernel_time": share,
                 "timing": "CUDA events around every launch of one separate profiled step (headline unprofiled)",
-                "profiled_step_ms": prof_ms, "peak_source": peak_src}
+                "profiled_step_ms": prof_ms, "peak_source": peak_src,
+                "layout": {"pull": bool(sst.get("pull")), "block_slots": sst.get("block_slots"),
+                           "index_words": sst.get("pull_index_words"), "cross_tile_copies": sst.get("n_foreign"),
+                           "halo_entries": sst.get("halo_total"), "tiles": sst.get("tiles")}}
 
     # ---- whole-step roofline on unique bytes (each state / constraint element once per sweep)
     step_roof = None

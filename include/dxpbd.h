@@ -169,9 +169,8 @@ int dxpbd_coloring(dxpbd_scene *scene, int32_t family, int32_t *out, int64_t out
  *  2: kernel launches of the last forward, 3: of the last backward, 4: substeps solved,
  *  5: worst final relative residual, 6: last loss, 7: foreign constraint entries (tiled PCG),
  *  8: halo slots summed over tiles, 9: E, 10: V, 11: T, 12: vertex tiles, 13: TMA path on,
- *  14: PCG matvec launches of the last backward that did work (iterations, plus one start
- *      matvec per solve for the single-reduction PCG), 15: substeps of the last backward whose
- *      derivative blocks came from the forward's cache (no replay),
+ *  14: PCG matvec launches of the last backward that did work (one per iteration),
+ *  15: substeps of the last backward whose derivative blocks came from the forward's cache (no replay),
  *  16: wave tiles of the wavefront sweep (0: per-color launches), 17: its work items per substep,
  *  18: its ticket lag L (bandwidth of the wave-tile order + 1), 19: most neighbours of a wave tile,
  *  20: pull layout on (closed-form K = 1 blocks, csrc/pull.cuh), 21: block slots of the tile layout

@@ -799,8 +799,7 @@ void dist_topology(const dxpbd_scene_desc *d, int qf, DistTopo &T) {
     };
     // pull layout (pull.cuh) for closed-form blocks: count pass, offsets, fill pass
     const char *pe = getenv("DXPBD_PULL");
-    const char *cge = getenv("DXPBD_CG");
-    if (qf == 1 && !(pe && atoi(pe) == 0) && !(cge && std::string(cge) == "cgcg")) {
+    if (qf == 1 && !(pe && atoi(pe) == 0)) {
         T.ptd.assign(nt, make_int4(0, 0, 0, 0));
         auto tile = [&](int t, uint32_t *idx, PullScratch &ws) {
             pull_tile_layout(t, nc, nt, T.halo[t], cnt.data(), fc.data(), ab_sorted.data(), T.fidx.data(), d->x_rest,
@@ -898,10 +897,11 @@ struct dxpbd_scene {
     DBuf<int> d_tpos;                   // sorted constraint position -> TMA layout position
     // pull layout (pull.cuh): closed-form K = 1 blocks; replaces tseg / cpair / vslot / hslot
     bool pull = false;
-    int ycap = 0, pull_minb = 2;
-    bool pull_keep = true;   // L2 evict-last for the static per-tile data (A/B: DXPBD_PULL_KEEP)
+    int ycap = 0;
     bool pull_persist = true;   // persistent matvec CTAs with next-tile prefetch (A/B: DXPBD_PULL_PERSIST)
-    size_t pull_psmem = 0;
+    int upd_ctas = 8;           // PCG update: CTAs per SM of its grid-stride launch (DXPBD_UPD_CTAS; large = one quad per thread)
+    size_t pull_psmem = 0, pull_rhs_psmem = 0;
+    int rhs_persist = 2;   // persistent rhs: CTAs per SM (0: one tile per CTA)
     int num_sms = 148;
     size_t pull_smem = 0, pull_rhs_smem = 0;
     DBuf<int4> d_ptd;
@@ -994,10 +994,6 @@ struct dxpbd_scene {
     bool defer_u = true;                               // PCG: u += alpha p deferred into the next matvec (measured best)
     int last_iters = 0;                                // PCG iterations of the previous solve (poll schedule)
     int poll_extra = 0;                                // iterations launched beyond last_iters before the first poll
-    DBuf<float3> r1, s1, w1;                           // single-reduction PCG ping-pong partners
-    bool cgcg = false;                                 // single-reduction PCG (k_cgcg_tma; opt-in DXPBD_CG=cgcg:
-                                                       // measured 10 % slower than matvec + update)
-    int cgcg_minb = 4;                                 // its resident CTAs per SM (launch bounds)
     bool tetv = true;                                  // no distance constraints: 2-launch PCG iteration (k_cg_tetv)
     int tetv_minb = 1;                                 // its launch-bounds CTAs per SM
     int mv_minb = 4;                                   // TMA matvec: launch-bounds CTAs per SM (A/B: DXPBD_MV_MINB)
@@ -1640,7 +1636,6 @@ BwdSetup backward_prepare(dxpbd_scene *s, int num_keys, const int32_t *key_frame
     if (s->xr.n < (size_t)V) s->xr.alloc(V);
     auto ensure4 = [&](DBuf<float3> &b) { if (b.n < (size_t)V) b.alloc(V); };
     ensure4(s->ax); ensure4(s->rhs); ensure4(s->y); ensure4(s->r); ensure4(s->p); ensure4(s->q); ensure4(s->p1);
-    if (s->use_tma && s->qf == 1 && !s->T && s->cgcg) { ensure4(s->r1); ensure4(s->s1); ensure4(s->w1); }
     ensure4(s->uprev); ensure4(s->u0);
     if (s->warm_order == 2 && s->use_tma) ensure4(s->uprev2);
     const bool warm2 = su.warm2 = s->warm_order == 2 && s->use_tma;
@@ -1723,33 +1718,18 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     CGBufs bufs{s->ax.p, s->r.p, s->p.p, s->p1.p, s->q.p, nullptr};
     TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
     TmaTiles tt = s->tma_tiles();
-    // single-reduction PCG (kernels.cuh k_cgcg_tma): cloth-only TMA path
-    const bool cgcg = s->use_tma && s->qf == 1 && !s->T && s->cgcg;
-    const bool defer = s->use_tma && !cgcg && s->defer_u;   // u update deferred into the next matvec
+    const bool defer = s->use_tma && s->defer_u;   // u update deferred into the next matvec
     // no distance constraints (tets and contacts only): tet + vertex matvec in one launch, q folded
     // into the update (tet_kernels.cuh k_cg_tetv)
     const bool tetv = s->T && E == 0 && !s->use_tma && s->tetv;
     const float *const tQr = s->tq_r ? s->tq_r : s->t_Q.p;   // tet blocks of this substep
     const int nbt = tetv ? nblk(s->T) : 0;
-    CGCGBufs cb{s->ax.p, s->p.p, {s->r.p, s->r1.p}, {s->p1.p, s->s1.p}, {s->q.p, s->w1.p}, s->rhs.p};
-    auto cgcg_launch = [&](int i) {
-        if (s->cgcg_minb == 3)
-            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<kMvThreads, kMvMinB - 1><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
-        else
-            LAUNCH(DXPBD_K_CG_DIST, (k_cgcg_tma<kMvThreads, kMvMinB><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(i, tt, V, Qc, cb, xw, cs)));
-    };
-    if (cgcg)
-        cgcg_launch(-1);
-    else if (!started)   // else fused into the rhs kernel
+    if (!started)   // else fused into the rhs kernel
         LAUNCH(DXPBD_K_CG_INIT, k_cg_start<<<nblk(V), kBlock, 0, st>>>(V, s->rhs.p, s->r.p, s->p.p, xw, cs));
     int launches = 1;
     int it = 0;
     // one PCG iteration (it >= 0, or it = -1 with the graph-mode state: counter and pointers on the device)
     auto iteration = [&](int it, cudaStream_t st, const CGState &cs) -> int {
-        if (cgcg) {
-            cgcg_launch(it);
-            return 1;
-        }
         if (tetv) {
             if (s->tetv_minb == 3)
                 LAUNCH(DXPBD_K_CG_TET, k_cg_tetv<3><<<nbt + nblk(V), kBlock, 0, st>>>(it, nbt, V, s->tdev(), tQr, bufs,
@@ -1764,18 +1744,10 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
         if (s->pull) {
             const PullTiles pt = s->pull_tiles();
             float3 *uf = defer ? s->ax.p : nullptr;
-            if (s->pull_persist && s->pull_minb == 3)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull_p<3><<<std::min(s->ntiles, 3 * s->num_sms), kTileV, s->pull_psmem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, s->ntiles, uf)));
-            else if (s->pull_persist)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull_p<2><<<std::min(s->ntiles, 2 * s->num_sms), kTileV, s->pull_psmem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, s->ntiles, uf)));
-            else if (s->pull_minb == 1)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<1><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
-            else if (s->pull_minb == 3 && !s->pull_keep)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<3, false><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
-            else if (s->pull_minb == 3)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<3><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
+            if (s->pull_persist)
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull_p<<<std::min(s->ntiles, 2 * s->num_sms), kTileV, s->pull_psmem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, s->ntiles, uf)));
             else
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<2><<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
+                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
         } else if (s->use_tma) {
             if (s->mv_minb == 3)
                 LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<kMvThreads, kMvMinB - 1><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
@@ -1793,13 +1765,14 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->tdev(), cs));
             n += 2;
         }
+        const int ugrid = std::min(nblk(V / 4 + 1), s->upd_ctas * s->num_sms);   // whole waves only
         if (defer)
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<false><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<false><<<ugrid, kBlock, 0, st>>>(V, it, bufs, xw, cs));
         else
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<true><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<true><<<ugrid, kBlock, 0, st>>>(V, it, bufs, xw, cs));
         return n + 1;
     };
-    if (s->pcg_graph && !cgcg && !s->prof) {
+    if (s->pcg_graph && !s->prof) {
         // the whole iteration loop as one graph launch: a WHILE node over one iteration whose update kernel's
         // last block sets the condition (kernels.cuh pcg_ctl_end); built once per scene, the buffers that
         // change between substeps are read from pcg_pp
@@ -1859,7 +1832,7 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
     // small scenes: the first chunk (the previous solve's iteration count) as ONE graph launch of that
     // many iterations (kernels with their iteration index baked in, the substep's rotating buffers read
     // from pcg_pp; iterations past convergence exit at once as in the stream launches)
-    const bool chunk_graph = sweep_graph_on(s) && !cgcg;
+    const bool chunk_graph = sweep_graph_on(s);
     while (it < maxit) {
         int end = std::min(maxit, it + chunk);
         chunk = 2;
@@ -2025,6 +1998,8 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_WARM")) s->warm_order = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_NB")) s->nb = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_TET_PIPE")) s->tet_pipe = atoi(ev) != 0;
+    if (const char *ev = getenv("DXPBD_UPD_CTAS")) s->upd_ctas = std::max(1, std::min(1 << 16, atoi(ev)));
+    DX_CHECK_CUDA(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, s->device));
     if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
@@ -2103,18 +2078,16 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 upload(s->d_pidx.p, topo.pidx.data(), sizeof(uint32_t) * topo.pidx.size(), DXPBD_MEM_HOST, st);
                 s->pull_smem = pull_smem_bytes(s->hcap, s->ycap, 1);
                 s->pull_rhs_smem = pull_smem_bytes(s->hcap, s->ycap, 2);
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
-                if (const char *ev = getenv("DXPBD_PULL_KEEP")) s->pull_keep = atoi(ev) != 0;
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_smem));
                 s->pull_psmem = pull_persist_smem_bytes(s->hcap, s->ycap);
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull_p<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_psmem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull_p<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_psmem));
+                s->pull_rhs_psmem = pull_persist_smem_bytes(s->hcap, s->ycap, 2);
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull_p<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_psmem));
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull_p<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_psmem));
+                if (const char *ev = getenv("DXPBD_RHS_PERSIST")) s->rhs_persist = atoi(ev);
+                DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_psmem));
                 DX_CHECK_CUDA(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, s->device));
                 if (const char *ev = getenv("DXPBD_PULL_PERSIST")) s->pull_persist = atoi(ev) != 0;
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_smem));
-                if (const char *ev = getenv("DXPBD_PULL_MINB")) s->pull_minb = std::max(1, std::min(3, atoi(ev)));
             } else {
                 s->d_tseg.alloc(topo.tseg.size());
                 upload(s->d_tseg.p, topo.tseg.data(), sizeof(int4) * topo.tseg.size(), DXPBD_MEM_HOST, st);
@@ -2135,10 +2108,6 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
             s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0);
             DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
             DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-            DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-            DX_CHECK_CUDA(cudaFuncSetAttribute(k_cgcg_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-            if (const char *ev = getenv("DXPBD_CGCG_MINB")) s->cgcg_minb = atoi(ev);
-            if (const char *ev = getenv("DXPBD_CG")) s->cgcg = std::string(ev) == "cgcg";
             DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
         }
         s->d_fidx.alloc(topo.fidx.size());
@@ -2364,17 +2333,17 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
     double worst = 0.0;
     int solves = 0;
     // PCG iteration loops as graph launches (pcg_solve): counts and convergence come back once, at the end
-    const bool gmode = s->pcg_graph && !s->prof && !(s->use_tma && s->qf == 1 && !s->T && s->cgcg);
+    const bool gmode = s->pcg_graph && !s->prof;
     if (gmode) {
         if (!s->pcg_ctl.p) s->pcg_ctl.alloc(1);
         if (!s->pcg_pp.p) s->pcg_pp.alloc(1);
         DX_CHECK_CUDA(cudaMemsetAsync(s->pcg_ctl.p, 0, sizeof(PcgCtl), st));
     }
     // PCG start fused into the TMA rhs kernel (no tet rhs pass after it, standard PCG)
-    const bool fuse_start = s->use_tma && !s->T && !(s->cgcg && s->qf == 1);
+    const bool fuse_start = s->use_tma && !s->T;
     // replay of substep n-1 on the aux stream during the PCG of substep n (independent work: the
     // replay reads only checkpoints); blocks double-buffered, ordered by events
-    const bool ovl_cloth = s->overlap && s->use_tma && s->qf == 1 && !s->T && !g_comp && !s->cgcg;
+    const bool ovl_cloth = s->overlap && s->use_tma && s->qf == 1 && !s->T && !g_comp;
     // tet-only scenes: the tet blocks (and material controls) are double-buffered the same way
     const bool ovl_tet = s->overlap && s->T && E == 0 && !s->NC && !s->use_tma;
     const bool ovl = ovl_cloth || ovl_tet;
@@ -2518,7 +2487,17 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         {
             TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
             TmaTiles tt = s->tma_tiles();
-            if (s->pull)
+            if (s->pull && s->pull_persist && s->rhs_persist == 1)
+                LAUNCH(DXPBD_K_RHS, k_rhs_pull_p<1><<<std::min(s->ntiles, s->num_sms), kTileV, s->pull_rhs_psmem, st>>>(
+                    s->pull_tiles(), V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
+                    s->r.p, s->u0.p, 0, s->ntiles, fuse_start ? s->p.p : nullptr,
+                    CGState{s->cg_sc.p, s->cg_sc.p + (size_t)(s->cg_max_iter + 1) * 4, s->cg_tol * s->cg_tol}));
+            else if (s->pull && s->pull_persist && s->rhs_persist == 2)
+                LAUNCH(DXPBD_K_RHS, k_rhs_pull_p<2><<<std::min(s->ntiles, 2 * s->num_sms), kTileV, s->pull_rhs_psmem, st>>>(
+                    s->pull_tiles(), V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
+                    s->r.p, s->u0.p, 0, s->ntiles, fuse_start ? s->p.p : nullptr,
+                    CGState{s->cg_sc.p, s->cg_sc.p + (size_t)(s->cg_max_iter + 1) * 4, s->cg_tol * s->cg_tol}));
+            else if (s->pull)
                 LAUNCH(DXPBD_K_RHS, k_rhs_pull<<<s->ntiles, kTileV, s->pull_rhs_smem, st>>>(
                     s->pull_tiles(), V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
                     s->r.p, s->u0.p, 0, fuse_start ? s->p.p : nullptr,
@@ -2617,9 +2596,8 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         for (int n = std::min(N, last_key_state) - 1; n >= 0; --n) nc_used += cached(n) ? 1 : 0;
         s->stats[15] = nc_used;
     }
-    // PCG matvec launches that did work: one per iteration (+ the start matvec per solve for the
-    // single-reduction form)
-    s->stats[14] = total_it + ((s->use_tma && s->qf == 1 && !s->T && s->cgcg) ? solves : 0);
+    // PCG matvec launches that did work: one per iteration
+    s->stats[14] = total_it;
     s->stats[1] = max_it;
     s->stats[3] = launches;
     s->stats[4] = solves;

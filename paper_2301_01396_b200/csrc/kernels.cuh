@@ -1054,184 +1054,6 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_matvec_tma(int it, TmaTiles T, 
     block_reduce_add<1>(acc, s.sc + (it + 1) * 4 + 0);
 }
 
-// ---------------------------------------------------------------------------------------------
-// Single-reduction PCG (Chronopoulos-Gear form of preconditioned CG; same iterates as
-// k_cg_matvec_tma + k_cg_update4 in exact arithmetic), one fused kernel per iteration.  With
-// M the mass matrix, W = M^-1 the Jacobi preconditioner and A = M + Q_c + A_dist:
-//   kernel -1:  u_0 = W r_0, w_0 = A u_0;  slot 0 = (delta_0 = u_0.w_0, gamma_0 = r_0.u_0, r_0.r_0), |b|^2
-//   kernel i:   beta_i = gamma_i / gamma_{i-1} (0 for i = 0),
-//               alpha_i = gamma_i / (delta_i - beta_i gamma_i / alpha_{i-1})  (gamma_0 / delta_0),
-//               p_i = u_i + beta_i p_{i-1},  s_i = w_i + beta_i s_{i-1}   (s_i = A p_i),
-//               x += alpha_i p_i,  r_{i+1} = r_i - alpha_i s_i,  u_{i+1} = W r_{i+1},
-//               w_{i+1} = A u_{i+1} (tile matvec),  slot i+1 = (delta, gamma, rr);  alpha_i -> slot i.
-// M u_{i+1} = r_{i+1} on free vertices, so the vertex term of w needs no extra read.  Halo values
-// u_{i+1} are recomputed from the neighbours' r_i, w_i, s_{i-1} (ping-pong buffers: the owners
-// write r_{i+1}, w_{i+1}, s_i in the same launch).  Pinned vertices: u = p = s = r = w = 0.
-struct CGCGBufs {
-    float3 *x, *p;
-    float3 *r[2], *s[2], *w[2];
-    const float3 *b;
-};
-
-template <int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_cgcg_tma(int i, TmaTiles T, int V, const float *__restrict__ Qc,
-                                                       CGCGBufs B, const float *__restrict__ wv, CGState s) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
-    unsigned char *stages = smem_raw + 64;
-    float4 *sq = reinterpret_cast<float4 *>(stages + (size_t)tma_stage_bytes(T.cap, T.Q2 != nullptr) * kTmaStages);
-    float4 *sp = sq + kTileV;
-    const int hcap = T.hcap;
-    const int t = blockIdx.x;
-    const int v0 = t * kTileV;
-    const int nv = min(kTileV, V - v0);
-    __shared__ int4 sb[kMaxColors];
-    constexpr int NO = (kTileV + NT - 1) / NT, NH = (512 + NT - 1) / NT;
-    // ---- round trip 1
-    const bool done = i >= 0 && cg_done(s, i + 1);
-    if (threadIdx.x < T.ncol) sb[threadIdx.x] = T.tseg[(size_t)t * T.ncol + threadIdx.x];
-    float wo[NO];
-    int so[NO];
-#pragma unroll
-    for (int u = 0; u < NO; ++u) {
-        const int l = threadIdx.x + u * NT;
-        wo[u] = wv[min(v0 + l, V - 1)];
-        so[u] = l < kTileV ? T.vslot[(size_t)t * kTileV + l] : 0;
-    }
-    int hv[NH], hs[NH];
-#pragma unroll
-    for (int u = 0; u < NH; ++u) {
-        const int h = threadIdx.x + u * NT;
-        hv[u] = h < hcap ? T.hpad[(size_t)t * hcap + h] : -1;
-        hs[u] = h < hcap ? T.hslot[(size_t)t * hcap + h] : 0;
-    }
-    if (done) return;
-    __syncthreads();
-    if (threadIdx.x == NT - 32) {
-        for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
-        fence_mbar_init();
-        const uint32_t sbytes = tma_stage_bytes(T.cap, T.Q2 != nullptr);
-        for (int c = 0; c < min(kTmaStages, T.ncol); ++c) tma_issue(&bars[c], stages + (size_t)c * sbytes, sb[c], T);
-    }
-    // ---- scalars of this iteration (double, from the previous launches' reductions)
-    double al = 0.0, be = 0.0;
-    if (i >= 0) {
-        const double gi = s.sc[i * 4 + 1], di = s.sc[i * 4 + 0];
-        if (i == 0) {
-            al = di > 0.0 ? gi / di : 0.0;
-        } else {
-            const double gp = s.sc[(i - 1) * 4 + 1], ap = s.sc[(i - 1) * 4 + 3];
-            be = gp > 0.0 ? gi / gp : 0.0;
-            const double den = ap != 0.0 ? di - be * gi / ap : di;
-            al = den > 0.0 ? gi / den : 0.0;
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) s.sc[i * 4 + 3] = al;
-    }
-    const float alpha = (float)al, beta = (float)be;
-    const float3 z3 = make_float3(0.f, 0.f, 0.f);
-    const float3 *__restrict__ rin = B.r[i >= 0 ? (i & 1) : 0];
-    float3 *__restrict__ rout = B.r[(i + 1) & 1];
-    const float3 *__restrict__ win = B.w[i >= 0 ? (i & 1) : 1];
-    float3 *__restrict__ wout = B.w[(i + 1) & 1];
-    const float3 *__restrict__ sin_ = B.s[(i + 1) & 1];   // s_{i-1}
-    float3 *__restrict__ sout = B.s[i >= 0 ? (i & 1) : 0];
-    // ---- round trip 2: own r_i, w_i, s_{i-1}, p_{i-1}, x (and b for kernel -1); halo r_i, w_i, s_{i-1}
-    float acc[3] = {0.f, 0.f, 0.f};   // delta, gamma, rr of slot i + 1
-    float bacc = 0.f;
-    float3 ro[NO], wq[NO], so_[NO], po[NO], xo[NO];
-#pragma unroll
-    for (int u = 0; u < NO; ++u) {
-        const int v = min(v0 + (int)threadIdx.x + u * NT, V - 1);
-        ro[u] = rin[v];
-        if (i >= 0) {
-            wq[u] = win[v];
-            so_[u] = i > 0 ? sin_[v] : z3;
-            po[u] = i > 0 ? B.p[v] : z3;
-            xo[u] = B.x[v];
-        } else {
-            wq[u] = B.b[v];   // kernel -1: |b|^2
-        }
-    }
-    float hw[NH];
-    float3 hr[NH], hwq[NH], hsv[NH];
-#pragma unroll
-    for (int u = 0; u < NH; ++u) {
-        const int v = max(hv[u], 0);
-        hw[u] = wv[v];
-        hr[u] = rin[v];
-        hwq[u] = i >= 0 ? win[v] : z3;
-        hsv[u] = i > 0 ? sin_[v] : z3;
-    }
-#pragma unroll
-    for (int u = 0; u < NO; ++u) {
-        const int l = threadIdx.x + u * NT;
-        float3 un = z3, wn = z3;
-        if (l < nv) {
-            const int v = v0 + l;
-            const float w = wo[u];
-            float3 rn = z3;
-            if (i >= 0) {
-                float3 pv = z3, sv = wq[u] + beta * so_[u];
-                if (w > 0.f) pv = w * ro[u] + beta * po[u];
-                B.p[v] = pv;
-                sout[v] = sv;
-                B.x[v] = xo[u] + alpha * pv;
-                if (w > 0.f) rn = ro[u] - alpha * sv;
-                rout[v] = rn;
-            } else {
-                if (w > 0.f) {
-                    rn = ro[u];
-                    bacc += dot3(wq[u], wq[u]);
-                }
-            }
-            if (w > 0.f) {
-                un = w * rn;
-                wn = rn;
-                if (Qc) {
-                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v],
-                                  Qc[4 * (size_t)V + v], Qc[5 * (size_t)V + v]};
-                    wn = wn + sym3_mul(A, un);
-                }
-                acc[0] += dot3(un, wn);
-                acc[1] += dot3(rn, un);
-                acc[2] += dot3(rn, rn);
-            }
-        }
-        if (l < kTileV) {
-            sp[so[u]] = f4of(un);
-            sq[so[u]] = f4of(wn);
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < NH; ++u) {
-        if (hv[u] >= 0) {
-            float3 un = z3;
-            if (hw[u] > 0.f) un = hw[u] * (i >= 0 ? hr[u] - alpha * (hwq[u] + beta * hsv[u]) : hr[u]);
-            sp[hs[u]] = f4of(un);
-        }
-    }
-    for (int h = threadIdx.x + NH * NT; h < hcap; h += blockDim.x) {   // rare: large halos
-        const int v = T.hpad[(size_t)t * hcap + h];
-        if (v < 0) continue;
-        const float w = wv[v];
-        float3 un = z3;
-        if (w > 0.f) un = w * (i >= 0 ? rin[v] - alpha * (win[v] + beta * (i > 0 ? sin_[v] : z3)) : rin[v]);
-        sp[T.hslot[(size_t)t * hcap + h]] = f4of(un);
-    }
-    __syncthreads();
-    acc[0] += tma_tile_colors<NT>(bars, stages, sp, sq, sb, T);
-#pragma unroll
-    for (int u = 0; u < NO; ++u) {
-        const int l = threadIdx.x + u * NT;
-        if (l < nv) wout[v0 + l] = wo[u] > 0.f ? xyz(sq[so[u]]) : z3;
-    }
-    block_reduce_add<3>(acc, s.sc + (i + 1) * 4);
-    if (i < 0) {
-        float bb[1] = {bacc};
-        block_reduce_add<1>(bb, s.bnorm2);
-    }
-}
-
 // rhs (warm start): b = M u - Q_n y + dphi, r0 = b - A_n (u + du); A_dist applied tile-locally
 // with the same staging / slot layout as the matvec.
 __global__ void __launch_bounds__(kTmaThreads, kRhsMinB) k_rhs_tma(TmaTiles T, int V, const float *__restrict__ Qc,
@@ -1549,9 +1371,11 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         if (s.ctl) pcg_ctl_end(s, it);
         return;
     }
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nq = V / 4;
     float acc[2] = {0.f, 0.f};
+    // grid-stride over quads of vertices: the solver launches a grid that fills every SM once (no
+    // partial last wave); a one-quad-per-thread grid works as well
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= nq; t += gridDim.x * blockDim.x) {
     if (t < nq) {
         const float4 *__restrict__ p = reinterpret_cast<const float4 *>((it & 1) ? B.p1 : B.p0);
         float4 *__restrict__ u = reinterpret_cast<float4 *>(B.u);
@@ -1584,7 +1408,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
             if (UPD_U) u[3 * t + c] = make_float4(uu[4 * c], uu[4 * c + 1], uu[4 * c + 2], uu[4 * c + 3]);
             r[3 * t + c] = make_float4(rr[4 * c], rr[4 * c + 1], rr[4 * c + 2], rr[4 * c + 3]);
         }
-    } else if (t == nq) {   // tail vertices
+    } else {   // t == nq: tail vertices
         for (int v = 4 * nq; v < V; ++v) {
             const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
             const double pq = s.sc[(it + 1) * 4 + 0];
@@ -1599,6 +1423,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
             acc[0] += w * r2;
             acc[1] += r2;
         }
+    }
     }
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
     if (s.ctl) pcg_ctl_end(s, it);
