@@ -899,9 +899,7 @@ struct dxpbd_scene {
     bool pull = false;
     int ycap = 0;
     bool pull_persist = true;   // persistent matvec CTAs with next-tile prefetch (A/B: DXPBD_PULL_PERSIST)
-    int upd_ctas = 8;           // PCG update: CTAs per SM of its grid-stride launch (DXPBD_UPD_CTAS; large = one quad per thread)
-    size_t pull_psmem = 0, pull_rhs_psmem = 0;
-    int rhs_persist = 2;   // persistent rhs: CTAs per SM (0: one tile per CTA)
+    size_t pull_psmem = 0;
     int num_sms = 148;
     size_t pull_smem = 0, pull_rhs_smem = 0;
     DBuf<int4> d_ptd;
@@ -1765,11 +1763,10 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             LAUNCH(DXPBD_K_CG_TET, k_fold_q4<<<nblk(V), kBlock, 0, st>>>(V, it, bufs, s->tdev(), cs));
             n += 2;
         }
-        const int ugrid = std::min(nblk(V / 4 + 1), s->upd_ctas * s->num_sms);   // whole waves only
         if (defer)
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<false><<<ugrid, kBlock, 0, st>>>(V, it, bufs, xw, cs));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<false><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
         else
-            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<true><<<ugrid, kBlock, 0, st>>>(V, it, bufs, xw, cs));
+            LAUNCH(DXPBD_K_CG_UPDATE, k_cg_update4<true><<<nblk(V / 4 + 1), kBlock, 0, st>>>(V, it, bufs, xw, cs));
         return n + 1;
     };
     if (s->pcg_graph && !s->prof) {
@@ -1998,8 +1995,6 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_WARM")) s->warm_order = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_NB")) s->nb = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_TET_PIPE")) s->tet_pipe = atoi(ev) != 0;
-    if (const char *ev = getenv("DXPBD_UPD_CTAS")) s->upd_ctas = std::max(1, std::min(1 << 16, atoi(ev)));
-    DX_CHECK_CUDA(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, s->device));
     if (const char *ev = getenv("DXPBD_NB_REPLAY")) s->nb_rep = atoi(ev) == 2 ? 2 : 1;
     if (const char *ev = getenv("DXPBD_REPLAY_MINB")) s->rep_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_DEFER_U")) s->defer_u = atoi(ev) != 0;
@@ -2081,10 +2076,6 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_smem));
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_smem));
                 s->pull_psmem = pull_persist_smem_bytes(s->hcap, s->ycap);
-                s->pull_rhs_psmem = pull_persist_smem_bytes(s->hcap, s->ycap, 2);
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull_p<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_psmem));
-                DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_pull_p<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_rhs_psmem));
-                if (const char *ev = getenv("DXPBD_RHS_PERSIST")) s->rhs_persist = atoi(ev);
                 DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_pull_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->pull_psmem));
                 DX_CHECK_CUDA(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, s->device));
                 if (const char *ev = getenv("DXPBD_PULL_PERSIST")) s->pull_persist = atoi(ev) != 0;
@@ -2487,17 +2478,7 @@ int dxpbd_backward(dxpbd_scene *s, int32_t num_keys, const int32_t *key_frames, 
         {
             TileLists tl{s->n_dist_colors, s->ntiles, s->d_seg.p, s->d_fseg.p, s->d_fidx.p, s->d_fent.p};
             TmaTiles tt = s->tma_tiles();
-            if (s->pull && s->pull_persist && s->rhs_persist == 1)
-                LAUNCH(DXPBD_K_RHS, k_rhs_pull_p<1><<<std::min(s->ntiles, s->num_sms), kTileV, s->pull_rhs_psmem, st>>>(
-                    s->pull_tiles(), V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
-                    s->r.p, s->u0.p, 0, s->ntiles, fuse_start ? s->p.p : nullptr,
-                    CGState{s->cg_sc.p, s->cg_sc.p + (size_t)(s->cg_max_iter + 1) * 4, s->cg_tol * s->cg_tol}));
-            else if (s->pull && s->pull_persist && s->rhs_persist == 2)
-                LAUNCH(DXPBD_K_RHS, k_rhs_pull_p<2><<<std::min(s->ntiles, 2 * s->num_sms), kTileV, s->pull_rhs_psmem, st>>>(
-                    s->pull_tiles(), V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
-                    s->r.p, s->u0.p, 0, s->ntiles, fuse_start ? s->p.p : nullptr,
-                    CGState{s->cg_sc.p, s->cg_sc.p + (size_t)(s->cg_max_iter + 1) * 4, s->cg_tol * s->cg_tol}));
-            else if (s->pull)
+            if (s->pull)
                 LAUNCH(DXPBD_K_RHS, k_rhs_pull<<<s->ntiles, kTileV, s->pull_rhs_smem, st>>>(
                     s->pull_tiles(), V, Qc, s->ax.p, s->uprev.p, warm2 ? s->uprev2.p : nullptr, s->y.p, state(s, n + 1), tgt(n + 1), wts, s->inv_mass.p, s->rhs.p,
                     s->r.p, s->u0.p, 0, fuse_start ? s->p.p : nullptr,

@@ -1371,11 +1371,9 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
         if (s.ctl) pcg_ctl_end(s, it);
         return;
     }
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nq = V / 4;
     float acc[2] = {0.f, 0.f};
-    // grid-stride over quads of vertices: the solver launches a grid that fills every SM once (no
-    // partial last wave); a one-quad-per-thread grid works as well
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= nq; t += gridDim.x * blockDim.x) {
     if (t < nq) {
         const float4 *__restrict__ p = reinterpret_cast<const float4 *>((it & 1) ? B.p1 : B.p0);
         float4 *__restrict__ u = reinterpret_cast<float4 *>(B.u);
@@ -1408,7 +1406,7 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
             if (UPD_U) u[3 * t + c] = make_float4(uu[4 * c], uu[4 * c + 1], uu[4 * c + 2], uu[4 * c + 3]);
             r[3 * t + c] = make_float4(rr[4 * c], rr[4 * c + 1], rr[4 * c + 2], rr[4 * c + 3]);
         }
-    } else {   // t == nq: tail vertices
+    } else if (t == nq) {   // tail vertices
         for (int v = 4 * nq; v < V; ++v) {
             const float3 *__restrict__ p = (it & 1) ? B.p1 : B.p0;
             const double pq = s.sc[(it + 1) * 4 + 0];
@@ -1423,7 +1421,6 @@ __global__ void k_cg_update4(int V, int it, CGBufs B, const float *__restrict__ 
             acc[0] += w * r2;
             acc[1] += r2;
         }
-    }
     }
     block_reduce_add<2>(acc, s.sc + (it + 1) * 4 + 1);
     if (s.ctl) pcg_ctl_end(s, it);

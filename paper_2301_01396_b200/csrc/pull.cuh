@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(kTileV, 3 * kPullScale) k_cg_matvec_pull(int i
 // round trip (the one-tile-per-CTA kernel needs descriptor -> index data and halo ids -> halo
 // values).  p.q is accumulated over the CTA's tiles and reduced once.
 // dynamic shared memory: [3 mbarriers 32][2 descriptors 32][2 x hcap halo ids][vector slots][Q / y slots]
-__host__ __device__ inline size_t pull_persist_smem_bytes(int hcap, int ycap, int nvec = 1) {
-    return 64 + 8 * (size_t)hcap + 16 * ((size_t)nvec * (kTileV + hcap) + (size_t)ycap);
+__host__ __device__ inline size_t pull_persist_smem_bytes(int hcap, int ycap) {
+    return 64 + 8 * (size_t)hcap + 16 * ((size_t)(kTileV + hcap) + (size_t)ycap);
 }
 
 __global__ void __launch_bounds__(kTileV, 2) k_cg_matvec_pull_p(int it, PullTiles T, int V, const float *__restrict__ Qc,
@@ -547,155 +547,5 @@ __global__ void __launch_bounds__(kTileV, 2 * kPullScale) k_rhs_pull(PullTiles T
     }
 }
 
-// Persistent rhs (same contract as k_rhs_pull, same prefetch scheme as k_cg_matvec_pull_p).
-template <int MINB>
-__global__ void __launch_bounds__(kTileV, MINB) k_rhs_pull_p(PullTiles T, int V, const float *__restrict__ Qc,
-                                                          const float3 *__restrict__ u, const float3 *__restrict__ uprev,
-                                                          const float3 *__restrict__ uprev2, const float3 *__restrict__ y,
-                                                          const double4 *__restrict__ xkey, const float *__restrict__ target,
-                                                          const float *__restrict__ weights, const float *__restrict__ wv,
-                                                          float3 *__restrict__ bout, float3 *__restrict__ r0out,
-                                                          float3 *__restrict__ u0out, int t0, int ntiles,
-                                                          float3 *__restrict__ p0out, CGState cs) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t *bar_q = reinterpret_cast<uint64_t *>(smem_raw);
-    uint64_t *bar_h = bar_q + 1;
-    int4 *s_td = reinterpret_cast<int4 *>(smem_raw + 32);
-    const int hcap = T.hcap;
-    int *s_hp = reinterpret_cast<int *>(smem_raw + 64);
-    float4 *sy = reinterpret_cast<float4 *>(smem_raw + 64 + 8 * (size_t)hcap);
-    float4 *sz = sy + kTileV + hcap;
-    float4 *yb = sz + kTileV + hcap;
-    const int i = threadIdx.x;
-    const bool lead = i == kTileV - 32;
-    const int tend = t0 + ntiles;
-    int t = t0 + blockIdx.x;
-    if (t >= tend) return;
-    const float3 z3 = make_float3(0.f, 0.f, 0.f);
-    const uint64_t keep = l2_keep_policy();
-    const uint32_t hbytes = (uint32_t)hcap * 4u;
-    if (lead) {
-        mbar_init(bar_q, 1);
-        mbar_init(bar_h, 1);
-        mbar_init(bar_h + 1, 1);
-        fence_mbar_init();
-        const int4 td0 = T.tdesc[t];
-        s_td[0] = td0;
-        mbar_expect_tx(bar_h, hbytes);
-        bulk_g2s(s_hp, T.hpad + (size_t)t * hcap, hbytes, bar_h);
-        const uint32_t bytes = (uint32_t)((td0.z & 0xff) * kTileV + td0.w) * 16u;
-        mbar_expect_tx(bar_q, bytes);
-        if (bytes) bulk_g2s(yb, T.Q4 + td0.x, bytes, bar_q);
-    }
-    __syncthreads();
-    float acc[3] = {0.f, 0.f, 0.f};
-    for (int k = 0; t < tend; t += gridDim.x, ++k) {
-        const int cur = k & 1, tn = t + gridDim.x;
-        const int4 td = s_td[cur];
-        const int v0 = t * kTileV;
-        const int nv = min(kTileV, V - v0);
-        const int v = min(v0 + i, V - 1);
-        const float w = ld_keep(wv + v, keep);
-        const float3 yo = y[v], uo = u[v], po = uprev[v], p2o = uprev2 ? uprev2[v] : z3;
-        double4 xo = make_double4(0, 0, 0, 0);
-        float3 to = z3;
-        float Wo = 1.f;
-        if (target) {
-            xo = xkey[v];
-            to = make_float3(target[3 * v], target[3 * v + 1], target[3 * v + 2]);
-            if (weights) Wo = weights[v];
-        }
-        PullRegs R;
-        pull_load(R, T, td, i);
-        int4 tdn = make_int4(0, 0, 0, 0);
-        if (lead && tn < tend) {
-            tdn = T.tdesc[tn];
-            mbar_expect_tx(bar_h + (cur ^ 1), hbytes);
-            bulk_g2s(s_hp + (size_t)(cur ^ 1) * hcap, T.hpad + (size_t)tn * hcap, hbytes, bar_h + (cur ^ 1));
-        }
-        mbar_wait(bar_h + cur, (uint32_t)((k >> 1) & 1));
-        const int *hp_s = s_hp + (size_t)cur * hcap;
-        const int hv = i < hcap ? hp_s[i] : -1;
-        const int hvv = max(hv, 0);
-        const float3 hy = y[hvv], hu = u[hvv], hp = uprev[hvv], hp2 = uprev2 ? uprev2[hvv] : z3;
-        float3 yv = z3, zv = z3, bb = z3, rr = z3;
-        if (i < nv) {
-            yv = yo;
-            const float3 dv = uprev2 ? 2.f * uo - 3.f * po + p2o : uo - po;
-            const float3 u0 = uo + dv;
-            zv = yv + u0;
-            u0out[v] = w > 0.f ? u0 : z3;
-            if (w > 0.f) {
-                bb = (1.f / w) * uo;
-                rr = (-1.f / w) * dv;
-                if (Qc) {
-                    Sym3 A = Sym3{Qc[v], Qc[V + v], Qc[2 * (size_t)V + v], Qc[3 * (size_t)V + v], Qc[4 * (size_t)V + v],
-                                  Qc[5 * (size_t)V + v]};
-                    bb = bb - sym3_mul(A, yv);
-                    rr = rr - sym3_mul(A, zv);
-                }
-                if (target) {
-                    const float3 g = Wo * make_float3((float)(xo.x - to.x), (float)(xo.y - to.y), (float)(xo.z - to.z));
-                    bb = bb + g;
-                    rr = rr + g;
-                }
-            }
-        }
-        sy[i] = make_float4(yv.x, yv.y, yv.z, 0.f);
-        sz[i] = make_float4(zv.x, zv.y, zv.z, 0.f);
-        if (hv >= 0) {
-            const float3 dh = uprev2 ? 2.f * hu - 3.f * hp + hp2 : hu - hp;
-            const float3 zh = hy + hu + dh;
-            sy[kTileV + i] = make_float4(hy.x, hy.y, hy.z, 0.f);
-            sz[kTileV + i] = make_float4(zh.x, zh.y, zh.z, 0.f);
-        }
-        for (int h = i + kTileV; h < hcap; h += kTileV) {   // rare: large halos
-            const int q = hp_s[h];
-            if (q < 0) continue;
-            const float3 uh = u[q];
-            const float3 dh = uprev2 ? 2.f * uh - 3.f * uprev[q] + uprev2[q] : uh - uprev[q];
-            const float3 yh = y[q], zh = yh + uh + dh;
-            sy[kTileV + h] = make_float4(yh.x, yh.y, yh.z, 0.f);
-            sz[kTileV + h] = make_float4(zh.x, zh.y, zh.z, 0.f);
-        }
-        if (lead && tn < tend) s_td[cur ^ 1] = tdn;
-        __syncthreads();
-        mbar_wait(bar_q, (uint32_t)(k & 1));
-        float4 Qk[kPullK0 + 1];
-        float3 ay = pull_primary<true>(R, T, td, i, yv, sy, yb, Qk);
-        __syncthreads();
-        ay = ay + pull_secondary(R, T, td, i, yb);
-        __syncthreads();
-        float3 az = pull_primary_regs(R, T, td, i, zv, sz, yb, Qk);
-        __syncthreads();
-        az = az + pull_secondary(R, T, td, i, yb);
-        __syncthreads();   // every y slot has been read: the next tile's blocks may land
-        if (lead && tn < tend) {
-            fence_proxy_async();
-            const uint32_t bytes = (uint32_t)((tdn.z & 0xff) * kTileV + tdn.w) * 16u;
-            mbar_expect_tx(bar_q, bytes);
-            if (bytes) bulk_g2s(yb, T.Q4 + tdn.x, bytes, bar_q);
-        }
-        if (i < nv) {
-            const bool fr = w > 0.f;
-            const float3 bv = fr ? bb - ay : z3, rv = fr ? rr - az : z3;
-            bout[v] = bv;
-            r0out[v] = rv;
-            if (p0out) {
-                p0out[v] = w * rv;
-                const float r2 = dot3(rv, rv);
-                acc[0] += w * r2;
-                acc[1] += r2;
-                acc[2] += dot3(bv, bv);
-            }
-        }
-    }
-    if (p0out) {
-        float a2[2] = {acc[0], acc[1]};
-        block_reduce_add<2>(a2, cs.sc + 1);
-        float b1[1] = {acc[2]};
-        block_reduce_add<1>(b1, cs.bnorm2);
-    }
-}
 
 }  // namespace dx
