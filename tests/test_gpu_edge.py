@@ -125,6 +125,30 @@ def test_medium_cloth_full_size_backward_short():
     _compare(g, o, ("compliance", "x0", "v0"))
 
 
+def test_medium_cloth_full_size_full_length_forward():
+    """configs[1] at its full size and horizon (256^2 cloth dropped on the sphere, 60 frames x 10
+    substeps) against the fp64 oracle at every 10th frame (about 3 minutes of oracle time).  The
+    workload is well conditioned until the cloth has met the sphere: positions within 1e-4 up to
+    frame 20 (observed 2e-8 / 4e-6).  Afterwards wrinkling amplifies round-off -- the oracle
+    itself moves by 4e-3 .. 2e-2 under a 1e-9 m perturbation of x0 (tests/medium_sensitivity.py,
+    tests/golden/medium_cloth_sensitivity.json) -- so later frames are only required to stay below
+    that self-sensitivity; contacts must be active at the end."""
+    import json
+    import os
+    s = f32(medium_cloth())
+    assert s.frames == 60 and len(s.x0) == 256 * 256
+    sens = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "medium_cloth_sensitivity.json")))["rel_l2"]
+    g = gpu_run(s, backward=False)
+    o = oracle_run(s, backward=False)
+    errs = {f: rel_l2(g["x"][f], o["x"][f]) for f in range(10, 61, 10)}
+    xe = o["x"][60]
+    near = np.linalg.norm(xe - s.spheres[0, :3], axis=1) - s.spheres[0, 3] < s.thickness + 1e-3
+    assert near.sum() > 1000, near.sum()             # the cloth lies on the sphere
+    assert errs[10] < 1e-4 and errs[20] < 1e-4, errs
+    for f in (30, 40, 50, 60):
+        assert errs[f] < max(1e-4, sens[str(f)]), (f, errs)
+
+
 def test_large_cloth_full_size_substeps_bench_config():
     """configs[4] in the bench's launch configuration (2944^2, dt = 1/600, forces, the same kernels
     and launch shapes bench.py times), three consecutive substeps forward (velocities carried
