@@ -994,7 +994,6 @@ struct dxpbd_scene {
     int poll_extra = 0;                                // iterations launched beyond last_iters before the first poll
     bool tetv = true;                                  // no distance constraints: 2-launch PCG iteration (k_cg_tetv)
     int tetv_minb = 1;                                 // its launch-bounds CTAs per SM
-    int mv_minb = 4;                                   // TMA matvec: launch-bounds CTAs per SM (A/B: DXPBD_MV_MINB)
     float psd_tol = 1e-6f;                             // tet PD projection: Jacobi stop (off-diagonal / scale)
     int psd_sweeps = 12;                               // and sweep cap
     int psd_minb = 3;                                  // its launch-bounds CTAs per SM (measured best)
@@ -1747,12 +1746,8 @@ int pcg_solve(dxpbd_scene *s, cudaStream_t st, int &iters_out, double &relres_ou
             else
                 LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_pull<<<s->ntiles, kTileV, s->pull_smem, st>>>(it, pt, V, Qc, bufs, xw, cs, 0, uf)));
         } else if (s->use_tma) {
-            if (s->mv_minb == 3)
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<kMvThreads, kMvMinB - 1><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
-                                                                                                         defer ? s->ax.p : nullptr)));
-            else
-                LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<kMvThreads, kMvMinB><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
-                                                                                                         defer ? s->ax.p : nullptr)));
+            LAUNCH(DXPBD_K_CG_DIST, (k_cg_matvec_tma<kMvThreads, kMvMinB><<<s->ntiles, kMvThreads, s->tma_smem, st>>>(it, tt, V, Qc, bufs, xw, cs, 0,
+                                                                                                     defer ? s->ax.p : nullptr)));
         } else if (s->qf == 1)
             LAUNCH(DXPBD_K_CG_DIST, k_cg_matvec<1><<<s->ntiles, kBlock, 0, st>>>(it, tl, V, s->d_idx.p, s->Qd.p, E, Qc, bufs, xw, cs));
         else
@@ -2003,7 +1998,6 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
     if (const char *ev = getenv("DXPBD_PSD_TOL")) s->psd_tol = (float)atof(ev);
     if (const char *ev = getenv("DXPBD_PSD_SWEEPS")) s->psd_sweeps = atoi(ev);
     if (const char *ev = getenv("DXPBD_PSD_MINB")) s->psd_minb = atoi(ev);
-    if (const char *ev = getenv("DXPBD_MV_MINB")) s->mv_minb = atoi(ev);
     if (const char *ev = getenv("DXPBD_OVERLAP")) s->overlap = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_QCACHE")) s->qcache_on = atoi(ev) != 0;
     if (const char *ev = getenv("DXPBD_POLL_EXTRA")) s->poll_extra = atoi(ev);
@@ -2098,7 +2092,6 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
             s->tma_smem = tma_smem_bytes(s->hcap, s->capm, s->qf == 0);
             s->tma_rhs_smem = tma_rhs_smem_bytes(s->hcap, s->capm, s->qf == 0);
             DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
-            DX_CHECK_CUDA(cudaFuncSetAttribute(k_cg_matvec_tma<kMvThreads, kMvMinB - 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_smem));
             DX_CHECK_CUDA(cudaFuncSetAttribute(k_rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->tma_rhs_smem));
         }
         s->d_fidx.alloc(topo.fidx.size());
