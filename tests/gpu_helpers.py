@@ -56,3 +56,25 @@ def oracle_run(scene, frames=None, pd=True, backward=True, solver="direct"):
 
 def f32(scene):
     return as_float32_exact(scene)
+
+
+def random_network(V=1100, k=8, seed=5):
+    """An irregular spring network (not a lattice): every vertex tied to k random others among its 60
+    nearest neighbours in a unit cube (mean degree 2k), a few pinned vertices."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0.0, 1.0, size=(V, 3))
+    pairs = set()
+    for i in range(V):
+        near = np.argsort(((x - x[i]) ** 2).sum(1))[1:61]
+        for j in rng.choice(near, size=k, replace=False):
+            pairs.add((min(i, int(j)), max(i, int(j))))
+    idx = np.array(sorted(pairs), np.int32)
+    w = np.full(V, 1000.0)
+    w[rng.choice(V, size=12, replace=False)] = 0.0
+    from synth import Scene
+    from synth.scenes import _base
+    d = _base("network", V, x_rest=x, x0=x + 0.004 * rng.standard_normal(x.shape) * (w > 0)[:, None], inv_mass=w,
+              dist_idx=idx, dist_compliance=10.0 ** rng.uniform(-8, -6, len(idx)))
+    tgt = x + 0.02 * rng.standard_normal(x.shape)
+    return Scene(**d, frame_dt=1 / 60, substeps=4, iterations=1, frames=2, key_frames=np.array([2], np.int32),
+                 targets=tgt[None])

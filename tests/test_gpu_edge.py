@@ -6,7 +6,7 @@ import pytest
 
 from synth import Scene, tiny_cloth, large_cloth, garment, medium_cloth
 from synth.scenes import _base
-from tests.gpu_helpers import f32, gpu_run, oracle_run, rel_l2
+from tests.gpu_helpers import f32, gpu_run, oracle_run, random_network, rel_l2
 from tests.test_gpu_cloth import _compare
 
 pytestmark = pytest.mark.gpu
@@ -27,6 +27,22 @@ def test_contacts_only_no_constraints():
     g = gpu_run(s, ("sphere",))
     o = oracle_run(s)
     _compare(g, o, ("sphere", "x0", "v0"))
+
+
+def test_irregular_network_pull_layout_tails():
+    """An irregular mesh of mean degree 16 (several tiles, large halos): the pull layout needs more than
+    kTileV overflow entries per tile and more than 8 secondaries per vertex (the kernels' in-loop tail
+    paths), checked on the host-only layout; positions and gradients against the oracle."""
+    api = _api()
+    s = f32(random_network())
+    L = api.dxpbd_pull_layout(**api.scene_kwargs(s))
+    assert L["tiles"] >= 2
+    assert int(L["tdesc"][:, 3].max()) > L["tile_v"]                 # overflow entries beyond one per thread
+    assert int((L["tdesc"][:, 2] >> 8).max()) > 4                   # secondary pairs beyond the 4 held in registers
+    g = gpu_run(s, ("compliance",))
+    assert g["stats"]["pull"]
+    o = oracle_run(s)
+    _compare(g, o, ("compliance", "x0", "v0"))
 
 
 def test_zero_keyframes_and_keyframe_at_frame0():

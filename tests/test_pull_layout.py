@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from synth import garment, large_cloth, medium_cloth, tiny_cloth
+from tests.gpu_helpers import random_network
 
 
 def _layout(s):
@@ -21,6 +22,7 @@ def _cases():
         ("cloth_ragged", lambda: large_cloth(n=75, frames=1, side=10.0 * 74 / 2943.0, key_frames=(1,))),
         ("sphere48", lambda: medium_cloth(n=48, frames=1)),
         ("garment_tube", lambda: garment(n_around=64, n_along=48, frames=1)),
+        ("random_network", lambda: random_network()),   # irregular, degree 16: overflow > kTileV, > 8 secondaries
     ]
 
 
@@ -83,7 +85,7 @@ def _emulate(L, Q_user, p):
     return out, written
 
 
-@pytest.mark.parametrize("case", range(5))
+@pytest.mark.parametrize("case", range(6))
 def test_pull_layout_reproduces_the_constraint_sum(case):
     name, mk = _cases()[case]
     s = mk()
