@@ -899,6 +899,10 @@ struct dxpbd_scene {
     bool pull = false;
     int ycap = 0;
     bool pull_persist = true;   // persistent matvec CTAs with next-tile prefetch (A/B: DXPBD_PULL_PERSIST)
+    // prediction fused into the first distance color of a K = 1 sweep (k_dist_first); the vertices no
+    // color-0 constraint touches are predicted from this list (DXPBD_FUSE_PREDICT)
+    bool fuse_predict = false;
+    DBuf<int> uncov;
     size_t pull_psmem = 0;
     int num_sms = 148;
     size_t pull_smem = 0, pull_rhs_smem = 0;
@@ -1316,7 +1320,12 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
             WaveDist dd{s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, s->E, nullptr, nullptr, nullptr, nullptr, nullptr};
             LAUNCH(DXPBD_K_DIST_PROJECT, (launch_wave<false, true>(s, 0, s->wave_grid_fwd, pr, dd, xo, st)));
         }
-    } else {
+    }
+    const PredictArgs pa{state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f, s->dtd, 1.0 / s->dtd, s->gravity};
+    const bool fuse = s->fuse_predict && !wave && !graph && K == 1;
+    if (fuse) {
+        if (s->uncov.n) LAUNCH(DXPBD_K_PREDICT, k_predict_list<<<nblk((int)s->uncov.n), kBlock, 0, st>>>((int)s->uncov.n, s->uncov.p, pa, xo));
+    } else if (!wave) {
         LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
                                                                        s->dtd, 1.0 / s->dtd, s->gravity, xo));
     }
@@ -1327,7 +1336,14 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
         for (int c = 0; c < (wave ? 0 : s->n_dist_colors); ++c) {
             int b = s->dist_off[c], cnt = s->dist_off[c + 1] - b;
             if (!cnt) continue;
-            if (!rd && !wr && s->qc_count && n >= s->qc_first) {
+            if (fuse && c == 0 && s->qc_count && n >= s->qc_first) {
+                float4 *slot = s->qcache.p + (size_t)(n - s->qc_first) * s->d_Qt.n;
+                LAUNCH(DXPBD_K_DIST_PROJECT, (k_dist_first<true, 3><<<nblk(cnt), kBlock, 0, st>>>(
+                    b, cnt, s->E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, pa, slot, nullptr, xo, s->d_tpos.p, s->d_fpos.p, slot)));
+            } else if (fuse && c == 0) {
+                LAUNCH(DXPBD_K_DIST_PROJECT, (k_dist_first<false, 4><<<nblk(cnt), kBlock, 0, st>>>(
+                    b, cnt, s->E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, pa, nullptr, nullptr, xo, nullptr, nullptr, nullptr)));
+            } else if (!rd && !wr && s->qc_count && n >= s->qc_first) {
                 // cached substep: the replay kernel (same iterates bit for bit) also stores Q_n
                 float4 *slot = s->qcache.p + (size_t)(n - s->qc_first) * s->d_Qt.n;
                 LAUNCH(DXPBD_K_DIST_PROJECT, (k_dist_replay1<2, 3><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
@@ -1424,7 +1440,12 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st, int stage = 0) {
             LAUNCH(DXPBD_K_DIST_REPLAY, (launch_wave<true, false>(s, 1, s->wave_grid_rep, pr, dd, x, st)));
         else
             LAUNCH(DXPBD_K_DIST_REPLAY, (launch_wave<true, true>(s, 1, s->wave_grid_rep, pr, dd, x, st)));
-    } else {
+    }
+    const PredictArgs pa{state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f, s->dtd, 1.0 / s->dtd, s->gravity};
+    const bool fuse = s->fuse_predict && !wave && !sweep_graph_on(s) && K == 1 && s->qf == 1;
+    if (fuse) {
+        if (s->uncov.n) LAUNCH(DXPBD_K_PREDICT, k_predict_list<<<nblk((int)s->uncov.n), kBlock, 0, st>>>((int)s->uncov.n, s->uncov.p, pa, x));
+    } else if (!wave) {
         LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
                                                                        s->dtd, 1.0 / s->dtd, s->gravity, x));
     }
@@ -1440,7 +1461,12 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st, int stage = 0) {
             if (!cnt) continue;
             float *eo = want_e ? s->ed.p : nullptr;
             const bool last_color = c == s->n_dist_colors - 1 && !s->T && !s->NC;   // nothing reads its iterate
-            if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3 && last_color)
+            if (fuse && c == 0)
+                LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_first<true, 3><<<nblk(cnt), kBlock, 0, st>>>(
+                    b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2, pa,
+                    s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
+                    s->use_tma ? s->d_tpos.p : nullptr, s->use_tma ? s->d_fpos.p : nullptr, qtw)));
+            else if (first && last && s->qf == 1 && s->nb_rep == 2 && s->rep_minb == 3 && last_color)
                 LAUNCH(DXPBD_K_DIST_REPLAY, (k_dist_replay1<2, 3, false><<<nblk((cnt + 1) / 2), kBlock, 0, st>>>(
                     b, cnt, E, s->d_idx.p, s->d_rest.p, s->d_alpha.p, inv_dt2,
                     s->use_tma ? qtw : reinterpret_cast<float4 *>(s->Qd.p), eo, x,
@@ -2106,6 +2132,19 @@ int dxpbd_create(const dxpbd_scene_desc *d, dxpbd_scene **out) {
         upload(alpha_u.p, d->dist_compliance, sizeof(float) * E, DXPBD_MEM_HOST, st);
         s->d_perm.alloc(E);
         upload(s->d_perm.p, s->dist_perm_h.data(), sizeof(int32_t) * E, DXPBD_MEM_HOST, st);
+        {   // vertices no color-0 constraint touches (prediction fused into the first color, k_dist_first)
+            std::vector<char> cov(V, 0);
+            for (int q = s->dist_off[0]; q < s->dist_off[1]; ++q) { cov[ab_sorted[q].x] = 1; cov[ab_sorted[q].y] = 1; }
+            std::vector<int> un;
+            for (int v = 0; v < V; ++v)
+                if (!cov[v]) un.push_back(v);
+            const char *ev = getenv("DXPBD_FUSE_PREDICT");
+            s->fuse_predict = nc >= 2 && s->iterations == 1 && (int64_t)un.size() * 4 <= V && !(ev && atoi(ev) == 0);
+            if (s->fuse_predict && !un.empty()) {
+                s->uncov.alloc(un.size());
+                upload(s->uncov.p, un.data(), sizeof(int) * un.size(), DXPBD_MEM_HOST, st);
+            }
+        }
         s->d_idx.alloc(E + 2);   // +2: the bulk copies round segment ends up to 16 bytes
         DX_CHECK_CUDA(cudaMemsetAsync(s->d_idx.p, 0, sizeof(int2) * (E + 2), st));
         upload(s->d_idx.p, ab_sorted.data(), sizeof(int2) * E, DXPBD_MEM_HOST, st);

@@ -243,6 +243,66 @@ __global__ void __launch_bounds__(kBlock, MINB) k_dist_replay1(int begin, int co
     }
 }
 
+// Prediction fused into the first color of a K = 1 sweep: a color is vertex-disjoint, so the
+// constraint's thread predicts its two endpoints itself (predict_one, the arithmetic of k_predict)
+// instead of reading the x~ a separate pass stored -- one write and one read of the fp64 state less
+// per substep, bit-identical iterates.  Vertices no color-0 constraint touches are predicted by
+// k_predict_list.  Forward (REPLAY = false) and replay / block-caching forward (REPLAY = true, the
+// arithmetic of k_dist_replay1).
+struct PredictArgs {
+    const double4 *xn, *xprev;
+    const float4 *v0;
+    const float *f;
+    double dt, inv_dt;
+    float3 g;
+};
+__global__ void k_predict_list(int n, const int *__restrict__ ids, PredictArgs P, double4 *__restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int i = ids[k];
+    out[i] = predict_one(i, P.xn, P.xprev, P.v0, P.f, P.dt, P.inv_dt, P.g);
+}
+template <bool REPLAY, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_dist_first(int begin, int count, int E, const int2 *__restrict__ idx,
+                                                             const float *__restrict__ rest,
+                                                             const float *__restrict__ alpha, float inv_dt2,
+                                                             PredictArgs P, float4 *__restrict__ Q4,
+                                                             float *__restrict__ eout, double4 *__restrict__ x,
+                                                             const int *__restrict__ tpos,
+                                                             const int *__restrict__ fpos, float4 *__restrict__ fQ) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const int j = begin + t;
+    const int2 e = idx[j];
+    const float rs = rest[j], al = alpha[j];
+    int tp = j, fp = -1;
+    if (REPLAY) {
+        if (tpos) tp = tpos[j];
+        if (fpos) fp = fpos[j];
+    }
+    double4 pa = predict_one(e.x, P.xn, P.xprev, P.v0, P.f, P.dt, P.inv_dt, P.g);
+    double4 pb = predict_one(e.y, P.xn, P.xprev, P.v0, P.f, P.dt, P.inv_dt, P.g);
+    const float at = rmul(al, inv_dt2);
+    DistCore o;
+    const bool ok = dist_core(pa, pb, rs, at, 0.f, o);
+    if (REPLAY) {
+        float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float3 ec = make_float3(0.f, 0.f, 0.f);
+        if (ok) {
+            q4 = qpack_iso_rank1(o.n, o.dl, (float)(1.0 / o.len), o.J);
+            const float iJ = 1.f / o.J;
+            const float tt = (-(0.f + o.dl) * inv_dt2 - at * 0.f) * iJ;
+            ec = ec + tt * o.n;
+        }
+        Q4[tp] = q4;
+        if (fp >= 0) fQ[fp] = q4;
+        if (eout) { eout[j] = ec.x; eout[E + j] = ec.y; eout[2 * E + j] = ec.z; }
+    }
+    if (ok) dist_apply(pa, pb, o);
+    x[e.x] = pa;
+    x[e.y] = pb;
+}
+
 template <bool FIRST, bool LAST, int QF = 0>
 __global__ void __launch_bounds__(kBlock) k_dist_replay(int begin, int count, int E, const int2 *__restrict__ idx,
                                                         const float *__restrict__ rest,

@@ -305,6 +305,29 @@ def test_wave_sweep_bit_identical(monkeypatch, case):
 
 
 @pytest.mark.parametrize("case", range(4))
+def test_fused_predict_bit_identical(monkeypatch, case):
+    """Prediction fused into the first distance color (k_dist_first: forward, block-caching forward
+    and replay; large scenes, or any scene with the sweep graphs off) reproduces the separate
+    prediction pass bit for bit: positions of every frame, loss and every gradient, with and
+    without the forward's block cache."""
+    name, mk, grads = _wave_cases()[case]
+    s = mk()
+    frames = s.frames
+    monkeypatch.setenv("DXPBD_SWEEP_GRAPH", "0")
+    monkeypatch.setenv("DXPBD_FUSE_PREDICT", "0")
+    xa, la, ga, _ = _run_all(s, grads, frames)
+    monkeypatch.setenv("DXPBD_FUSE_PREDICT", "1")
+    for qcache in ("1", "0"):
+        monkeypatch.setenv("DXPBD_QCACHE", qcache)
+        xb, lb, gb, _ = _run_all(s, grads, frames)
+        for f in range(frames + 1):
+            np.testing.assert_array_equal(xa[f], xb[f], err_msg=f"{name} qcache={qcache} frame {f}")
+        assert la == lb, (name, qcache)
+        for k in grads:
+            np.testing.assert_array_equal(ga[k], gb[k], err_msg=f"{name} qcache={qcache} {k}")
+
+
+@pytest.mark.parametrize("case", range(4))
 def test_pull_matvec_matches_push(monkeypatch, case):
     """The pull-style PCG kernels (pull.cuh: one vertex per thread, persistent and one tile per CTA)
     solve the same systems as the push kernels (k_cg_matvec_tma / k_rhs_tma): identical positions,

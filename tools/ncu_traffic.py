@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 from bench import TRAFFIC_JSON, src_hash  # noqa: E402
 
 CLASS_OF = {"k_cg_matvec_pull_p": "cg_dist", "k_cg_matvec_pull": "cg_dist", "k_rhs_pull": "rhs", "k_cg_matvec_tma": "cg_dist", "k_rhs_tma": "rhs", "k_cg_update4": "cg_update",
-            "k_dist_project1": "dist_project", "k_dist_replay1": "dist_replay", "k_predict": "predict",
+            "k_dist_project1": "dist_project", "k_dist_first": "dist_first", "k_dist_replay1": "dist_replay", "k_predict": "predict",
             "k_wave_project": "dist_project", "k_wave_replay": "dist_replay", "k_cg_tetv": "cg_tet",
             "k_tet_psd": "tet_replay"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
