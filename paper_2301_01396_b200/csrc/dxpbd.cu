@@ -1325,6 +1325,7 @@ int forward_substep(dxpbd_scene *s, int n, cudaStream_t st) {
     const bool fuse = s->fuse_predict && !wave && !graph && K == 1;
     if (fuse) {
         if (s->uncov.n) LAUNCH(DXPBD_K_PREDICT, k_predict_list<<<nblk((int)s->uncov.n), kBlock, 0, st>>>((int)s->uncov.n, s->uncov.p, pa, xo));
+        else launches = 0;   // no prediction launch at all
     } else if (!wave) {
         LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
                                                                        s->dtd, 1.0 / s->dtd, s->gravity, xo));
@@ -1445,6 +1446,7 @@ int replay_substep(dxpbd_scene *s, int n, cudaStream_t st, int stage = 0) {
     const bool fuse = s->fuse_predict && !wave && !sweep_graph_on(s) && K == 1 && s->qf == 1;
     if (fuse) {
         if (s->uncov.n) LAUNCH(DXPBD_K_PREDICT, k_predict_list<<<nblk((int)s->uncov.n), kBlock, 0, st>>>((int)s->uncov.n, s->uncov.p, pa, x));
+        else launches = 0;   // no prediction launch at all
     } else if (!wave) {
         LAUNCH(DXPBD_K_PREDICT, k_predict<<<nblk(V), kBlock, 0, st>>>(V, state(s, n), n > 0 ? state(s, n - 1) : nullptr, s->v0.p, f,
                                                                        s->dtd, 1.0 / s->dtd, s->gravity, x));
